@@ -1,0 +1,168 @@
+// Instruction-issue microbenchmark for sm_100a: measures sustained thread-instructions per clock per SM
+// for the integer/half2/DPX/shuffle ops the alignment kernels are built from, alone and in mixes.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o ubench ubench.cu
+// This pins the roofline constants. Not part of the product path.
+#include <cuda_fp16.h>
+#include <cstdint>
+#include <cstdio>
+#include <vector>
+#include <string>
+
+#define CHAINS 8
+#define INNER 32
+#define OUTER 256
+
+#define BAR(x) asm volatile("" : "+r"(x))
+
+enum Op { OP_IADD3, OP_IMAD, OP_LOP3, OP_PRMT, OP_IMNMX, OP_VIMNMX3, OP_VIADDMNMX, OP_VIADDMNMX_RELU,
+          OP_VIMNMX_S16X2, OP_VIMNMX3_S16X2, OP_VIADDMNMX_S16X2, OP_VIADDMNMX_S16X2_RELU, OP_VIADD_16X2,
+          OP_HMNMX2, OP_VHMNMX, OP_HADD2, OP_HFMA2, OP_HFMA2_RELU, OP_HSET2, OP_FMNMX, OP_FMNMX3, OP_FADD, OP_FFMA,
+          OP_SHFL_UP, OP_SHFL_UP8, OP_LDS, OP_VCMPEQ2ISH,
+          // mixes (two or more ops per chain step)
+          MIX_VIMNMX16_HFMA2, MIX_HMNMX2_HFMA2, MIX_VIADDMNMX16_IMAD, MIX_HMNMX2_VIMNMX16, MIX_VIMNMX16_VIADD16,
+          MIX_PRMT_VIMNMX16, MIX_PRMT_HFMA2, MIX_IMNMX_IMAD, MIX_HMNMX2_HADD2_SHFL, MIX_VIMNMX16_IMAD,
+          MIX_HSET2_HFMA2, MIX_HSET2_HMNMX2, MIX_CELL_DPX, MIX_CELL_H2, MIX_VIADD16_IMAD, MIX_LDS_VIMNMX16,
+          MIX_SHFL_VIMNMX16, MIX_IADD3_IMAD, MIX_LOP3_IMAD, OP_COUNT };
+
+static const char* names[] = {"IADD3","IMAD","LOP3","PRMT","IMNMX(VIMNMX.S32)","VIMNMX3","VIADDMNMX","VIADDMNMX.RELU",
+  "VIMNMX.S16x2","VIMNMX3.S16x2","VIADDMNMX.S16x2","VIADDMNMX.S16x2.RELU","VIADD.16x2",
+  "HMNMX2(alt max/min)","VHMNMX(2 h2max fused)","HADD2","HFMA2","HFMA2.RELU","HSET2.BF.EQ","FMNMX","FMNMX3","FADD","FFMA",
+  "SHFL.UP(w32)","SHFL.UP(w8)","LDS.32","LOP3+VIMNMX.U16x2(eq-ish)",
+  "mix VIMNMX16+HFMA2","mix HMNMX2+HFMA2","mix VIADDMNMX16+IMAD","mix HMNMX2+VIMNMX16","mix VIMNMX16+VIADD16",
+  "mix PRMT+VIMNMX16","mix PRMT+HFMA2","mix IMNMX+IMAD","mix 4xHMNMX2+4xHADD2+1SHFL(per 9)","mix VIMNMX16+IMAD",
+  "mix HSET2+HFMA2","mix HSET2+HMNMX2","mix DPX cell(PRMT,2VIMNMX,VIADDMNMX,VIADD,VIADDMNMX.RELU)","mix H2 cell(HSET2,HFMA2.RELU,4HMNMX2,3HADD2)",
+  "mix VIADD16+IMAD","mix LDS+3xVIMNMX16","mix SHFL+7xVIMNMX16","mix IADD3+IMAD","mix LOP3+IMAD"};
+// instructions counted per chain step
+static const int per_step[] = {1,1,1,1,1,1,1,1, 1,1,1,1,1, 1,1,1,1,1,1,1,1,1,1, 1,1,1,2,
+  2,2,2,2,2, 2,2,2,9,2, 2,2,6,9, 2,4,8,2,2};
+
+__device__ __forceinline__ uint32_t h2max(uint32_t a, uint32_t b){ uint32_t d; asm volatile("max.f16x2 %0,%1,%2;" : "=r"(d) : "r"(a),"r"(b)); return d; }
+__device__ __forceinline__ uint32_t h2add(uint32_t a, uint32_t b){ uint32_t d; asm volatile("add.f16x2 %0,%1,%2;" : "=r"(d) : "r"(a),"r"(b)); return d; }
+__device__ __forceinline__ uint32_t h2fma(uint32_t a, uint32_t b, uint32_t c){ uint32_t d; asm volatile("fma.rn.f16x2 %0,%1,%2,%3;" : "=r"(d) : "r"(a),"r"(b),"r"(c)); return d; }
+__device__ __forceinline__ uint32_t h2fmarelu(uint32_t a, uint32_t b, uint32_t c){ uint32_t d; asm volatile("fma.rn.relu.f16x2 %0,%1,%2,%3;" : "=r"(d) : "r"(a),"r"(b),"r"(c)); return d; }
+__device__ __forceinline__ uint32_t h2seteq(uint32_t a, uint32_t b){ uint32_t d; asm volatile("set.eq.f16x2.f16x2 %0,%1,%2;" : "=r"(d) : "r"(a),"r"(b)); return d; }
+
+template <int OP>
+__global__ void __launch_bounds__(1024, 1) bench(uint32_t* out, const uint32_t* in, long long* cyc) {
+  __shared__ uint32_t sm[1024];
+  uint32_t x[CHAINS];
+  uint32_t y = in[0] + threadIdx.x, z = in[1], w = in[2];
+#pragma unroll
+  for (int j = 0; j < CHAINS; ++j) x[j] = in[3 + j] ^ threadIdx.x;
+  sm[threadIdx.x] = y;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int o = 0; o < OUTER; ++o) {
+#pragma unroll
+    for (int i = 0; i < INNER; ++i) {
+#pragma unroll
+      for (int j = 0; j < CHAINS; ++j) {
+        uint32_t v = x[j];
+        if (OP == OP_IADD3) { asm volatile("add.s32 %0,%0,%1;" : "+r"(v) : "r"(y)); }
+        else if (OP == OP_IMAD) { asm volatile("mad.lo.s32 %0,%0,%1,%2;" : "+r"(v) : "r"(y),"r"(z)); }
+        else if (OP == OP_LOP3) { asm volatile("lop3.b32 %0,%0,%1,%2,0x96;" : "+r"(v) : "r"(y),"r"(z)); }
+        else if (OP == OP_PRMT) { asm volatile("prmt.b32 %0,%1,%2,%0;" : "+r"(v) : "r"(y),"r"(z)); }
+        else if (OP == OP_IMNMX) { if (i & 1) asm volatile("max.s32 %0,%0,%1;" : "+r"(v) : "r"(y)); else asm volatile("min.s32 %0,%0,%1;" : "+r"(v) : "r"(z)); }
+        else if (OP == OP_VIMNMX3) { v = __vimax3_s32((int)v,(int)y,(int)z); BAR(v); }
+        else if (OP == OP_VIADDMNMX) { v = __viaddmax_s32((int)v,(int)y,(int)z); BAR(v); }
+        else if (OP == OP_VIADDMNMX_RELU) { v = __viaddmax_s32_relu((int)v,(int)y,(int)z); BAR(v); }
+        else if (OP == OP_VIMNMX_S16X2) { v = __vmaxs2(v,y); BAR(v); }
+        else if (OP == OP_VIMNMX3_S16X2) { v = __vimax3_s16x2(v,y,z); BAR(v); }
+        else if (OP == OP_VIADDMNMX_S16X2) { v = __viaddmax_s16x2(v,y,z); BAR(v); }
+        else if (OP == OP_VIADDMNMX_S16X2_RELU) { v = __viaddmax_s16x2_relu(v,y,z); BAR(v); }
+        else if (OP == OP_VIADD_16X2) { v = __vadd2(v,y); BAR(v); }
+        else if (OP == OP_HMNMX2) { if (i & 1) v = h2max(v,y); else asm volatile("min.f16x2 %0,%0,%1;" : "+r"(v) : "r"(z)); }
+        else if (OP == OP_VHMNMX) { v = h2max(v,y); v = h2max(v,z); }
+        else if (OP == OP_HADD2) { v = h2add(v,y); }
+        else if (OP == OP_HFMA2) { v = h2fma(v,y,z); }
+        else if (OP == OP_HFMA2_RELU) { v = h2fmarelu(v,y,z); }
+        else if (OP == OP_HSET2) { v = h2seteq(v,y); }
+        else if (OP == OP_FMNMX) { if (i & 1) asm volatile("max.f32 %0,%0,%1;" : "+f"(*(float*)&v) : "f"(*(float*)&y)); else asm volatile("min.f32 %0,%0,%1;" : "+f"(*(float*)&v) : "f"(*(float*)&z)); }
+        else if (OP == OP_FMNMX3) { asm volatile("max.f32 %0,%0,%1,%2;" : "+f"(*(float*)&v) : "f"(*(float*)&y),"f"(*(float*)&z)); }
+        else if (OP == OP_FADD) { asm volatile("add.f32 %0,%0,%1;" : "+f"(*(float*)&v) : "f"(*(float*)&y)); }
+        else if (OP == OP_FFMA) { asm volatile("fma.rn.f32 %0,%0,%1,%2;" : "+f"(*(float*)&v) : "f"(*(float*)&y),"f"(*(float*)&z)); }
+        else if (OP == OP_SHFL_UP) { v = __shfl_up_sync(0xffffffffu, v, 1, 32); BAR(v); }
+        else if (OP == OP_SHFL_UP8) { v = __shfl_up_sync(0xffffffffu, v, 1, 8); BAR(v); }
+        else if (OP == OP_LDS) { v = sm[v & 1023]; BAR(v); }
+        else if (OP == OP_VCMPEQ2ISH) { uint32_t t; asm volatile("lop3.b32 %0,%1,%2,%3,0x80;" : "=r"(t) : "r"(v),"r"(y),"r"(z)); v = __vminu2(t, w); BAR(v); }
+        else if (OP == MIX_VIMNMX16_HFMA2) { v = __vmaxs2(v,y); BAR(v); v = h2fma(v,y,z); }
+        else if (OP == MIX_HMNMX2_HFMA2) { v = h2max(v,y); v = h2fma(v,y,z); }
+        else if (OP == MIX_VIADDMNMX16_IMAD) { v = __viaddmax_s16x2(v,y,z); BAR(v); asm volatile("mad.lo.s32 %0,%0,%1,%2;" : "+r"(v) : "r"(y),"r"(z)); }
+        else if (OP == MIX_HMNMX2_VIMNMX16) { v = h2max(v,y); v = __vmaxs2(v,z); BAR(v); }
+        else if (OP == MIX_VIMNMX16_VIADD16) { v = __vmaxs2(v,y); BAR(v); v = __vadd2(v,z); BAR(v); }
+        else if (OP == MIX_PRMT_VIMNMX16) { asm volatile("prmt.b32 %0,%1,%2,%0;" : "+r"(v) : "r"(y),"r"(z)); v = __vmaxs2(v,z); BAR(v); }
+        else if (OP == MIX_PRMT_HFMA2) { asm volatile("prmt.b32 %0,%1,%2,%0;" : "+r"(v) : "r"(y),"r"(z)); v = h2fma(v,y,z); }
+        else if (OP == MIX_IMNMX_IMAD) { asm volatile("max.s32 %0,%0,%1;" : "+r"(v) : "r"(y)); asm volatile("mad.lo.s32 %0,%0,%1,%2;" : "+r"(v) : "r"(y),"r"(z)); }
+        else if (OP == MIX_HMNMX2_HADD2_SHFL) {
+          v = h2max(v,y); v = h2add(v,z); v = h2max(v,w); v = h2add(v,y); v = h2max(v,z); v = h2add(v,w); v = h2max(v,y); v = h2add(v,z);
+          v = __shfl_up_sync(0xffffffffu, v, 1, 8); BAR(v);
+        }
+        else if (OP == MIX_VIMNMX16_IMAD) { v = __vmaxs2(v,y); BAR(v); asm volatile("mad.lo.s32 %0,%0,%1,%2;" : "+r"(v) : "r"(y),"r"(z)); }
+        else if (OP == MIX_HSET2_HFMA2) { v = h2seteq(v,y); v = h2fma(v,y,z); }
+        else if (OP == MIX_HSET2_HMNMX2) { v = h2seteq(v,y); v = h2max(v,z); }
+        else if (OP == MIX_CELL_DPX) {
+          uint32_t s; asm volatile("prmt.b32 %0,%1,%2,%3;" : "=r"(s) : "r"(y),"r"(z),"r"(v));
+          uint32_t u1 = __vmaxs2(v, w); BAR(u1);
+          uint32_t u2 = __vmaxs2(v, y); BAR(u2);
+          uint32_t g = __viaddmax_s16x2(u1, z, u2); BAR(g);
+          uint32_t ga = __vadd2(g, w); BAR(ga);
+          v = __viaddmax_s16x2_relu(v, s, ga); BAR(v);
+        }
+        else if (OP == MIX_CELL_H2) {
+          uint32_t e = h2seteq(v, y);
+          uint32_t d = h2fmarelu(e, z, v);
+          uint32_t u1 = h2max(v, w);
+          uint32_t u2 = h2max(v, y);
+          uint32_t xx = h2add(u1, z);
+          uint32_t g = h2max(xx, u2);
+          uint32_t ga = h2add(g, w);
+          uint32_t h = h2max(d, ga);
+          v = h2add(h, z);
+        }
+        else if (OP == MIX_VIADD16_IMAD) { v = __vadd2(v,y); BAR(v); asm volatile("mad.lo.s32 %0,%0,%1,%2;" : "+r"(v) : "r"(y),"r"(z)); }
+        else if (OP == MIX_LDS_VIMNMX16) { uint32_t t = sm[(v & 1023)]; BAR(t); v = __vmaxs2(v,t); BAR(v); v = __vmaxs2(v,y); BAR(v); v = __vmaxs2(v,z); BAR(v); }
+        else if (OP == MIX_SHFL_VIMNMX16) { uint32_t t = __shfl_up_sync(0xffffffffu, v, 1, 8); BAR(t);
+          v = __vmaxs2(v,t); BAR(v); v = __vmaxs2(v,y); BAR(v); v = __vmaxs2(v,z); BAR(v); v = __vmaxs2(v,w); BAR(v);
+          v = __vmaxs2(v,y); BAR(v); v = __vmaxs2(v,z); BAR(v); v = __vmaxs2(v,w); BAR(v); }
+        else if (OP == MIX_IADD3_IMAD) { asm volatile("add.s32 %0,%0,%1;" : "+r"(v) : "r"(y)); asm volatile("mad.lo.s32 %0,%0,%1,%2;" : "+r"(v) : "r"(y),"r"(z)); }
+        else if (OP == MIX_LOP3_IMAD) { asm volatile("lop3.b32 %0,%0,%1,%2,0x96;" : "+r"(v) : "r"(y),"r"(z)); asm volatile("mad.lo.s32 %0,%0,%1,%2;" : "+r"(v) : "r"(y),"r"(z)); }
+        x[j] = v;
+      }
+    }
+  }
+  long long t1 = clock64();
+  uint32_t acc = 0;
+#pragma unroll
+  for (int j = 0; j < CHAINS; ++j) acc ^= x[j];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+template <int OP> void run(int nsm, uint32_t* out, uint32_t* in, long long* cyc, int threads) {
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  bench<OP><<<nsm, threads>>>(out, in, cyc); cudaDeviceSynchronize();
+  cudaEventRecord(e0);
+  bench<OP><<<nsm, threads>>>(out, in, cyc);
+  cudaEventRecord(e1); cudaDeviceSynchronize();
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  std::vector<long long> h(nsm); cudaMemcpy(h.data(), cyc, nsm * sizeof(long long), cudaMemcpyDeviceToHost);
+  double avg = 0; for (auto c : h) avg += c; avg /= nsm;
+  double instr = (double)threads * CHAINS * INNER * OUTER * per_step[OP];
+  printf("%2d %-70s thr=%4d  %7.2f src-instr/clk/SM  cyc/step/SMSP-warp=%.3f (%.3f ms, %.0f cyc, eff clk %.0f MHz)\n", OP, names[OP], threads, instr / avg, avg / ((double)CHAINS*INNER*OUTER) / (threads/128.0), ms, avg, avg / ms / 1e3);
+  cudaError_t err = cudaGetLastError(); if (err != cudaSuccess) printf("  CUDA error %s\n", cudaGetErrorString(err));
+}
+
+template <int OP> struct Runner { static void go(int nsm, uint32_t* o, uint32_t* i, long long* c) { run<OP>(nsm,o,i,c,1024); if (OP < 3) run<OP>(nsm,o,i,c,256); Runner<OP+1>::go(nsm,o,i,c); } };
+template <> struct Runner<OP_COUNT> { static void go(int, uint32_t*, uint32_t*, long long*) {} };
+
+int main() {
+  cudaDeviceProp p; cudaGetDeviceProperties(&p, 0);
+  int nsm = p.multiProcessorCount;
+  printf("device %s, %d SMs, clock %d kHz\n", p.name, nsm, p.clockRate);
+  uint32_t *out, *in; long long* cyc;
+  cudaMalloc(&out, (size_t)nsm * 1024 * 4); cudaMalloc(&in, 64 * 4); cudaMalloc(&cyc, nsm * 8);
+  uint32_t hin[64]; for (int i = 0; i < 64; ++i) hin[i] = 0x00030002u * (i + 1);
+  cudaMemcpy(in, hin, sizeof(hin), cudaMemcpyHostToDevice);
+  Runner<0>::go(nsm, out, in, cyc);
+  return 0;
+}
