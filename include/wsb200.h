@@ -1,0 +1,134 @@
+/*
+ * wsb200.h -- C ABI of the B200-native batched pairwise-alignment library (libwsb200.so).
+ *
+ * This is the drop-in boundary for the reference's batch hot path.  Every entry point is plain C: pointers and
+ * sizes only, no C++/torch types.  Functions return 0 on success or a negative wsb_status; they never throw.
+ *
+ * What each entry point replaces in the reference (pkg/src/waveseq/):
+ *   wsb_score_batch      batch.run_batch in score_only mode: the worker pool over _run_unit -> engine_score /
+ *                        engine_score_packed (batch.py:167-247, engine.py:383-400, 512-597), i.e. the numba kernels
+ *                        K.run_linear32 / run_merged32 / run_exact32 / run_linear16 / run_merged16
+ *                        (engine.py:333-363, 574-585; _kernels.py:181-201, 337-357, 502-524, 684-698, 843-858).
+ *   wsb_traceback_batch  batch.run_batch in traceback mode (batch.py:174-175); CIGARs follow the full-matrix walk
+ *                        refdp.ref_traceback (refdp.py:158-235), see DESIGN.md "CIGAR oracle".
+ *   wsb_batch_*          the same two calls split into upload / run / download so a caller can keep the sequence
+ *                        pools resident in HBM (BatchJob's queries/subjects/pairs, batch.py:68-89).
+ *   wsb_plan_shards      the cell-count balanced replacement of _plan_units/_chunk_units (batch.py:118-164) used to
+ *                        shard one job over several GPUs (one wsb_ctx per GPU, no collective).
+ *
+ * Sequence pools: one byte per symbol, 0..3 = A,C,G,T, 4 (or any value >= 4) = flagged / non-ACGT
+ * (core.py:63-118; engine._encode_q5, engine.py:203-207).  Sequence k of a pool occupies
+ * codes[off[k] .. off[k] + len[k]).  A pair p aligns query pair_q[p] (rows, CIGAR 'I' consumes it) against
+ * subject pair_s[p] (columns, CIGAR 'D' consumes it).
+ *
+ * Results are written by pair index, so they do not depend on scheduling, variant or GPU count
+ * (batch.py:206, tests/test_batch.py:89-99).
+ */
+#ifndef WSB200_H
+#define WSB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct wsb_ctx wsb_ctx;     /* one per GPU: device, streams, scratch.  Not re-entrant. */
+typedef struct wsb_batch wsb_batch; /* device-resident sequence pools + pair list + result buffers */
+
+typedef struct wsb_scheme {
+    int32_t match;      /* ScoringScheme.match_score   (core.py:125) */
+    int32_t mismatch;   /* ScoringScheme.mismatch_score */
+    int32_t gap_open;   /* alpha >= 0: cost of the first symbol of a gap run */
+    int32_t gap_extend; /* beta >= 0: cost of each further symbol (affine only) */
+    int32_t gap_model;  /* WSB_GAP_LINEAR | WSB_GAP_AFFINE */
+} wsb_scheme;
+
+enum wsb_align_type { WSB_GLOBAL = 0, WSB_LOCAL = 1, WSB_SEMIGLOBAL = 2 }; /* engine._ATYPE, engine.py:34 */
+enum wsb_gap_model { WSB_GAP_LINEAR = 0, WSB_GAP_AFFINE = 1 };
+
+/* Arithmetic variant of the score kernels.  AUTO picks, per pair, the packed half2 kernel when every DP value is an
+ * exactly representable fp16 integer (|v| <= 2048) and the scheme allows the merged gap state
+ * (engine.merged_state_exact, engine.py:71-94), else the int32 kernel.  Forcing F16X2 makes out-of-range pairs fail
+ * with WSB_E_RANGE in their status slot (the reference's PackedRangeOverflow, engine.py:530-534). */
+enum wsb_variant { WSB_VARIANT_AUTO = 0, WSB_VARIANT_F16X2 = 1, WSB_VARIANT_I32 = 2 };
+
+enum wsb_status {
+    WSB_OK = 0,
+    WSB_E_CUDA = -1,     /* CUDA runtime / launch failure; see wsb_last_error */
+    WSB_E_ARG = -2,      /* bad argument (null pointer, index out of range, unknown enum) */
+    WSB_E_NOMEM = -3,    /* host or device allocation failed */
+    WSB_E_LENGTH = -4,   /* max_step*(m+n) >= 2^29  (core.check_length_bounds, core.py:191-195) */
+    WSB_E_RANGE = -5,    /* pair does not fit the forced packed variant (PackedRangeOverflow) */
+    WSB_E_SCHEME = -6,   /* forced packed variant with an affine scheme the merged state cannot represent */
+    WSB_E_CAPACITY = -7, /* caller-provided CIGAR buffer too small */
+    WSB_E_NODEVICE = -8  /* no CUDA device */
+};
+
+const char* wsb_strerror(int status);
+const char* wsb_version(void);
+int wsb_device_count(int* count);
+
+int wsb_ctx_create(int device, wsb_ctx** out);
+void wsb_ctx_destroy(wsb_ctx* ctx);
+const char* wsb_last_error(const wsb_ctx* ctx);
+int wsb_ctx_sm_count(const wsb_ctx* ctx);
+
+/* ---- resident-batch API ---- */
+
+/* Copy the pools and the pair list to the device (async on the ctx stream) and build the execution plan inputs
+ * (per-pair lengths).  Host arrays may be pageable or pinned; they are not referenced after the call returns. */
+int wsb_batch_create(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t* q_off, const int32_t* q_len, int64_t n_q,
+                     const uint8_t* s_codes, const int64_t* s_off, const int32_t* s_len, int64_t n_s,
+                     const int32_t* pair_q, const int32_t* pair_s, int64_t n_pairs, wsb_batch** out);
+void wsb_batch_destroy(wsb_batch* b);
+
+/* Score every pair on the device; results stay in HBM until wsb_batch_fetch_scores.  kernel_ms (optional) receives
+ * the device time of the launched kernels measured with CUDA events on the ctx stream; n_launches (optional) the
+ * number of kernels launched.  Plans are cached per (scheme, align_type, variant). */
+int wsb_batch_score(wsb_batch* b, const wsb_scheme* scheme, int align_type, int variant, float* kernel_ms,
+                    int32_t* n_launches);
+
+/* out_i/out_j: end cell (query, subject), 1-based matrix coordinates = exclusive 0-based span ends; global -> (m, n).
+ * status (optional): per-pair wsb_status (0 or WSB_E_LENGTH / WSB_E_RANGE). */
+int wsb_batch_fetch_scores(wsb_batch* b, int32_t* out_score, int32_t* out_i, int32_t* out_j, int32_t* status);
+
+/* Direction-code fill + on-device walk + run-length CIGAR emission.  cigar receives runs packed as
+ * (length << 2) | op with op 0 = M, 1 = I, 2 = D in forward order; pair p owns cigar[cigar_off[p] .. cigar_off[p+1]).
+ * cigar_off has n_pairs + 1 entries.  If cigar_cap is too small the call returns WSB_E_CAPACITY and
+ * cigar_off[n_pairs] holds the required run count. */
+int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* scheme, int align_type, float* kernel_ms, int32_t* n_launches);
+int wsb_batch_fetch_traceback(wsb_batch* b, int32_t* out_score, int32_t* q_start, int32_t* q_end, int32_t* s_start,
+                              int32_t* s_end, uint32_t* cigar, int64_t cigar_cap, int64_t* cigar_off, int32_t* status);
+
+int64_t wsb_batch_total_cells(const wsb_batch* b); /* sum of m*n over pairs (BatchReport.total_cells, batch.py:243-247) */
+
+/* ---- one-shot host API (host buffers in, host buffers out) ---- */
+int wsb_score_batch(wsb_ctx* ctx, const wsb_scheme* scheme, int align_type, int variant, const uint8_t* q_codes,
+                    const int64_t* q_off, const int32_t* q_len, int64_t n_q, const uint8_t* s_codes,
+                    const int64_t* s_off, const int32_t* s_len, int64_t n_s, const int32_t* pair_q,
+                    const int32_t* pair_s, int64_t n_pairs, int32_t* out_score, int32_t* out_i, int32_t* out_j,
+                    int32_t* status);
+
+int wsb_traceback_batch(wsb_ctx* ctx, const wsb_scheme* scheme, int align_type, const uint8_t* q_codes,
+                        const int64_t* q_off, const int32_t* q_len, int64_t n_q, const uint8_t* s_codes,
+                        const int64_t* s_off, const int32_t* s_len, int64_t n_s, const int32_t* pair_q,
+                        const int32_t* pair_s, int64_t n_pairs, int32_t* out_score, int32_t* q_start, int32_t* q_end,
+                        int32_t* s_start, int32_t* s_end, uint32_t* cigar, int64_t cigar_cap, int64_t* cigar_off,
+                        int32_t* status);
+
+/* ---- host-only helpers (no GPU needed) ---- */
+
+/* engine.merged_state_exact (engine.py:71-94) */
+int wsb_merged_state_exact(const wsb_scheme* scheme);
+/* 1 when an m x n problem under the scheme is exact in the packed half2 kernel (all values integers, |v| <= 2048) */
+int wsb_f16_range_ok(const wsb_scheme* scheme, int32_t m, int32_t n);
+/* Cell-count balanced sharding of pairs over n_shards GPUs (longest-processing-time first).  shard_of[p] receives
+ * the shard of pair p; shard_cells[k] (optional) the cells assigned to shard k. */
+int wsb_plan_shards(const int32_t* q_len, const int32_t* s_len, const int32_t* pair_q, const int32_t* pair_s,
+                    int64_t n_pairs, int32_t n_shards, int32_t* shard_of, int64_t* shard_cells);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WSB200_H */

@@ -1,0 +1,245 @@
+"""ctypes binding of libwsb200.so (include/wsb200.h).  There is no CPU fallback: if the library is missing or no
+CUDA device is present, every compute entry point raises DeviceError."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .core import DeviceError, LengthOverflow, PackedRangeOverflow, WaveseqError
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libwsb200.so")
+_lib = None
+
+ALIGN_TYPE_ID = {"global": 0, "local": 1, "semiglobal": 2}
+GAP_MODEL_ID = {"linear": 0, "affine": 1}
+VARIANT_ID = {"auto": 0, "f16x2": 1, "i32": 2}
+
+WSB_OK, WSB_E_CUDA, WSB_E_ARG, WSB_E_NOMEM, WSB_E_LENGTH, WSB_E_RANGE, WSB_E_SCHEME, WSB_E_CAPACITY, WSB_E_NODEVICE = (
+    0, -1, -2, -3, -4, -5, -6, -7, -8)
+
+EXPORTED_SYMBOLS = (
+    "wsb_strerror", "wsb_version", "wsb_device_count", "wsb_ctx_create", "wsb_ctx_destroy", "wsb_last_error",
+    "wsb_ctx_sm_count", "wsb_batch_create", "wsb_batch_destroy", "wsb_batch_score", "wsb_batch_fetch_scores",
+    "wsb_batch_traceback", "wsb_batch_fetch_traceback", "wsb_batch_total_cells", "wsb_score_batch",
+    "wsb_traceback_batch", "wsb_merged_state_exact", "wsb_f16_range_ok", "wsb_plan_shards",
+)
+
+
+class SchemeStruct(ctypes.Structure):
+    _fields_ = [("match", ctypes.c_int32), ("mismatch", ctypes.c_int32), ("gap_open", ctypes.c_int32),
+                ("gap_extend", ctypes.c_int32), ("gap_model", ctypes.c_int32)]
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def load():
+    """Load the shared library (no GPU needed for loading or for the host-only helpers)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise DeviceError(f"{_LIB_PATH} is missing: build it with `python -m paper_2205_07610_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(_LIB_PATH)
+    p, i32, i64, ci = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int
+    lib.wsb_strerror.restype = ctypes.c_char_p
+    lib.wsb_strerror.argtypes = [ci]
+    lib.wsb_version.restype = ctypes.c_char_p
+    lib.wsb_last_error.restype = ctypes.c_char_p
+    lib.wsb_last_error.argtypes = [p]
+    lib.wsb_device_count.argtypes = [p]
+    lib.wsb_ctx_create.argtypes = [ci, p]
+    lib.wsb_ctx_destroy.argtypes = [p]
+    lib.wsb_ctx_destroy.restype = None
+    lib.wsb_ctx_sm_count.argtypes = [p]
+    lib.wsb_batch_create.argtypes = [p, p, p, p, i64, p, p, p, i64, p, p, i64, p]
+    lib.wsb_batch_destroy.argtypes = [p]
+    lib.wsb_batch_destroy.restype = None
+    lib.wsb_batch_score.argtypes = [p, p, ci, ci, p, p]
+    lib.wsb_batch_fetch_scores.argtypes = [p, p, p, p, p]
+    lib.wsb_batch_traceback.argtypes = [p, p, ci, p, p]
+    lib.wsb_batch_fetch_traceback.argtypes = [p, p, p, p, p, p, p, i64, p, p]
+    lib.wsb_batch_total_cells.argtypes = [p]
+    lib.wsb_batch_total_cells.restype = i64
+    lib.wsb_score_batch.argtypes = [p, p, ci, ci, p, p, p, i64, p, p, p, i64, p, p, i64, p, p, p, p]
+    lib.wsb_traceback_batch.argtypes = [p, p, ci, p, p, p, i64, p, p, p, i64, p, p, i64, p, p, p, p, p, p, i64, p, p]
+    lib.wsb_merged_state_exact.argtypes = [p]
+    lib.wsb_f16_range_ok.argtypes = [p, i32, i32]
+    lib.wsb_plan_shards.argtypes = [p, p, p, p, i64, i32, p, p]
+    _lib = lib
+    return lib
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def scheme_struct(scheme) -> SchemeStruct:
+    return SchemeStruct(int(scheme.match_score), int(scheme.mismatch_score), int(scheme.gap_open),
+                        int(scheme.gap_extend), GAP_MODEL_ID[scheme.gap_model])
+
+
+def status_exception(status: int, detail: str = "") -> Exception:
+    msg = load().wsb_strerror(status).decode()
+    if detail:
+        msg = f"{msg}: {detail}"
+    if status == WSB_E_LENGTH:
+        return LengthOverflow(msg)
+    if status == WSB_E_RANGE:
+        return PackedRangeOverflow(msg)
+    if status in (WSB_E_ARG, WSB_E_SCHEME):
+        return ValueError(msg)
+    if status == WSB_E_NOMEM:
+        return MemoryError(msg)
+    if status in (WSB_E_CUDA, WSB_E_NODEVICE):
+        return DeviceError(msg)
+    return WaveseqError(msg)
+
+
+def device_count() -> int:
+    n = ctypes.c_int(0)
+    load().wsb_device_count(ctypes.byref(n))
+    return n.value
+
+
+def merged_state_exact(scheme) -> bool:
+    s = scheme_struct(scheme)
+    return bool(load().wsb_merged_state_exact(ctypes.byref(s)))
+
+
+def f16_range_ok(scheme, m: int, n: int) -> bool:
+    s = scheme_struct(scheme)
+    return bool(load().wsb_f16_range_ok(ctypes.byref(s), int(m), int(n)))
+
+
+def plan_shards(q_len, s_len, pair_q, pair_s, n_shards: int):
+    q_len = np.ascontiguousarray(q_len, np.int32); s_len = np.ascontiguousarray(s_len, np.int32)
+    pair_q = np.ascontiguousarray(pair_q, np.int32); pair_s = np.ascontiguousarray(pair_s, np.int32)
+    shard_of = np.zeros(len(pair_q), np.int32)
+    cells = np.zeros(n_shards, np.int64)
+    rc = load().wsb_plan_shards(_ptr(q_len), _ptr(s_len), _ptr(pair_q), _ptr(pair_s), len(pair_q), n_shards,
+                                _ptr(shard_of), _ptr(cells))
+    if rc:
+        raise status_exception(rc)
+    return shard_of, cells
+
+
+class Context:
+    """One per GPU (wsb_ctx): owns the stream, events and scratch.  Not re-entrant."""
+
+    def __init__(self, device: int = 0):
+        self._lib = load()
+        h = ctypes.c_void_p()
+        rc = self._lib.wsb_ctx_create(int(device), ctypes.byref(h))
+        if rc:
+            raise status_exception(rc, f"device {device}")
+        self._h = h
+        self.device = device
+
+    @property
+    def sm_count(self) -> int:
+        return int(self._lib.wsb_ctx_sm_count(self._h))
+
+    def last_error(self) -> str:
+        return self._lib.wsb_last_error(self._h).decode()
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.wsb_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Batch:
+    """Device-resident pools + pair list (wsb_batch)."""
+
+    def __init__(self, ctx: Context, q_codes, q_off, q_len, s_codes, s_off, s_len, pair_q, pair_s):
+        self._lib = load()
+        self.ctx = ctx
+        arrs = [np.ascontiguousarray(q_codes, np.uint8), np.ascontiguousarray(q_off, np.int64),
+                np.ascontiguousarray(q_len, np.int32), np.ascontiguousarray(s_codes, np.uint8),
+                np.ascontiguousarray(s_off, np.int64), np.ascontiguousarray(s_len, np.int32),
+                np.ascontiguousarray(pair_q, np.int32), np.ascontiguousarray(pair_s, np.int32)]
+        self.n_pairs = len(arrs[6])
+        self.h2d_bytes = int(sum(a.nbytes for a in arrs))
+        h = ctypes.c_void_p()
+        rc = self._lib.wsb_batch_create(ctx._h, _ptr(arrs[0]), _ptr(arrs[1]), _ptr(arrs[2]), len(arrs[2]),
+                                        _ptr(arrs[3]), _ptr(arrs[4]), _ptr(arrs[5]), len(arrs[5]),
+                                        _ptr(arrs[6]), _ptr(arrs[7]), self.n_pairs, ctypes.byref(h))
+        if rc:
+            raise status_exception(rc, ctx.last_error())
+        self._h = h
+
+    @property
+    def total_cells(self) -> int:
+        return int(self._lib.wsb_batch_total_cells(self._h))
+
+    def score(self, scheme, align_type: str, variant: str = "auto", timed: bool = True):
+        """Run the score kernels; returns (kernel_ms, launches).  Results stay on the device."""
+        s = scheme_struct(scheme)
+        ms = ctypes.c_float(0.0)
+        nl = ctypes.c_int32(0)
+        rc = self._lib.wsb_batch_score(self._h, ctypes.byref(s), ALIGN_TYPE_ID[align_type], VARIANT_ID[variant],
+                                       ctypes.byref(ms) if timed else None, ctypes.byref(nl))
+        if rc:
+            raise status_exception(rc, self.ctx.last_error())
+        return float(ms.value), int(nl.value)
+
+    def fetch_scores(self):
+        n = self.n_pairs
+        score = np.empty(n, np.int32); ei = np.empty(n, np.int32); ej = np.empty(n, np.int32)
+        status = np.empty(n, np.int32)
+        rc = self._lib.wsb_batch_fetch_scores(self._h, _ptr(score), _ptr(ei), _ptr(ej), _ptr(status))
+        if rc:
+            raise status_exception(rc, self.ctx.last_error())
+        return score, ei, ej, status
+
+    def traceback(self, scheme, align_type: str, timed: bool = True):
+        s = scheme_struct(scheme)
+        ms = ctypes.c_float(0.0)
+        nl = ctypes.c_int32(0)
+        rc = self._lib.wsb_batch_traceback(self._h, ctypes.byref(s), ALIGN_TYPE_ID[align_type],
+                                           ctypes.byref(ms) if timed else None, ctypes.byref(nl))
+        if rc:
+            raise status_exception(rc, self.ctx.last_error())
+        return float(ms.value), int(nl.value)
+
+    def fetch_traceback(self, cigar_cap: int | None = None):
+        n = self.n_pairs
+        out = {k: np.empty(n, np.int32) for k in ("score", "q_start", "q_end", "s_start", "s_end", "status")}
+        off = np.zeros(n + 1, np.int64)
+        cap = int(cigar_cap) if cigar_cap is not None else max(16 * n, 1024)
+        while True:
+            cig = np.empty(cap, np.uint32)
+            rc = self._lib.wsb_batch_fetch_traceback(self._h, _ptr(out["score"]), _ptr(out["q_start"]),
+                                                     _ptr(out["q_end"]), _ptr(out["s_start"]), _ptr(out["s_end"]),
+                                                     _ptr(cig), cap, _ptr(off), _ptr(out["status"]))
+            if rc == WSB_E_CAPACITY and cigar_cap is None:
+                cap = int(off[n])
+                continue
+            if rc:
+                raise status_exception(rc, self.ctx.last_error())
+            break
+        out["cigar"] = cig[:int(off[n])]
+        out["cigar_off"] = off
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.wsb_batch_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

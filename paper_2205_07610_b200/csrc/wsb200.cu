@@ -1,0 +1,563 @@
+// wsb200.cu -- host side of libwsb200.so: contexts, resident batches, the length-bucketing planner, kernel dispatch
+// and the C ABI declared in include/wsb200.h.  No CPU compute path exists here: every alignment runs in the CUDA
+// kernels of score_kernels.cuh / traceback_kernels.cuh.
+#include "../../include/wsb200.h"
+#include "score_kernels.cuh"
+#include "traceback_kernels.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <new>
+#include <numeric>
+#include <string>
+#include <thread>
+#include <tuple>
+#include <type_traits>
+#include <vector>
+
+using namespace wsb;
+
+// ------------------------------------------------------------------------------------------------ objects
+struct wsb_ctx {
+    int device = 0;
+    int sm_count = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::string last_error;
+};
+
+struct LaunchGroup {  // pairs that run in one kernel launch
+    int variant = 0;  // WSB_VARIANT_F16X2 | WSB_VARIANT_I32
+    int shape = 0;    // index into the (P, K) shape table of the variant
+    int gap = 0;      // GAP_LINEAR | GAP_MERGED | GAP_EXACT
+    int64_t n_units = 0;
+    int64_t unit_off = 0;  // offset (in int32) into the plan's unit array; -1 = identity mapping
+    int max_m = 0, max_n = 0;
+};
+
+struct Plan {
+    std::vector<LaunchGroup> groups;
+    int32_t* d_units = nullptr;
+    std::vector<int32_t> status;  // per pair
+    bool any_error = false;
+};
+
+struct wsb_batch {
+    wsb_ctx* ctx = nullptr;
+    int64_t n_q = 0, n_s = 0, n_pairs = 0;
+    uint8_t *d_qcodes = nullptr, *d_scodes = nullptr;
+    int64_t *d_qoff = nullptr, *d_soff = nullptr;
+    int32_t *d_qlen = nullptr, *d_slen = nullptr, *d_pq = nullptr, *d_ps = nullptr;
+    int32_t *d_score = nullptr, *d_i = nullptr, *d_j = nullptr;
+    std::vector<int32_t> m, n;  // per pair lengths (host)
+    bool uniform = false;       // every pair has the same (m, n)
+    int64_t total_cells = 0;
+    std::map<std::tuple<int, int, int, int, int, int, int>, Plan> plans;
+    const Plan* last_plan = nullptr;
+    void* d_bnd = nullptr;
+    size_t bnd_bytes = 0;
+    TracebackState tb;  // traceback_kernels.cuh
+};
+
+#define CUDA_TRY(ctx, expr)                                                                        \
+    do {                                                                                           \
+        cudaError_t e_ = (expr);                                                                   \
+        if (e_ != cudaSuccess) {                                                                   \
+            (ctx)->last_error = std::string(#expr) + ": " + cudaGetErrorString(e_);                \
+            return e_ == cudaErrorMemoryAllocation ? WSB_E_NOMEM : WSB_E_CUDA;                     \
+        }                                                                                          \
+    } while (0)
+
+// ------------------------------------------------------------------------------------------------ small helpers
+extern "C" const char* wsb_strerror(int status) {
+    switch (status) {
+        case WSB_OK: return "ok";
+        case WSB_E_CUDA: return "CUDA runtime or kernel launch failure";
+        case WSB_E_ARG: return "invalid argument";
+        case WSB_E_NOMEM: return "out of memory";
+        case WSB_E_LENGTH: return "sequence lengths exceed the supported score range (max_step*(m+n) >= 2^29)";
+        case WSB_E_RANGE: return "problem exceeds the packed half2 value range";
+        case WSB_E_SCHEME: return "packed affine mode requires a merged-state-exact scheme";
+        case WSB_E_CAPACITY: return "output buffer too small";
+        case WSB_E_NODEVICE: return "no CUDA device available";
+        default: return "unknown status";
+    }
+}
+
+extern "C" const char* wsb_version(void) { return "wsb200 0.1.0 (sm_100a)"; }
+
+extern "C" int wsb_device_count(int* count) {
+    if (!count) return WSB_E_ARG;
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) { *count = 0; (void)cudaGetLastError(); return WSB_E_NODEVICE; }
+    *count = n;
+    return n > 0 ? WSB_OK : WSB_E_NODEVICE;
+}
+
+static int max_step(const wsb_scheme* s) {
+    return std::max({std::abs(s->match), std::abs(s->mismatch), s->gap_open, s->gap_extend, 1});
+}
+
+extern "C" int wsb_merged_state_exact(const wsb_scheme* s) {
+    if (!s) return 0;
+    const int worst = std::min(s->mismatch, s->match);
+    if (s->match < s->mismatch) return 0;
+    if (s->gap_open + s->gap_extend < -worst) return 0;
+    if (2 * s->gap_extend < -worst) return 0;
+    return 1;
+}
+
+extern "C" int wsb_f16_range_ok(const wsb_scheme* s, int32_t m, int32_t n) {
+    if (!s) return 0;
+    // every finite value the kernel forms is bounded by max_step*(m+n) plus one open/extend/mismatch shift
+    const int64_t bound = (int64_t)max_step(s) * ((int64_t)m + n) + std::abs(s->mismatch) + s->gap_open + s->gap_extend;
+    return bound <= 2048 ? 1 : 0;
+}
+
+extern "C" int wsb_plan_shards(const int32_t* q_len, const int32_t* s_len, const int32_t* pair_q, const int32_t* pair_s,
+                               int64_t n_pairs, int32_t n_shards, int32_t* shard_of, int64_t* shard_cells) {
+    if (!q_len || !s_len || !pair_q || !pair_s || !shard_of || n_pairs < 0 || n_shards < 1) return WSB_E_ARG;
+    std::vector<int64_t> cells((size_t)n_pairs);
+    bool uniform = true;
+    for (int64_t p = 0; p < n_pairs; ++p) {
+        cells[p] = (int64_t)q_len[pair_q[p]] * s_len[pair_s[p]];
+        if (cells[p] != cells[0]) uniform = false;
+    }
+    std::vector<int64_t> load((size_t)n_shards, 0);
+    if (uniform) {  // contiguous equal blocks keep the pools' locality
+        for (int64_t p = 0; p < n_pairs; ++p) {
+            const int k = (int)std::min<int64_t>(n_shards - 1, p * n_shards / std::max<int64_t>(n_pairs, 1));
+            shard_of[p] = k; load[k] += cells[p];
+        }
+    } else {  // longest-processing-time first: biggest pair to the least loaded shard
+        std::vector<int64_t> order((size_t)n_pairs);
+        std::iota(order.begin(), order.end(), 0);
+        std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return cells[a] > cells[b]; });
+        for (int64_t p : order) {
+            int k = 0;
+            for (int x = 1; x < n_shards; ++x) if (load[x] < load[k]) k = x;
+            shard_of[p] = k; load[k] += cells[p];
+        }
+    }
+    if (shard_cells) for (int k = 0; k < n_shards; ++k) shard_cells[k] = load[k];
+    return WSB_OK;
+}
+
+// ------------------------------------------------------------------------------------------------ context
+extern "C" int wsb_ctx_create(int device, wsb_ctx** out) {
+    if (!out) return WSB_E_ARG;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0) { (void)cudaGetLastError(); return WSB_E_NODEVICE; }
+    if (device < 0 || device >= n) return WSB_E_ARG;
+    wsb_ctx* c = new (std::nothrow) wsb_ctx();
+    if (!c) return WSB_E_NOMEM;
+    c->device = device;
+    if (cudaSetDevice(device) != cudaSuccess ||
+        cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
+        (void)cudaGetLastError();
+        delete c;
+        return WSB_E_CUDA;
+    }
+    *out = c;
+    return WSB_OK;
+}
+
+extern "C" void wsb_ctx_destroy(wsb_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+extern "C" const char* wsb_last_error(const wsb_ctx* c) { return c ? c->last_error.c_str() : "null context"; }
+extern "C" int wsb_ctx_sm_count(const wsb_ctx* c) { return c ? c->sm_count : 0; }
+
+// ------------------------------------------------------------------------------------------------ batch
+template <class T> static int upload(wsb_ctx* ctx, T** dst, const T* src, int64_t count) {
+    *dst = nullptr;
+    const size_t bytes = sizeof(T) * (size_t)std::max<int64_t>(count, 1);
+    CUDA_TRY(ctx, cudaMalloc((void**)dst, bytes));
+    if (count > 0) CUDA_TRY(ctx, cudaMemcpyAsync(*dst, src, sizeof(T) * (size_t)count, cudaMemcpyHostToDevice, ctx->stream));
+    return WSB_OK;
+}
+
+extern "C" void wsb_batch_destroy(wsb_batch* b) {
+    if (!b) return;
+    cudaSetDevice(b->ctx->device);
+    cudaStreamSynchronize(b->ctx->stream);
+    for (void* p : {(void*)b->d_qcodes, (void*)b->d_scodes, (void*)b->d_qoff, (void*)b->d_soff, (void*)b->d_qlen,
+                    (void*)b->d_slen, (void*)b->d_pq, (void*)b->d_ps, (void*)b->d_score, (void*)b->d_i, (void*)b->d_j,
+                    b->d_bnd})
+        if (p) cudaFree(p);
+    for (auto& kv : b->plans) if (kv.second.d_units) cudaFree(kv.second.d_units);
+    b->tb.release();
+    delete b;
+}
+
+extern "C" int wsb_batch_create(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t* q_off, const int32_t* q_len,
+                                int64_t n_q, const uint8_t* s_codes, const int64_t* s_off, const int32_t* s_len,
+                                int64_t n_s, const int32_t* pair_q, const int32_t* pair_s, int64_t n_pairs,
+                                wsb_batch** out) {
+    if (!ctx || !out || !q_codes || !q_off || !q_len || !s_codes || !s_off || !s_len || !pair_q || !pair_s ||
+        n_q <= 0 || n_s <= 0 || n_pairs <= 0 || n_pairs > (int64_t)0x7fffffff)
+        return WSB_E_ARG;
+    *out = nullptr;
+    CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    wsb_batch* b = new (std::nothrow) wsb_batch();
+    if (!b) return WSB_E_NOMEM;
+    b->ctx = ctx; b->n_q = n_q; b->n_s = n_s; b->n_pairs = n_pairs;
+
+    // per-pair lengths, index validation and the uniformity test, split over host threads
+    try { b->m.resize((size_t)n_pairs); b->n.resize((size_t)n_pairs); } catch (...) { delete b; return WSB_E_NOMEM; }
+    const int nthr = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency())), n_pairs / 65536 + 1));
+    std::vector<int> bad(nthr, 0), uni(nthr, 1);
+    std::vector<int64_t> cells(nthr, 0);
+    const int m0 = (pair_q[0] >= 0 && pair_q[0] < n_q) ? q_len[pair_q[0]] : -1;
+    const int n0 = (pair_s[0] >= 0 && pair_s[0] < n_s) ? s_len[pair_s[0]] : -1;
+    auto work = [&](int k) {
+        const int64_t lo = n_pairs * k / nthr, hi = n_pairs * (k + 1) / nthr;
+        int64_t acc = 0;
+        for (int64_t p = lo; p < hi; ++p) {
+            const int a = pair_q[p], c = pair_s[p];
+            if (a < 0 || a >= n_q || c < 0 || c >= n_s) { bad[k] = 1; b->m[p] = b->n[p] = 0; continue; }
+            const int mm = q_len[a], nn = s_len[c];
+            if (mm < 0 || nn < 0) { bad[k] = 1; continue; }
+            b->m[p] = mm; b->n[p] = nn;
+            acc += (int64_t)mm * nn;
+            if (mm != m0 || nn != n0) uni[k] = 0;
+        }
+        cells[k] = acc;
+    };
+    if (nthr == 1) work(0);
+    else {
+        std::vector<std::thread> th;
+        for (int k = 0; k < nthr; ++k) th.emplace_back(work, k);
+        for (auto& x : th) x.join();
+    }
+    b->uniform = true;
+    for (int k = 0; k < nthr; ++k) {
+        if (bad[k]) { delete b; return WSB_E_ARG; }
+        if (!uni[k]) b->uniform = false;
+        b->total_cells += cells[k];
+    }
+
+    const int64_t q_bytes = q_off[n_q - 1] + q_len[n_q - 1];
+    const int64_t s_bytes = s_off[n_s - 1] + s_len[n_s - 1];
+    int64_t q_total = 0, s_total = 0;  // pools need not be packed in order: take the furthest end
+    for (int64_t k = 0; k < n_q; ++k) q_total = std::max(q_total, q_off[k] + q_len[k]);
+    for (int64_t k = 0; k < n_s; ++k) s_total = std::max(s_total, s_off[k] + s_len[k]);
+    (void)q_bytes; (void)s_bytes;
+    int rc;
+#define UP(dst, src, cnt) if ((rc = upload(ctx, &b->dst, src, cnt)) != WSB_OK) { wsb_batch_destroy(b); return rc; }
+    UP(d_qcodes, q_codes, q_total) UP(d_scodes, s_codes, s_total)
+    UP(d_qoff, q_off, n_q) UP(d_soff, s_off, n_s) UP(d_qlen, q_len, n_q) UP(d_slen, s_len, n_s)
+    UP(d_pq, pair_q, n_pairs) UP(d_ps, pair_s, n_pairs)
+#undef UP
+    for (int32_t** p : {&b->d_score, &b->d_i, &b->d_j}) {
+        cudaError_t e = cudaMalloc((void**)p, sizeof(int32_t) * (size_t)n_pairs);
+        if (e != cudaSuccess) { ctx->last_error = cudaGetErrorString(e); wsb_batch_destroy(b); return WSB_E_NOMEM; }
+    }
+    cudaError_t e = cudaStreamSynchronize(ctx->stream);  // host arrays may be reused by the caller after return
+    if (e != cudaSuccess) { ctx->last_error = cudaGetErrorString(e); wsb_batch_destroy(b); return WSB_E_CUDA; }
+    *out = b;
+    return WSB_OK;
+}
+
+extern "C" int64_t wsb_batch_total_cells(const wsb_batch* b) { return b ? b->total_cells : 0; }
+
+// ------------------------------------------------------------------------------------------------ kernel shapes
+struct Shape { int P, K; };
+// packed half2 shapes: short reads in a single stage; (8,32) also chains stages for longer packed reads
+static const Shape kShapesF16[] = {{4, 16}, {8, 19}, {8, 32}};
+// int32 shapes: narrow groups for short reads, full warps with wide stages for long reads
+static const Shape kShapesI32[] = {{8, 16}, {16, 16}, {32, 16}};
+constexpr int kNumShapes = 3;
+
+static double padded_cost(const Shape& s, int m, int n) {
+    const int w = s.P * s.K;
+    const int stages = (n + w - 1) / w;
+    return (double)(m + s.P - 1) * stages * w;
+}
+
+static int best_shape(const Shape* shapes, int m, int n) {
+    int best = 0;
+    double bc = padded_cost(shapes[0], m, n);
+    for (int k = 1; k < kNumShapes; ++k) {
+        const double c = padded_cost(shapes[k], m, n);
+        if (c < bc) { bc = c; best = k; }
+    }
+    return best;
+}
+
+using KernelFn = void (*)(const ScoreParams);
+
+template <class AR, int P, int K, int GAP> static KernelFn pick_atype(int atype) {
+    switch (atype) {
+        case AT_GLOBAL: return score_kernel<AR, P, K, AT_GLOBAL, GAP>;
+        case AT_LOCAL: return score_kernel<AR, P, K, AT_LOCAL, GAP>;
+        default: return score_kernel<AR, P, K, AT_SEMI, GAP>;
+    }
+}
+
+template <class AR, int P, int K> static KernelFn pick_gap(int atype, int gap) {
+    if (gap == GAP_LINEAR) return pick_atype<AR, P, K, GAP_LINEAR>(atype);
+    if (gap == GAP_MERGED) return pick_atype<AR, P, K, GAP_MERGED>(atype);
+    if constexpr (std::is_same<AR, ArI32>::value) return pick_atype<ArI32, P, K, GAP_EXACT>(atype);
+    return nullptr;  // the packed kernels have no exact three-state model
+}
+
+static KernelFn pick_kernel(int variant, int shape, int atype, int gap) {
+    if (variant == WSB_VARIANT_F16X2) {
+        switch (shape) {
+            case 0: return pick_gap<ArF16, 4, 16>(atype, gap);
+            case 1: return pick_gap<ArF16, 8, 19>(atype, gap);
+            default: return pick_gap<ArF16, 8, 32>(atype, gap);
+        }
+    }
+    switch (shape) {
+        case 0: return pick_gap<ArI32, 8, 16>(atype, gap);
+        case 1: return pick_gap<ArI32, 16, 16>(atype, gap);
+        default: return pick_gap<ArI32, 32, 16>(atype, gap);
+    }
+}
+
+// ------------------------------------------------------------------------------------------------ planner
+// Length-bucketing partitioner: classify every pair (variant by value range, kernel shape by padded work), sort each
+// class by work so neighbouring lane groups (and the two halves of a packed unit) carry near-equal loads, and emit one
+// launch group per (variant, shape).  Replaces batch._plan_units / _chunk_units (batch.py:118-164).
+static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int variant, Plan& plan) {
+    wsb_ctx* ctx = b->ctx;
+    const int64_t np = b->n_pairs;
+    const bool affine = sch->gap_model == WSB_GAP_AFFINE;
+    const bool merged_ok = !affine || wsb_merged_state_exact(sch);
+    // the packed kernel's junk-cell argument needs never-matching pads to be non-improving
+    const bool f16_scheme_ok = merged_ok && sch->mismatch <= 0 && sch->match >= 0;
+    const int gap_i32 = !affine ? GAP_LINEAR : (wsb_merged_state_exact(sch) ? GAP_MERGED : GAP_EXACT);
+    const int gap_f16 = !affine ? GAP_LINEAR : GAP_MERGED;
+    const int ms = max_step(sch);
+    plan.status.assign((size_t)np, 0);
+
+    if (variant == WSB_VARIANT_F16X2 && !merged_ok) return WSB_E_SCHEME;
+
+    auto classify = [&](int m, int n, int& var, int& shape, int& status) {
+        status = 0; var = -1; shape = 0;
+        if (m == 0 || n == 0) return;  // empty side: resolved on the host below, never launched
+        if ((int64_t)ms * ((int64_t)m + n) >= (1ll << 29)) { status = WSB_E_LENGTH; return; }
+        const bool fits = f16_scheme_ok && wsb_f16_range_ok(sch, m, n);
+        if (variant == WSB_VARIANT_F16X2 && !fits) { status = WSB_E_RANGE; return; }
+        if (variant != WSB_VARIANT_I32 && fits) { var = WSB_VARIANT_F16X2; shape = best_shape(kShapesF16, m, n); }
+        else { var = WSB_VARIANT_I32; shape = best_shape(kShapesI32, m, n); }
+    };
+
+    if (b->uniform) {
+        int var, shape, status;
+        classify(b->m[0], b->n[0], var, shape, status);
+        if (status) { std::fill(plan.status.begin(), plan.status.end(), status); plan.any_error = true; return WSB_OK; }
+        if (var < 0) return WSB_OK;
+        LaunchGroup g;
+        g.variant = var; g.shape = shape; g.gap = var == WSB_VARIANT_F16X2 ? gap_f16 : gap_i32;
+        g.n_units = var == WSB_VARIANT_F16X2 ? (np + 1) / 2 : np;
+        g.unit_off = -1; g.max_m = b->m[0]; g.max_n = b->n[0];
+        plan.groups.push_back(g);
+        return WSB_OK;
+    }
+
+    // general path: bucket, sort by work (descending), pair neighbours
+    std::vector<int64_t> bucket[2][kNumShapes];
+    for (int64_t p = 0; p < np; ++p) {
+        int var, shape, status;
+        classify(b->m[p], b->n[p], var, shape, status);
+        if (status) { plan.status[p] = status; plan.any_error = true; continue; }
+        if (var < 0) continue;
+        bucket[var == WSB_VARIANT_F16X2 ? 0 : 1][shape].push_back(p);
+    }
+    std::vector<int32_t> units;
+    for (int cls = 0; cls < 2; ++cls)
+        for (int s = 0; s < kNumShapes; ++s) {
+            auto& v = bucket[cls][s];
+            if (v.empty()) continue;
+            std::stable_sort(v.begin(), v.end(), [&](int64_t x, int64_t y) {
+                const int64_t cx = (int64_t)b->m[x] * b->n[x], cy = (int64_t)b->m[y] * b->n[y];
+                if (cx != cy) return cx > cy;
+                return b->n[x] > b->n[y];
+            });
+            LaunchGroup g;
+            g.variant = cls == 0 ? WSB_VARIANT_F16X2 : WSB_VARIANT_I32;
+            g.shape = s; g.gap = cls == 0 ? gap_f16 : gap_i32;
+            g.unit_off = (int64_t)units.size();
+            for (int64_t p : v) { g.max_m = std::max(g.max_m, b->m[p]); g.max_n = std::max(g.max_n, b->n[p]); }
+            if (cls == 0) {
+                g.n_units = ((int64_t)v.size() + 1) / 2;
+                for (size_t k = 0; k < v.size(); k += 2) {
+                    units.push_back((int32_t)v[k]);
+                    units.push_back(k + 1 < v.size() ? (int32_t)v[k + 1] : -1);
+                }
+            } else {
+                g.n_units = (int64_t)v.size();
+                for (int64_t p : v) units.push_back((int32_t)p);
+            }
+            plan.groups.push_back(g);
+        }
+    if (!units.empty()) {
+        CUDA_TRY(ctx, cudaMalloc((void**)&plan.d_units, units.size() * sizeof(int32_t)));
+        CUDA_TRY(ctx, cudaMemcpyAsync(plan.d_units, units.data(), units.size() * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+    return WSB_OK;
+}
+
+// pairs with an empty side never reach the device (engine.py:281-288); fill their slots after the kernels
+__global__ void empty_side_kernel(const int32_t* pair_q, const int32_t* pair_s, const int32_t* q_len, const int32_t* s_len,
+                                  int64_t n_pairs, int atype, int affine, int alpha, int beta, int32_t* out_score,
+                                  int32_t* out_i, int32_t* out_j) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n_pairs) return;
+    const int m = q_len[pair_q[p]], n = s_len[pair_s[p]];
+    if (m != 0 && n != 0) return;
+    if (atype == AT_GLOBAL) {
+        const int len = m == 0 ? n : m;
+        const int cost = len <= 0 ? 0 : (affine ? alpha + (len - 1) * beta : alpha * len);
+        out_score[p] = -cost; out_i[p] = m; out_j[p] = n;
+    } else if (atype == AT_LOCAL) {
+        out_score[p] = 0; out_i[p] = 0; out_j[p] = 0;
+    } else {
+        out_score[p] = 0; out_i[p] = 0; out_j[p] = m == 0 ? n : 0;
+    }
+}
+
+static int check_scheme(const wsb_scheme* s, int atype) {
+    if (!s) return WSB_E_ARG;
+    if (atype < 0 || atype > 2) return WSB_E_ARG;
+    if (s->gap_model != WSB_GAP_LINEAR && s->gap_model != WSB_GAP_AFFINE) return WSB_E_ARG;
+    if (s->gap_open < 0 || s->gap_extend < 0) return WSB_E_ARG;
+    return WSB_OK;
+}
+
+extern "C" int wsb_batch_score(wsb_batch* b, const wsb_scheme* sch, int atype, int variant, float* kernel_ms,
+                               int32_t* n_launches) {
+    if (!b) return WSB_E_ARG;
+    int rc = check_scheme(sch, atype);
+    if (rc) return rc;
+    if (variant < WSB_VARIANT_AUTO || variant > WSB_VARIANT_I32) return WSB_E_ARG;
+    wsb_ctx* ctx = b->ctx;
+    CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    const bool affine = sch->gap_model == WSB_GAP_AFFINE;
+    const int beta_eff = affine ? sch->gap_extend : sch->gap_open;
+
+    auto key = std::make_tuple(sch->match, sch->mismatch, sch->gap_open, sch->gap_extend, sch->gap_model, atype, variant);
+    auto it = b->plans.find(key);
+    if (it == b->plans.end()) {
+        Plan plan;
+        rc = build_plan(b, sch, atype, variant, plan);
+        if (rc) { if (plan.d_units) cudaFree(plan.d_units); return rc; }
+        it = b->plans.emplace(key, std::move(plan)).first;
+    }
+    const Plan& plan = it->second;
+    b->last_plan = &plan;
+
+    // launch geometry + border scratch
+    struct Geo { KernelFn fn; int grid; int64_t bnd_rows; };
+    std::vector<Geo> geo;
+    size_t bnd_need = 0;
+    for (const LaunchGroup& g : plan.groups) {
+        const Shape sh = g.variant == WSB_VARIANT_F16X2 ? kShapesF16[g.shape] : kShapesI32[g.shape];
+        KernelFn fn = pick_kernel(g.variant, g.shape, atype, g.gap);
+        if (!fn) return WSB_E_SCHEME;
+        int per_sm = 0;
+        CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, 0));
+        per_sm = std::max(per_sm, 1);
+        const int gpb = kThreads / sh.P;
+        const int64_t blocks_needed = (g.n_units + gpb - 1) / gpb;
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(blocks_needed, (int64_t)ctx->sm_count * per_sm));
+        const bool multi_stage = g.max_n > sh.P * sh.K;
+        const int64_t rows = multi_stage ? (int64_t)g.max_m + 2 : 0;
+        geo.push_back({fn, grid, rows});
+        bnd_need = std::max(bnd_need, (size_t)rows * 8u * (size_t)grid * gpb);
+    }
+    if (bnd_need > b->bnd_bytes) {
+        if (b->d_bnd) { cudaFree(b->d_bnd); b->d_bnd = nullptr; b->bnd_bytes = 0; }
+        CUDA_TRY(ctx, cudaMalloc(&b->d_bnd, bnd_need));
+        b->bnd_bytes = bnd_need;
+    }
+
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+    int launches = 0;
+    for (size_t k = 0; k < plan.groups.size(); ++k) {
+        const LaunchGroup& g = plan.groups[k];
+        ScoreParams prm;
+        prm.q_codes = b->d_qcodes; prm.q_off = b->d_qoff; prm.q_len = b->d_qlen;
+        prm.s_codes = b->d_scodes; prm.s_off = b->d_soff; prm.s_len = b->d_slen;
+        prm.pair_q = b->d_pq; prm.pair_s = b->d_ps;
+        prm.units = g.unit_off >= 0 ? plan.d_units + g.unit_off : nullptr;
+        prm.n_units = g.n_units; prm.n_pairs = b->n_pairs;
+        prm.out_score = b->d_score; prm.out_i = b->d_i; prm.out_j = b->d_j;
+        prm.match = sch->match; prm.mismatch = sch->mismatch; prm.alpha = sch->gap_open; prm.beta = beta_eff;
+        prm.bnd = geo[k].bnd_rows ? b->d_bnd : nullptr; prm.bnd_rows = geo[k].bnd_rows;
+        geo[k].fn<<<geo[k].grid, kThreads, 0, ctx->stream>>>(prm);
+        CUDA_TRY(ctx, cudaGetLastError());
+        ++launches;
+    }
+    {  // empty-side pairs (only possible for non-uniform batches or a uniform batch of empties)
+        bool any_empty = false;
+        if (b->uniform) any_empty = b->m[0] == 0 || b->n[0] == 0;
+        else for (int64_t p = 0; p < b->n_pairs && !any_empty; ++p) any_empty = b->m[p] == 0 || b->n[p] == 0;
+        if (any_empty) {
+            const int thr = 256;
+            empty_side_kernel<<<(unsigned)((b->n_pairs + thr - 1) / thr), thr, 0, ctx->stream>>>(
+                b->d_pq, b->d_ps, b->d_qlen, b->d_slen, b->n_pairs, atype, affine ? 1 : 0, sch->gap_open, beta_eff,
+                b->d_score, b->d_i, b->d_j);
+            CUDA_TRY(ctx, cudaGetLastError());
+            ++launches;
+        }
+    }
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+    if (kernel_ms) {
+        CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev1));
+        CUDA_TRY(ctx, cudaEventElapsedTime(kernel_ms, ctx->ev0, ctx->ev1));
+    }
+    if (n_launches) *n_launches = launches;
+    return WSB_OK;
+}
+
+extern "C" int wsb_batch_fetch_scores(wsb_batch* b, int32_t* out_score, int32_t* out_i, int32_t* out_j, int32_t* status) {
+    if (!b || !out_score || !out_i || !out_j) return WSB_E_ARG;
+    wsb_ctx* ctx = b->ctx;
+    CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+    const size_t bytes = sizeof(int32_t) * (size_t)b->n_pairs;
+    CUDA_TRY(ctx, cudaMemcpyAsync(out_score, b->d_score, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpyAsync(out_i, b->d_i, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaMemcpyAsync(out_j, b->d_j, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    if (status) {
+        if (b->last_plan) std::memcpy(status, b->last_plan->status.data(), bytes);
+        else std::memset(status, 0, bytes);
+    }
+    return WSB_OK;
+}
+
+extern "C" int wsb_score_batch(wsb_ctx* ctx, const wsb_scheme* scheme, int align_type, int variant,
+                               const uint8_t* q_codes, const int64_t* q_off, const int32_t* q_len, int64_t n_q,
+                               const uint8_t* s_codes, const int64_t* s_off, const int32_t* s_len, int64_t n_s,
+                               const int32_t* pair_q, const int32_t* pair_s, int64_t n_pairs, int32_t* out_score,
+                               int32_t* out_i, int32_t* out_j, int32_t* status) {
+    wsb_batch* b = nullptr;
+    int rc = wsb_batch_create(ctx, q_codes, q_off, q_len, n_q, s_codes, s_off, s_len, n_s, pair_q, pair_s, n_pairs, &b);
+    if (rc) return rc;
+    rc = wsb_batch_score(b, scheme, align_type, variant, nullptr, nullptr);
+    if (!rc) rc = wsb_batch_fetch_scores(b, out_score, out_i, out_j, status);
+    wsb_batch_destroy(b);
+    return rc;
+}
+
+// ------------------------------------------------------------------------------------------------ traceback ABI
+#include "traceback_host.inl"

@@ -1,0 +1,120 @@
+"""GPU parity: score + end cell of the CUDA kernels (through the C ABI) == the oracle, bit-exact."""
+import numpy as np
+import pytest
+
+from conftest import AFFINE_SCHEMES, COMBOS, LINEAR_SCHEMES, codes, load_golden, mutate_codes, random_codes
+from helpers import assert_scores_equal, gpu_scores, oracle_scores, scheme_of
+from paper_2205_07610_b200 import _native as N
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = N.Context(0)
+    yield c
+    c.close()
+
+
+def _random_batch(rng, count, lo, hi, related=0.5, flagged=0.0):
+    qs, ss = [], []
+    for _ in range(count):
+        q = random_codes(rng, int(rng.integers(lo, hi + 1)))
+        s = mutate_codes(rng, q) if rng.random() < related else random_codes(rng, int(rng.integers(lo, hi + 1)))
+        if flagged and rng.random() < flagged:
+            q = q.copy(); q[rng.integers(0, len(q))] = 4
+            s = s.copy(); s[rng.integers(0, len(s))] = 4
+        qs.append(q); ss.append(s)
+    return qs, ss, [(i, i) for i in range(count)]
+
+
+@pytest.mark.parametrize("align_type,gap_model", COMBOS)
+@pytest.mark.parametrize("variant", ["auto", "i32", "f16x2"])
+def test_golden_vectors(ctx, align_type, gap_model, variant):
+    recs = [r for name in ("kat.json", "adversarial.json") for r in load_golden(name)]
+    recs += load_golden("random_small.json")["pairs"]
+    recs = [r for r in recs if r["align_type"] == align_type and r["gap_model"] == gap_model]
+    by_scheme = {}
+    for r in recs:
+        by_scheme.setdefault(tuple(r["scheme"]), []).append(r)
+    for sch, rs in by_scheme.items():
+        scheme = scheme_of(sch, gap_model)
+        if variant == "f16x2":
+            if gap_model == "affine" and not N.merged_state_exact(scheme):
+                continue
+            rs = [r for r in rs if N.f16_range_ok(scheme, len(r["q"]), len(r["s"])) and scheme.mismatch_score <= 0 <= scheme.match_score]
+            if not rs:
+                continue
+        qs = [codes(r["q"]) for r in rs]; ss = [codes(r["s"]) for r in rs]
+        got = gpu_scores(ctx, qs, ss, [(i, i) for i in range(len(rs))], scheme, align_type, variant)
+        want = (np.array([r["score"] for r in rs]), np.array([r["end"][0] for r in rs]), np.array([r["end"][1] for r in rs]))
+        assert (got[3] == 0).all()
+        assert_scores_equal(got, want, f"{align_type}/{gap_model}/{variant}/{sch}")
+
+
+@pytest.mark.parametrize("align_type,gap_model", COMBOS)
+def test_random_vs_oracle_all_variants(ctx, align_type, gap_model):
+    rng = np.random.default_rng(101)
+    pool = AFFINE_SCHEMES if gap_model == "affine" else LINEAR_SCHEMES
+    for k, sch in enumerate(pool):
+        scheme = scheme_of(sch, gap_model)
+        qs, ss, pairs = _random_batch(rng, 300, 1, 300, flagged=0.2)
+        want = oracle_scores(qs, ss, pairs, scheme, align_type)
+        for variant in ("auto", "i32"):
+            got = gpu_scores(ctx, qs, ss, pairs, scheme, align_type, variant)
+            assert_scores_equal(got, want, f"{align_type}/{gap_model}/{variant}/{sch}")
+
+
+@pytest.mark.parametrize("align_type,gap_model", COMBOS)
+def test_uniform_150bp_f16_equals_i32_equals_oracle(ctx, align_type, gap_model):
+    rng = np.random.default_rng(7)
+    scheme = scheme_of((2, -1, 2, 1) if gap_model == "affine" else (2, -1, 1, 1), gap_model)
+    n = 4001  # odd: the last packed unit has an empty half
+    qs = [random_codes(rng, 150) for _ in range(n)]
+    ss = [mutate_codes(rng, q)[:150] if i % 2 else random_codes(rng, 150) for i, q in enumerate(qs)]
+    ss = [np.concatenate([s, random_codes(rng, 150 - len(s))]) for s in ss]
+    pairs = [(i, i) for i in range(n)]
+    want = oracle_scores(qs, ss, pairs, scheme, align_type)
+    f16 = gpu_scores(ctx, qs, ss, pairs, scheme, align_type, "f16x2")
+    i32 = gpu_scores(ctx, qs, ss, pairs, scheme, align_type, "i32")
+    assert_scores_equal(f16, want, "f16x2")
+    assert_scores_equal(i32, want, "i32")
+
+
+@pytest.mark.parametrize("align_type", ["global", "local", "semiglobal"])
+def test_multi_stage_long_reads(ctx, align_type):
+    rng = np.random.default_rng(11)
+    scheme = scheme_of((2, -1, 2, 1), "affine")
+    qs, ss = [], []
+    for L in (700, 1500, 2500, 513, 512, 1025):
+        q = random_codes(rng, L)
+        qs.append(q); ss.append(mutate_codes(rng, q, 0.1, 0.05, 0.05))
+    qs.append(random_codes(rng, 40)); ss.append(random_codes(rng, 3000))
+    qs.append(random_codes(rng, 3000)); ss.append(random_codes(rng, 40))
+    pairs = [(i, i) for i in range(len(qs))]
+    want = oracle_scores(qs, ss, pairs, scheme, align_type)
+    got = gpu_scores(ctx, qs, ss, pairs, scheme, align_type, "auto")
+    assert_scores_equal(got, want, align_type)
+    lin = scheme_of((2, -1, 1, 1), "linear")
+    assert_scores_equal(gpu_scores(ctx, qs, ss, pairs, lin, align_type), oracle_scores(qs, ss, pairs, lin, align_type), "linear")
+
+
+def test_all_pairs_index_pools(ctx):
+    rng = np.random.default_rng(3)
+    qs = [random_codes(rng, int(rng.integers(20, 200))) for _ in range(9)]
+    ss = [random_codes(rng, int(rng.integers(20, 200))) for _ in range(7)]
+    pairs = [(a, b) for a in range(9) for b in range(7)]
+    scheme = scheme_of((2, -1, 2, 1), "affine")
+    for at in ("global", "local", "semiglobal"):
+        assert_scores_equal(gpu_scores(ctx, qs, ss, pairs, scheme, at), oracle_scores(qs, ss, pairs, scheme, at), at)
+
+
+def test_forced_f16_reports_range_status(ctx):
+    rng = np.random.default_rng(4)
+    scheme = scheme_of((2, -1, 2, 1), "affine")
+    qs = [random_codes(rng, 100), random_codes(rng, 900)]
+    ss = [random_codes(rng, 100), random_codes(rng, 900)]
+    got = gpu_scores(ctx, qs, ss, [(0, 0), (1, 1)], scheme, "local", "f16x2")
+    assert got[3][0] == 0 and got[3][1] == N.WSB_E_RANGE
+    with pytest.raises(ValueError):
+        gpu_scores(ctx, qs, ss, [(0, 0)], scheme_of((2, -9, 2, 1), "affine"), "local", "f16x2")
