@@ -77,6 +77,11 @@ struct ArI32 {
     }
     static __device__ __forceinline__ bool any_gt(V a, V b) { return a > b; }
     static __device__ __forceinline__ bool any_ge(V a, V b) { return a >= b; }
+    static __device__ __forceinline__ V codes(int a, int) { return a; }
+    static __device__ __forceinline__ unsigned gt_mask(V a, V b) { return a > b ? 0xffffu : 0u; }
+    static __device__ __forceinline__ unsigned ge_mask(V a, V b) { return a >= b ? 0xffffu : 0u; }
+    static __device__ __forceinline__ unsigned bits(V a) { return (unsigned)a; }
+    static __device__ __forceinline__ int get_bits(unsigned w, int) { return (int)w; }
 };
 
 struct ArF16 {
@@ -97,6 +102,21 @@ struct ArF16 {
     template <bool RELU> static __device__ __forceinline__ V max3(V a, V b, V c) { return __hmax2(__hmax2(a, b), c); }
     static __device__ __forceinline__ bool any_gt(V a, V b) { return __hgt2_mask(a, b) != 0u; }
     static __device__ __forceinline__ bool any_ge(V a, V b) { return __hge2_mask(a, b) != 0u; }
+    // symbol codes 0..7 as fp16 integers, both halves in ONE register (the barrier stops the compiler from keeping
+    // the halves apart and re-packing them with a PRMT per cell)
+    static __device__ __forceinline__ V codes(int a, int b) {
+        const unsigned lut_lo = 0x42403C00u, lut_hi = 0x47464544u;  // high bytes of fp16(0..3), fp16(4..7)
+        const unsigned ha = __byte_perm(lut_lo, lut_hi, a) & 0xffu, hb = __byte_perm(lut_lo, lut_hi, b) & 0xffu;
+        unsigned bits = (ha << 8) | (hb << 24);
+        asm volatile("" : "+r"(bits));
+        V v; *reinterpret_cast<unsigned*>(&v) = bits; return v;
+    }
+    static __device__ __forceinline__ unsigned gt_mask(V a, V b) { return __hgt2_mask(a, b); }  // 0xffff per half
+    static __device__ __forceinline__ unsigned ge_mask(V a, V b) { return __hge2_mask(a, b); }
+    static __device__ __forceinline__ unsigned bits(V a) { return *reinterpret_cast<unsigned*>(&a); }
+    static __device__ __forceinline__ int get_bits(unsigned w, int v) {
+        return __half2int_rn(__ushort_as_half((unsigned short)(v ? (w >> 16) : (w & 0xffffu))));
+    }
 };
 
 template <class V> struct alignas(2 * sizeof(V)) Pair2 { V a, b; };
@@ -132,7 +152,9 @@ __device__ __forceinline__ int edge_h(bool global_edges, int k, int alpha, int b
 }
 
 // ---------------------------------------------------------------- the kernel
-template <class AR, int P, int K, int ATYPE, int GAP>
+// MASKED (int32, local only): keep pad columns out of the row maximum explicitly, for schemes where a never-matching
+// pad could still raise a score (mismatch > 0 or match < 0); all other instantiations rely on pads being non-improving.
+template <class AR, int P, int K, int ATYPE, int GAP, bool MASKED = false>
 __global__ void __launch_bounds__(kThreads) score_kernel(const ScoreParams prm) {
     using V = typename AR::V;
     constexpr int NV = AR::NV;
@@ -141,7 +163,10 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const ScoreParams prm) 
     constexpr bool LOCAL = ATYPE == AT_LOCAL;
     constexpr bool GLOBAL_EDGES = ATYPE == AT_GLOBAL;
 
+    constexpr int NCH = (K + 3) / 4;   // 16-byte chunks per row snapshot
     __shared__ V qring[GPB][kQRing];
+    // local alignments: per thread and sub-alignment, the strip's h + mismatch row at its latest record
+    __shared__ uint4 snap[LOCAL ? AR::NV : 1][LOCAL ? NCH : 1][LOCAL ? kThreads : 1];
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
@@ -197,7 +222,11 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const ScoreParams prm) 
             best_i[v] = 0;
             best_j[v] = (ATYPE == AT_SEMI) ? n[v] : 0;
         }
-        V bestvec = AR::splat(0);
+        V bestvec = AR::splat(0);  // local: per-lane running best value (both sub-alignments)
+        int best_c0[NV];           // local: first column - 1 of the strip at the record
+#pragma unroll
+        for (int v = 0; v < NV; ++v) best_c0[v] = 0;
+        (void)bestvec; (void)best_c0;
 
         for (int st = 0; st < nstages; ++st) {
             // ---- (re)fill the query ring with rows 1..kQRing at the start of a stage
@@ -208,7 +237,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const ScoreParams prm) 
 #pragma unroll
                     for (int v = 0; v < NV; ++v)
                         if (x < m[v]) { const int code = qp[v][x]; c[v] = code < 4 ? code : kFlagQuery; }
-                    qring[gib][x] = AR::pack(c[0], c[1]);
+                    qring[gib][x] = AR::codes(c[0], c[1]);
                 }
                 __syncwarp();
             }
@@ -221,7 +250,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const ScoreParams prm) 
 #pragma unroll
                 for (int v = 0; v < NV; ++v)
                     if (col0 + c < n[v]) { const int x = sp[v][col0 + c]; code[v] = x < 4 ? x : kFlagSubject; }
-                sc[c] = AR::pack(code[0], code[1]);
+                sc[c] = AR::codes(code[0], code[1]);
                 const int h0 = edge_h(GLOBAL_EDGES, col0 + c + 1, alpha, beta);
                 T[c] = AR::splat(GAP == GAP_EXACT ? kNeg32 : h0);  // exact model: T[] unused, EP holds E - beta
                 HM[c] = AR::splat(h0 + mism);
@@ -263,7 +292,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const ScoreParams prm) 
 #pragma unroll
                             for (int v = 0; v < NV; ++v)
                                 if (row < m[v]) { const int code = qp[v][row]; c[v] = code < 4 ? code : kFlagQuery; }
-                            qring[gib][row & (kQRing - 1)] = AR::pack(c[0], c[1]);
+                            qring[gib][row & (kQRing - 1)] = AR::codes(c[0], c[1]);
                         }
                         __syncwarp();
                     }
@@ -295,32 +324,37 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const ScoreParams prm) 
                             T[c] = left;
                         }
                         HM[c] = AR::add(h, c_mism);
-                        if (LOCAL) rm = AR::vmax(rm, h);
+                        if (LOCAL) rm = AR::vmax(rm, (MASKED && col0 + c >= n[0]) ? AR::splat(kNeg32) : h);
                     }
                     out_t = left;
                     out_hm = HM[K - 1];
 
                     if (LOCAL) {
-                        // Rare path: some cell of this row beats the running best.  In later stages a tie can still
-                        // win when it sits in a smaller row than the best found so far (columns grow with the stage).
-                        bool trig = AR::any_gt(rm, bestvec);
-                        if (st > 0 && !trig && r < max(best_i[0], best_i[NV - 1])) trig = AR::any_ge(rm, bestvec);
-                        if (trig) {
+                        // Record rows: the strip's row maximum beats the lane's running best (in later stages a tie
+                        // also counts when it sits in a smaller row).  The row itself is parked in shared memory with
+                        // predicated 16-byte stores; the column is resolved once, after the last stage.  Pad cells
+                        // never exceed an earlier real cell, so a pad "record" can only displace a non-winning one.
+                        unsigned gtm = AR::gt_mask(rm, bestvec);
+                        if (st > 0) {
+                            const unsigned gem = AR::ge_mask(rm, bestvec);
 #pragma unroll
-                            for (int v = 0; v < NV; ++v) {
-                                if (r <= m[v]) {
-                                    int bv = kNeg32, bc = -1;
+                            for (int v = 0; v < NV; ++v) if (r < best_i[v]) gtm |= gem & (0xffffu << (16 * v));
+                        }
+                        bestvec = AR::vmax(bestvec, rm);
 #pragma unroll
-                                    for (int c = 0; c < K; ++c) {
-                                        const int hv = AR::get(HM[c], v) - mism;
-                                        if (col0 + c < n[v] && hv > bv) { bv = hv; bc = c; }
-                                    }
-                                    if (bc >= 0 && better_cell(bv, r, col0 + bc + 1, best_v[v], best_i[v], best_j[v])) {
-                                        best_v[v] = bv; best_i[v] = r; best_j[v] = col0 + bc + 1;
-                                    }
+                        for (int v = 0; v < NV; ++v) {
+                            if (gtm & (0xffffu << (16 * v))) {
+                                best_i[v] = r; best_c0[v] = col0;
+#pragma unroll
+                                for (int ch = 0; ch < NCH; ++ch) {
+                                    uint4 w;
+                                    w.x = AR::bits(HM[4 * ch]);
+                                    w.y = 4 * ch + 1 < K ? AR::bits(HM[4 * ch + 1]) : 0u;
+                                    w.z = 4 * ch + 2 < K ? AR::bits(HM[4 * ch + 2]) : 0u;
+                                    w.w = 4 * ch + 3 < K ? AR::bits(HM[4 * ch + 3]) : 0u;
+                                    snap[v][ch][tid] = w;
                                 }
                             }
-                            bestvec = AR::pack(best_v[0], best_v[NV - 1]);
                         }
                     } else {
 #pragma unroll
@@ -375,16 +409,39 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const ScoreParams prm) 
         // ---- reduce over the lanes of the group: max value, then smallest row, then smallest column
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
-            int bv = best_v[v], bi = best_i[v], bj = best_j[v];
+            int bv = LOCAL ? AR::get(bestvec, v) : best_v[v];
+            int bi = best_i[v];
+            int bj = LOCAL ? best_c0[v] : best_j[v];  // local: strips are disjoint, so the strip origin orders columns
+            int who = t;
 #pragma unroll
             for (int off = P / 2; off >= 1; off >>= 1) {
                 const int ov = __shfl_xor_sync(gmask, bv, off, P);
                 const int oi = __shfl_xor_sync(gmask, bi, off, P);
                 const int oj = __shfl_xor_sync(gmask, bj, off, P);
-                const bool take = ov > bv || (ov == bv && (oi < bi || (oi == bi && oj < bj)));
-                if (take) { bv = ov; bi = oi; bj = oj; }
+                const int ow = __shfl_xor_sync(gmask, who, off, P);
+                if (better_cell(ov, oi, oj, bv, bi, bj)) { bv = ov; bi = oi; bj = oj; who = ow; }
             }
-            if (t == 0 && pidx[v] >= 0) {
+            if (LOCAL) {
+                if (t == who && pidx[v] >= 0) {  // the winning lane finds the first column of its parked row
+                    int j = 0;
+                    if (bv > 0) {
+                        const int target = bv + mism;
+                        int pos = K;
+#pragma unroll
+                        for (int ch = NCH - 1; ch >= 0; --ch) {
+                            const uint4 w = snap[v][ch][tid];
+                            if (4 * ch + 3 < K && AR::get_bits(w.w, v) == target) pos = 4 * ch + 3;
+                            if (4 * ch + 2 < K && AR::get_bits(w.z, v) == target) pos = 4 * ch + 2;
+                            if (4 * ch + 1 < K && AR::get_bits(w.y, v) == target) pos = 4 * ch + 1;
+                            if (AR::get_bits(w.x, v) == target) pos = 4 * ch;
+                        }
+                        j = bj + pos + 1;
+                    } else { bi = 0; }
+                    prm.out_score[pidx[v]] = bv;
+                    prm.out_i[pidx[v]] = bi;
+                    prm.out_j[pidx[v]] = j;
+                }
+            } else if (t == 0 && pidx[v] >= 0) {
                 prm.out_score[pidx[v]] = bv;
                 prm.out_i[pidx[v]] = bi;
                 prm.out_j[pidx[v]] = bj;

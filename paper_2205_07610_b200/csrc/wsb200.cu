@@ -301,33 +301,35 @@ static int best_shape(const Shape* shapes, int m, int n) {
 
 using KernelFn = void (*)(const ScoreParams);
 
-template <class AR, int P, int K, int GAP> static KernelFn pick_atype(int atype) {
+template <class AR, int P, int K, int GAP> static KernelFn pick_atype(int atype, bool masked) {
     switch (atype) {
         case AT_GLOBAL: return score_kernel<AR, P, K, AT_GLOBAL, GAP>;
-        case AT_LOCAL: return score_kernel<AR, P, K, AT_LOCAL, GAP>;
+        case AT_LOCAL:
+            if constexpr (std::is_same<AR, ArI32>::value) { if (masked) return score_kernel<AR, P, K, AT_LOCAL, GAP, true>; }
+            return score_kernel<AR, P, K, AT_LOCAL, GAP>;
         default: return score_kernel<AR, P, K, AT_SEMI, GAP>;
     }
 }
 
-template <class AR, int P, int K> static KernelFn pick_gap(int atype, int gap) {
-    if (gap == GAP_LINEAR) return pick_atype<AR, P, K, GAP_LINEAR>(atype);
-    if (gap == GAP_MERGED) return pick_atype<AR, P, K, GAP_MERGED>(atype);
-    if constexpr (std::is_same<AR, ArI32>::value) return pick_atype<ArI32, P, K, GAP_EXACT>(atype);
+template <class AR, int P, int K> static KernelFn pick_gap(int atype, int gap, bool masked) {
+    if (gap == GAP_LINEAR) return pick_atype<AR, P, K, GAP_LINEAR>(atype, masked);
+    if (gap == GAP_MERGED) return pick_atype<AR, P, K, GAP_MERGED>(atype, masked);
+    if constexpr (std::is_same<AR, ArI32>::value) return pick_atype<ArI32, P, K, GAP_EXACT>(atype, masked);
     return nullptr;  // the packed kernels have no exact three-state model
 }
 
-static KernelFn pick_kernel(int variant, int shape, int atype, int gap) {
+static KernelFn pick_kernel(int variant, int shape, int atype, int gap, bool masked) {
     if (variant == WSB_VARIANT_F16X2) {
         switch (shape) {
-            case 0: return pick_gap<ArF16, 4, 16>(atype, gap);
-            case 1: return pick_gap<ArF16, 8, 19>(atype, gap);
-            default: return pick_gap<ArF16, 8, 32>(atype, gap);
+            case 0: return pick_gap<ArF16, 4, 16>(atype, gap, masked);
+            case 1: return pick_gap<ArF16, 8, 19>(atype, gap, masked);
+            default: return pick_gap<ArF16, 8, 32>(atype, gap, masked);
         }
     }
     switch (shape) {
-        case 0: return pick_gap<ArI32, 8, 16>(atype, gap);
-        case 1: return pick_gap<ArI32, 16, 16>(atype, gap);
-        default: return pick_gap<ArI32, 32, 16>(atype, gap);
+        case 0: return pick_gap<ArI32, 8, 16>(atype, gap, masked);
+        case 1: return pick_gap<ArI32, 16, 16>(atype, gap, masked);
+        default: return pick_gap<ArI32, 32, 16>(atype, gap, masked);
     }
 }
 
@@ -471,7 +473,7 @@ extern "C" int wsb_batch_score(wsb_batch* b, const wsb_scheme* sch, int atype, i
     size_t bnd_need = 0;
     for (const LaunchGroup& g : plan.groups) {
         const Shape sh = g.variant == WSB_VARIANT_F16X2 ? kShapesF16[g.shape] : kShapesI32[g.shape];
-        KernelFn fn = pick_kernel(g.variant, g.shape, atype, g.gap);
+        KernelFn fn = pick_kernel(g.variant, g.shape, atype, g.gap, sch->mismatch > 0 || sch->match < 0);
         if (!fn) return WSB_E_SCHEME;
         int per_sm = 0;
         CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, 0));
