@@ -151,6 +151,12 @@ __device__ __forceinline__ int edge_h(bool global_edges, int k, int alpha, int b
     return (global_edges && k >= 1) ? -(alpha + beta * (k - 1)) : 0;
 }
 
+// dynamic shared memory of one block of score_kernel<AR, P, K, ATYPE, ...>
+template <class AR, int P, int K, int ATYPE> constexpr size_t score_smem_bytes() {
+    return (ATYPE == AT_LOCAL ? (size_t)AR::NV * ((K + 3) / 4) * kThreads * 16 : 0) +
+           (size_t)(kThreads / P) * kQRing * sizeof(typename AR::V);
+}
+
 // ---------------------------------------------------------------- the kernel
 // MASKED (int32, local only): keep pad columns out of the row maximum explicitly, for schemes where a never-matching
 // pad could still raise a score (mismatch > 0 or match < 0); all other instantiations rely on pads being non-improving.
@@ -164,9 +170,11 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const ScoreParams prm) 
     constexpr bool GLOBAL_EDGES = ATYPE == AT_GLOBAL;
 
     constexpr int NCH = (K + 3) / 4;   // 16-byte chunks per row snapshot
-    __shared__ V qring[GPB][kQRing];
+    // dynamic shared memory (see score_smem_bytes): row snapshots first (16-byte aligned), then the query rings
+    extern __shared__ uint4 smem_dyn[];
     // local alignments: per thread and sub-alignment, the strip's h + mismatch row at its latest record
-    __shared__ uint4 snap[LOCAL ? AR::NV : 1][LOCAL ? NCH : 1][LOCAL ? kThreads : 1];
+    uint4 (*snap)[NCH][kThreads] = reinterpret_cast<uint4 (*)[NCH][kThreads]>(smem_dyn);
+    V (*qring)[kQRing] = reinterpret_cast<V (*)[kQRing]>(smem_dyn + (LOCAL ? AR::NV * NCH * kThreads : 0));
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
@@ -260,15 +268,12 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const ScoreParams prm) 
             const V hm0 = AR::splat(edge_h(GLOBAL_EDGES, col0, alpha, beta) + mism);  // HM(0, col0): diagonal of row 1
             V hm_diag = hm0;
             V tl = AR::neg_inf(), hml = AR::neg_inf();
+            // stage 0: (T, HM) of the matrix' left border at the row lane 0 computes next
+            V edge_hm = AR::splat(edge_h(GLOBAL_EDGES, 1, alpha, beta) + mism);
+            V edge_t = (GAP == GAP_EXACT) ? AR::neg_inf() : AR::splat(edge_h(GLOBAL_EDGES, 1, alpha, beta));
             if (t == 0) {  // left border values for row 1
-                if (st == 0) {
-                    const int h = edge_h(GLOBAL_EDGES, 1, alpha, beta);
-                    hml = AR::splat(h + mism);
-                    tl = (GAP == GAP_EXACT) ? AR::neg_inf() : AR::splat(h);
-                } else {
-                    const Pair2<V> b = bnd[1];
-                    tl = b.a; hml = b.b;
-                }
+                if (st == 0) { tl = edge_t; hml = edge_hm; }
+                else { const Pair2<V> b = bnd[1]; tl = b.a; hml = b.b; }
             }
             // per-sub-alignment location of column n inside this stage (semiglobal / global capture)
             int cap_c[NV];
@@ -282,7 +287,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const ScoreParams prm) 
             for (int it = 1; it <= it_end; ++it) {
                 const int r = it - t;
                 // ring refill: rows [base+1, base+kQHalf] replace rows that every lane has passed
-                if (it > P && ((it - P) & (kQHalf - 1)) == 0) {
+                if (mm_w > kQRing && it > P && ((it - P) & (kQHalf - 1)) == 0) {
                     const int base = ((it - P) / kQHalf + 1) * kQHalf;  // first 0-based row index to fill
                     if (base < mm_w) {
                         __syncwarp();
@@ -386,19 +391,18 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const ScoreParams prm) 
                     }
                 }
                 // hand the strip's right-most column to the next lane; lane 0 takes the stage's left border
-                V nt = shfl_up_v<V>(gmask, out_t, P);
-                V nhm = shfl_up_v<V>(gmask, out_hm, P);
+                V nt = shfl_up_v<V>(0xffffffffu, out_t, P);
+                V nhm = shfl_up_v<V>(0xffffffffu, out_hm, P);
                 hm_diag = hml;
-                if (t == 0) {
-                    const int rn = r + 1;  // row lane 0 computes next
-                    if (st == 0) {
-                        const int h = edge_h(GLOBAL_EDGES, rn, alpha, beta);
-                        nhm = AR::splat(h + mism);
-                        nt = (GAP == GAP_EXACT) ? AR::neg_inf() : AR::splat(h);
-                    } else if (rn <= mm) {
-                        const Pair2<V> b = bnd[rn];
-                        nt = b.a; nhm = b.b;
+                if (st == 0) {  // warp-uniform: left border of the matrix, H(i, 0) walks down by beta per row
+                    if (GLOBAL_EDGES) {
+                        if (GAP != GAP_EXACT) edge_t = AR::add(edge_t, c_nbeta);
+                        edge_hm = AR::add(edge_hm, c_nbeta);
                     }
+                    if (t == 0) { nt = edge_t; nhm = edge_hm; }
+                } else if (t == 0 && r + 1 <= mm) {
+                    const Pair2<V> b = bnd[r + 1];
+                    nt = b.a; nhm = b.b;
                 }
                 tl = nt; hml = nhm;
                 if (r == 0) hm_diag = hm0;

@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <new>
@@ -278,10 +279,11 @@ extern "C" int64_t wsb_batch_total_cells(const wsb_batch* b) { return b ? b->tot
 // ------------------------------------------------------------------------------------------------ kernel shapes
 struct Shape { int P, K; };
 // packed half2 shapes: short reads in a single stage; (8,32) also chains stages for longer packed reads
-static const Shape kShapesF16[] = {{4, 16}, {8, 19}, {8, 32}};
+static const Shape kShapesF16[] = {{4, 16}, {8, 19}, {8, 32}, {4, 38}};
 // int32 shapes: narrow groups for short reads, full warps with wide stages for long reads
 static const Shape kShapesI32[] = {{8, 16}, {16, 16}, {32, 16}};
-constexpr int kNumShapes = 3;
+constexpr int kNumShapesF16 = 4, kNumShapesI32 = 3;
+constexpr int kNumShapes = 4;  // bucket array bound
 
 static double padded_cost(const Shape& s, int m, int n) {
     const int w = s.P * s.K;
@@ -289,10 +291,12 @@ static double padded_cost(const Shape& s, int m, int n) {
     return (double)(m + s.P - 1) * stages * w;
 }
 
-static int best_shape(const Shape* shapes, int m, int n) {
+static int best_shape(const Shape* shapes, int count, int m, int n) {
+    static const char* force = getenv("WSB_FORCE_SHAPE");  // tuning aid: index into the shape table
+    if (force && force[0]) return std::min(count - 1, std::max(0, atoi(force)));
     int best = 0;
     double bc = padded_cost(shapes[0], m, n);
-    for (int k = 1; k < kNumShapes; ++k) {
+    for (int k = 1; k < count; ++k) {
         const double c = padded_cost(shapes[k], m, n);
         if (c < bc) { bc = c; best = k; }
     }
@@ -300,30 +304,34 @@ static int best_shape(const Shape* shapes, int m, int n) {
 }
 
 using KernelFn = void (*)(const ScoreParams);
+struct KernelSel { KernelFn fn; size_t smem; };
 
-template <class AR, int P, int K, int GAP> static KernelFn pick_atype(int atype, bool masked) {
+template <class AR, int P, int K, int GAP> static KernelSel pick_atype(int atype, bool masked) {
     switch (atype) {
-        case AT_GLOBAL: return score_kernel<AR, P, K, AT_GLOBAL, GAP>;
+        case AT_GLOBAL: return {score_kernel<AR, P, K, AT_GLOBAL, GAP>, score_smem_bytes<AR, P, K, AT_GLOBAL>()};
         case AT_LOCAL:
-            if constexpr (std::is_same<AR, ArI32>::value) { if (masked) return score_kernel<AR, P, K, AT_LOCAL, GAP, true>; }
-            return score_kernel<AR, P, K, AT_LOCAL, GAP>;
-        default: return score_kernel<AR, P, K, AT_SEMI, GAP>;
+            if constexpr (std::is_same<AR, ArI32>::value) {
+                if (masked) return {score_kernel<AR, P, K, AT_LOCAL, GAP, true>, score_smem_bytes<AR, P, K, AT_LOCAL>()};
+            }
+            return {score_kernel<AR, P, K, AT_LOCAL, GAP>, score_smem_bytes<AR, P, K, AT_LOCAL>()};
+        default: return {score_kernel<AR, P, K, AT_SEMI, GAP>, score_smem_bytes<AR, P, K, AT_SEMI>()};
     }
 }
 
-template <class AR, int P, int K> static KernelFn pick_gap(int atype, int gap, bool masked) {
+template <class AR, int P, int K> static KernelSel pick_gap(int atype, int gap, bool masked) {
     if (gap == GAP_LINEAR) return pick_atype<AR, P, K, GAP_LINEAR>(atype, masked);
     if (gap == GAP_MERGED) return pick_atype<AR, P, K, GAP_MERGED>(atype, masked);
     if constexpr (std::is_same<AR, ArI32>::value) return pick_atype<ArI32, P, K, GAP_EXACT>(atype, masked);
-    return nullptr;  // the packed kernels have no exact three-state model
+    return {nullptr, 0};  // the packed kernels have no exact three-state model
 }
 
-static KernelFn pick_kernel(int variant, int shape, int atype, int gap, bool masked) {
+static KernelSel pick_kernel(int variant, int shape, int atype, int gap, bool masked) {
     if (variant == WSB_VARIANT_F16X2) {
         switch (shape) {
             case 0: return pick_gap<ArF16, 4, 16>(atype, gap, masked);
             case 1: return pick_gap<ArF16, 8, 19>(atype, gap, masked);
-            default: return pick_gap<ArF16, 8, 32>(atype, gap, masked);
+            case 2: return pick_gap<ArF16, 8, 32>(atype, gap, masked);
+            default: return pick_gap<ArF16, 4, 38>(atype, gap, masked);
         }
     }
     switch (shape) {
@@ -357,8 +365,8 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
         if ((int64_t)ms * ((int64_t)m + n) >= (1ll << 29)) { status = WSB_E_LENGTH; return; }
         const bool fits = f16_scheme_ok && wsb_f16_range_ok(sch, m, n);
         if (variant == WSB_VARIANT_F16X2 && !fits) { status = WSB_E_RANGE; return; }
-        if (variant != WSB_VARIANT_I32 && fits) { var = WSB_VARIANT_F16X2; shape = best_shape(kShapesF16, m, n); }
-        else { var = WSB_VARIANT_I32; shape = best_shape(kShapesI32, m, n); }
+        if (variant != WSB_VARIANT_I32 && fits) { var = WSB_VARIANT_F16X2; shape = best_shape(kShapesF16, kNumShapesF16, m, n); }
+        else { var = WSB_VARIANT_I32; shape = best_shape(kShapesI32, kNumShapesI32, m, n); }
     };
 
     if (b->uniform) {
@@ -468,22 +476,24 @@ extern "C" int wsb_batch_score(wsb_batch* b, const wsb_scheme* sch, int atype, i
     b->last_plan = &plan;
 
     // launch geometry + border scratch
-    struct Geo { KernelFn fn; int grid; int64_t bnd_rows; };
+    struct Geo { KernelFn fn; size_t smem; int grid; int64_t bnd_rows; };
     std::vector<Geo> geo;
     size_t bnd_need = 0;
     for (const LaunchGroup& g : plan.groups) {
         const Shape sh = g.variant == WSB_VARIANT_F16X2 ? kShapesF16[g.shape] : kShapesI32[g.shape];
-        KernelFn fn = pick_kernel(g.variant, g.shape, atype, g.gap, sch->mismatch > 0 || sch->match < 0);
+        const KernelSel sel = pick_kernel(g.variant, g.shape, atype, g.gap, sch->mismatch > 0 || sch->match < 0);
+        KernelFn fn = sel.fn;
         if (!fn) return WSB_E_SCHEME;
+        CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel.smem));
         int per_sm = 0;
-        CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, 0));
+        CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, sel.smem));
         per_sm = std::max(per_sm, 1);
         const int gpb = kThreads / sh.P;
         const int64_t blocks_needed = (g.n_units + gpb - 1) / gpb;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(blocks_needed, (int64_t)ctx->sm_count * per_sm));
         const bool multi_stage = g.max_n > sh.P * sh.K;
         const int64_t rows = multi_stage ? (int64_t)g.max_m + 2 : 0;
-        geo.push_back({fn, grid, rows});
+        geo.push_back({fn, sel.smem, grid, rows});
         bnd_need = std::max(bnd_need, (size_t)rows * 8u * (size_t)grid * gpb);
     }
     if (bnd_need > b->bnd_bytes) {
@@ -505,7 +515,7 @@ extern "C" int wsb_batch_score(wsb_batch* b, const wsb_scheme* sch, int atype, i
         prm.out_score = b->d_score; prm.out_i = b->d_i; prm.out_j = b->d_j;
         prm.match = sch->match; prm.mismatch = sch->mismatch; prm.alpha = sch->gap_open; prm.beta = beta_eff;
         prm.bnd = geo[k].bnd_rows ? b->d_bnd : nullptr; prm.bnd_rows = geo[k].bnd_rows;
-        geo[k].fn<<<geo[k].grid, kThreads, 0, ctx->stream>>>(prm);
+        geo[k].fn<<<geo[k].grid, kThreads, geo[k].smem, ctx->stream>>>(prm);
         CUDA_TRY(ctx, cudaGetLastError());
         ++launches;
     }
