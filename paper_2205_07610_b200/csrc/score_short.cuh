@@ -1,0 +1,366 @@
+// score_short.cuh -- the hot kernel: packed half2 LOCAL scoring of short reads that fit one stage.
+//
+// Same lane-group wavefront as score_kernels.cuh (lane t owns K columns, row r = it - t at iteration it, two
+// independent alignments in the halves of every register) but specialised for the case that carries the headline
+// benchmark (150 bp / 250 bp reads, local alignment): the whole subject fits P*K columns, the whole query fits the
+// shared-memory query buffer, and the 0 floor of local alignment makes the edge state a fixed point, so
+//   * there is no stage loop, no border scratch, no ring refill;
+//   * no lane ever idles or branches on "is my row inside the matrix": rows above row 1 and below row m are computed
+//     with a never-matching pad symbol, which keeps the all-zero edge state unchanged above the matrix and cannot
+//     produce a record below it (pads only lose score: mismatch <= 0, gaps cost >= 0 -- checked by the planner);
+//   * the per-row work beside the K cell updates is: one shared-memory load (query symbols), two shuffles, the
+//     record test and its predicated snapshot stores.
+//
+// Cell update, per packed pair of cells (reference semantics: _kernels.py:259-276 merged affine, :113-126 linear):
+//     eq = (q == s)                      HSET2.BF.EQ      ALU
+//     d  = max(hm_diag + delta*eq, 0)    HFMA2.RELU       FMA      hm = h + mismatch, so this is H_diag + sigma
+//     g  = max(T_up, T_left)             HMNMX2           ALU
+//     h  = max(g - alpha, d)             HADD2 + HMNMX2   FMA+ALU
+//     T  = max(g - gamma, d)             HADD2 + HMNMX2   FMA+ALU  gamma = min(alpha, beta)   (linear: T = h)
+//     hm = h + mismatch                  HADD2            FMA
+//     rm = max(rm, h)                    VHMNMX per 2     ALU
+#pragma once
+#include "score_kernels.cuh"
+
+namespace wsb {
+
+constexpr int kShortQRows = 320;  // query rows the short kernel can hold per lane group (>= 250 bp reads + P pads)
+
+template <int P, int K> constexpr size_t short_smem_bytes() {
+    return (size_t)2 * ((K + 3) / 4) * kThreads * 16 + (size_t)(kThreads / P) * kShortQRows * 4;
+}
+
+__device__ __forceinline__ unsigned h2u(__half2 v) { return *reinterpret_cast<unsigned*>(&v); }
+__device__ __forceinline__ __half2 u2h(unsigned v) { return *reinterpret_cast<__half2*>(&v); }
+
+// Record test + snapshot for both halves: if rm.half > best.half, park the strip's hm row (16-byte chunks, one chunk
+// every kThreads*16 = 2048 bytes) in that half's snapshot area and remember the iteration.  One SETP yields both
+// predicates; the stores and the two moves are predicated, so a row without a record costs issue slots only.
+static_assert(kThreads * 16 == 2048, "chunk stride is baked into the store offsets below");
+template <int NC, bool REC>
+__device__ __forceinline__ void record_chunks(const unsigned* w, unsigned rm, unsigned best, unsigned addr_p,
+                                              unsigned addr_q, int it, int& rec0, int& rec1) {
+    static_assert(NC >= 1 && NC <= 5, "chunk group size");
+    if constexpr (NC == 1 && REC) {
+        asm volatile(
+            "{\n\t.reg .pred p, q;\n\t"
+            "setp.gt.f16x2 p|q, %2, %3;\n\t"
+            "@p st.shared.v4.b32 [%4+0], {%6, %7, %8, %9};\n\t"
+            "@q st.shared.v4.b32 [%5+0], {%6, %7, %8, %9};\n\t"
+            "@p mov.b32 %0, %10;\n\t"
+            "@q mov.b32 %1, %10;\n\t"
+            "}\n"
+            : "+r"(rec0), "+r"(rec1)
+            : "r"(rm), "r"(best), "r"(addr_p), "r"(addr_q), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(it)
+            : "memory");
+    }
+    if constexpr (NC == 1 && !REC) {
+        asm volatile(
+            "{\n\t.reg .pred p, q;\n\t"
+            "setp.gt.f16x2 p|q, %0, %1;\n\t"
+            "@p st.shared.v4.b32 [%2+0], {%4, %5, %6, %7};\n\t"
+            "@q st.shared.v4.b32 [%3+0], {%4, %5, %6, %7};\n\t"
+            "}\n"
+            : 
+            : "r"(rm), "r"(best), "r"(addr_p), "r"(addr_q), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+            : "memory");
+    }
+    if constexpr (NC == 2 && REC) {
+        asm volatile(
+            "{\n\t.reg .pred p, q;\n\t"
+            "setp.gt.f16x2 p|q, %2, %3;\n\t"
+            "@p st.shared.v4.b32 [%4+0], {%6, %7, %8, %9};\n\t"
+            "@q st.shared.v4.b32 [%5+0], {%6, %7, %8, %9};\n\t"
+            "@p st.shared.v4.b32 [%4+2048], {%10, %11, %12, %13};\n\t"
+            "@q st.shared.v4.b32 [%5+2048], {%10, %11, %12, %13};\n\t"
+            "@p mov.b32 %0, %14;\n\t"
+            "@q mov.b32 %1, %14;\n\t"
+            "}\n"
+            : "+r"(rec0), "+r"(rec1)
+            : "r"(rm), "r"(best), "r"(addr_p), "r"(addr_q), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]), "r"(it)
+            : "memory");
+    }
+    if constexpr (NC == 2 && !REC) {
+        asm volatile(
+            "{\n\t.reg .pred p, q;\n\t"
+            "setp.gt.f16x2 p|q, %0, %1;\n\t"
+            "@p st.shared.v4.b32 [%2+0], {%4, %5, %6, %7};\n\t"
+            "@q st.shared.v4.b32 [%3+0], {%4, %5, %6, %7};\n\t"
+            "@p st.shared.v4.b32 [%2+2048], {%8, %9, %10, %11};\n\t"
+            "@q st.shared.v4.b32 [%3+2048], {%8, %9, %10, %11};\n\t"
+            "}\n"
+            : 
+            : "r"(rm), "r"(best), "r"(addr_p), "r"(addr_q), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+            : "memory");
+    }
+    if constexpr (NC == 3 && REC) {
+        asm volatile(
+            "{\n\t.reg .pred p, q;\n\t"
+            "setp.gt.f16x2 p|q, %2, %3;\n\t"
+            "@p st.shared.v4.b32 [%4+0], {%6, %7, %8, %9};\n\t"
+            "@q st.shared.v4.b32 [%5+0], {%6, %7, %8, %9};\n\t"
+            "@p st.shared.v4.b32 [%4+2048], {%10, %11, %12, %13};\n\t"
+            "@q st.shared.v4.b32 [%5+2048], {%10, %11, %12, %13};\n\t"
+            "@p st.shared.v4.b32 [%4+4096], {%14, %15, %16, %17};\n\t"
+            "@q st.shared.v4.b32 [%5+4096], {%14, %15, %16, %17};\n\t"
+            "@p mov.b32 %0, %18;\n\t"
+            "@q mov.b32 %1, %18;\n\t"
+            "}\n"
+            : "+r"(rec0), "+r"(rec1)
+            : "r"(rm), "r"(best), "r"(addr_p), "r"(addr_q), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]), "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(it)
+            : "memory");
+    }
+    if constexpr (NC == 3 && !REC) {
+        asm volatile(
+            "{\n\t.reg .pred p, q;\n\t"
+            "setp.gt.f16x2 p|q, %0, %1;\n\t"
+            "@p st.shared.v4.b32 [%2+0], {%4, %5, %6, %7};\n\t"
+            "@q st.shared.v4.b32 [%3+0], {%4, %5, %6, %7};\n\t"
+            "@p st.shared.v4.b32 [%2+2048], {%8, %9, %10, %11};\n\t"
+            "@q st.shared.v4.b32 [%3+2048], {%8, %9, %10, %11};\n\t"
+            "@p st.shared.v4.b32 [%2+4096], {%12, %13, %14, %15};\n\t"
+            "@q st.shared.v4.b32 [%3+4096], {%12, %13, %14, %15};\n\t"
+            "}\n"
+            : 
+            : "r"(rm), "r"(best), "r"(addr_p), "r"(addr_q), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]), "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11])
+            : "memory");
+    }
+    if constexpr (NC == 4 && REC) {
+        asm volatile(
+            "{\n\t.reg .pred p, q;\n\t"
+            "setp.gt.f16x2 p|q, %2, %3;\n\t"
+            "@p st.shared.v4.b32 [%4+0], {%6, %7, %8, %9};\n\t"
+            "@q st.shared.v4.b32 [%5+0], {%6, %7, %8, %9};\n\t"
+            "@p st.shared.v4.b32 [%4+2048], {%10, %11, %12, %13};\n\t"
+            "@q st.shared.v4.b32 [%5+2048], {%10, %11, %12, %13};\n\t"
+            "@p st.shared.v4.b32 [%4+4096], {%14, %15, %16, %17};\n\t"
+            "@q st.shared.v4.b32 [%5+4096], {%14, %15, %16, %17};\n\t"
+            "@p st.shared.v4.b32 [%4+6144], {%18, %19, %20, %21};\n\t"
+            "@q st.shared.v4.b32 [%5+6144], {%18, %19, %20, %21};\n\t"
+            "@p mov.b32 %0, %22;\n\t"
+            "@q mov.b32 %1, %22;\n\t"
+            "}\n"
+            : "+r"(rec0), "+r"(rec1)
+            : "r"(rm), "r"(best), "r"(addr_p), "r"(addr_q), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]), "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15]), "r"(it)
+            : "memory");
+    }
+    if constexpr (NC == 4 && !REC) {
+        asm volatile(
+            "{\n\t.reg .pred p, q;\n\t"
+            "setp.gt.f16x2 p|q, %0, %1;\n\t"
+            "@p st.shared.v4.b32 [%2+0], {%4, %5, %6, %7};\n\t"
+            "@q st.shared.v4.b32 [%3+0], {%4, %5, %6, %7};\n\t"
+            "@p st.shared.v4.b32 [%2+2048], {%8, %9, %10, %11};\n\t"
+            "@q st.shared.v4.b32 [%3+2048], {%8, %9, %10, %11};\n\t"
+            "@p st.shared.v4.b32 [%2+4096], {%12, %13, %14, %15};\n\t"
+            "@q st.shared.v4.b32 [%3+4096], {%12, %13, %14, %15};\n\t"
+            "@p st.shared.v4.b32 [%2+6144], {%16, %17, %18, %19};\n\t"
+            "@q st.shared.v4.b32 [%3+6144], {%16, %17, %18, %19};\n\t"
+            "}\n"
+            : 
+            : "r"(rm), "r"(best), "r"(addr_p), "r"(addr_q), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]), "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15])
+            : "memory");
+    }
+    if constexpr (NC == 5 && REC) {
+        asm volatile(
+            "{\n\t.reg .pred p, q;\n\t"
+            "setp.gt.f16x2 p|q, %2, %3;\n\t"
+            "@p st.shared.v4.b32 [%4+0], {%6, %7, %8, %9};\n\t"
+            "@q st.shared.v4.b32 [%5+0], {%6, %7, %8, %9};\n\t"
+            "@p st.shared.v4.b32 [%4+2048], {%10, %11, %12, %13};\n\t"
+            "@q st.shared.v4.b32 [%5+2048], {%10, %11, %12, %13};\n\t"
+            "@p st.shared.v4.b32 [%4+4096], {%14, %15, %16, %17};\n\t"
+            "@q st.shared.v4.b32 [%5+4096], {%14, %15, %16, %17};\n\t"
+            "@p st.shared.v4.b32 [%4+6144], {%18, %19, %20, %21};\n\t"
+            "@q st.shared.v4.b32 [%5+6144], {%18, %19, %20, %21};\n\t"
+            "@p st.shared.v4.b32 [%4+8192], {%22, %23, %24, %25};\n\t"
+            "@q st.shared.v4.b32 [%5+8192], {%22, %23, %24, %25};\n\t"
+            "@p mov.b32 %0, %26;\n\t"
+            "@q mov.b32 %1, %26;\n\t"
+            "}\n"
+            : "+r"(rec0), "+r"(rec1)
+            : "r"(rm), "r"(best), "r"(addr_p), "r"(addr_q), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]), "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15]), "r"(w[16]), "r"(w[17]), "r"(w[18]), "r"(w[19]), "r"(it)
+            : "memory");
+    }
+    if constexpr (NC == 5 && !REC) {
+        asm volatile(
+            "{\n\t.reg .pred p, q;\n\t"
+            "setp.gt.f16x2 p|q, %0, %1;\n\t"
+            "@p st.shared.v4.b32 [%2+0], {%4, %5, %6, %7};\n\t"
+            "@q st.shared.v4.b32 [%3+0], {%4, %5, %6, %7};\n\t"
+            "@p st.shared.v4.b32 [%2+2048], {%8, %9, %10, %11};\n\t"
+            "@q st.shared.v4.b32 [%3+2048], {%8, %9, %10, %11};\n\t"
+            "@p st.shared.v4.b32 [%2+4096], {%12, %13, %14, %15};\n\t"
+            "@q st.shared.v4.b32 [%3+4096], {%12, %13, %14, %15};\n\t"
+            "@p st.shared.v4.b32 [%2+6144], {%16, %17, %18, %19};\n\t"
+            "@q st.shared.v4.b32 [%3+6144], {%16, %17, %18, %19};\n\t"
+            "@p st.shared.v4.b32 [%2+8192], {%20, %21, %22, %23};\n\t"
+            "@q st.shared.v4.b32 [%3+8192], {%20, %21, %22, %23};\n\t"
+            "}\n"
+            : 
+            : "r"(rm), "r"(best), "r"(addr_p), "r"(addr_q), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]), "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15]), "r"(w[16]), "r"(w[17]), "r"(w[18]), "r"(w[19])
+            : "memory");
+    }
+}
+
+template <int K> __device__ __forceinline__ void record_rows(const __half2 (&hm)[K], __half2 rm, __half2 best,
+                                                             unsigned snap_addr, int it, int& rec0, int& rec1) {
+    constexpr int NCH = (K + 3) / 4;
+    unsigned w[NCH * 4];
+#pragma unroll
+    for (int c = 0; c < NCH * 4; ++c) w[c] = c < K ? h2u(hm[c]) : 0u;
+    constexpr int FIRST = NCH < 5 ? NCH : 5;
+    constexpr unsigned HS = NCH * kThreads * 16;  // byte distance between the two halves' snapshot areas
+    record_chunks<FIRST, true>(w, h2u(rm), h2u(best), snap_addr, snap_addr + HS, it, rec0, rec1);
+    if constexpr (NCH > 5) {
+        constexpr int SECOND = NCH - 5 < 5 ? NCH - 5 : 5;
+        record_chunks<SECOND, false>(w + 20, h2u(rm), h2u(best), snap_addr + 5 * 2048, snap_addr + HS + 5 * 2048, it, rec0, rec1);
+        static_assert(NCH <= 10, "strip too wide for the snapshot helper");
+    }
+}
+
+template <int P, int K, int GAP>
+__global__ void __launch_bounds__(kThreads) f16_local_short_kernel(const ScoreParams prm) {
+    using AR = ArF16;
+    constexpr int GPB = kThreads / P;
+    constexpr int NCH = (K + 3) / 4;
+    extern __shared__ uint4 smem_dyn[];
+    uint4 (*snap)[NCH][kThreads] = reinterpret_cast<uint4 (*)[NCH][kThreads]>(smem_dyn);
+    __half2 (*qbuf)[kShortQRows] = reinterpret_cast<__half2 (*)[kShortQRows]>(smem_dyn + 2 * NCH * kThreads);
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int t = tid & (P - 1);
+    const int gib = tid / P;
+    const unsigned gmask = group_mask<P>(lane);
+    const int64_t group_global = (int64_t)blockIdx.x * GPB + gib;
+    const int64_t n_groups = (int64_t)gridDim.x * GPB;
+    const unsigned snap_addr = (unsigned)__cvta_generic_to_shared(&snap[0][0][tid]);
+
+    const int mism = prm.mismatch;
+    const __half2 c_delta = AR::splat(prm.match - prm.mismatch);
+    const __half2 c_mism = AR::splat(mism);
+    const __half2 c_nalpha = AR::splat(-prm.alpha);
+    const __half2 c_ngamma = AR::splat(-min(prm.alpha, prm.beta));
+    const __half2 c_zero = AR::splat(0);
+    const int col0 = t * K;
+
+    const int64_t rounds = (prm.n_units + n_groups - 1) / n_groups;
+    for (int64_t rd = 0; rd < rounds; ++rd) {
+        const int64_t u = rd * n_groups + group_global;
+        int pidx[2], m[2], n[2];
+        const uint8_t* qp[2];
+        const uint8_t* sp[2];
+        int mm = 0;
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+            int p = -1;
+            if (u < prm.n_units) {
+                if (prm.units) p = prm.units[u * 2 + v];
+                else { const int64_t pp = u * 2 + v; p = pp < prm.n_pairs ? (int)pp : -1; }
+            }
+            pidx[v] = p; m[v] = 0; n[v] = 0; qp[v] = nullptr; sp[v] = nullptr;
+            if (p >= 0) {
+                const int a = prm.pair_q[p], b = prm.pair_s[p];
+                m[v] = prm.q_len[a]; n[v] = prm.s_len[b];
+                qp[v] = prm.q_codes + prm.q_off[a];
+                sp[v] = prm.s_codes + prm.s_off[b];
+            }
+            mm = max(mm, m[v]);
+        }
+        const int mm_w = __reduce_max_sync(0xffffffffu, mm);
+        if (mm_w == 0) continue;
+
+        // query buffer: P pad rows, then the rows of both queries, pad rows up to the warp's longest query
+        __syncwarp();
+        for (int x = t; x < mm_w + 2 * P; x += P) {  // rows up to mm_w + P - 1 are read during the ramp-down
+            const int row = x - P;
+            int c[2] = {kPadQuery, kPadQuery};
+#pragma unroll
+            for (int v = 0; v < 2; ++v)
+                if (row >= 0 && row < m[v]) { const int code = qp[v][row]; c[v] = code < 4 ? code : kFlagQuery; }
+            qbuf[gib][x] = AR::codes(c[0], c[1]);
+        }
+        __half2 sc[K], T[K], HM[K];
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+            int code[2] = {kPadSubject, kPadSubject};
+#pragma unroll
+            for (int v = 0; v < 2; ++v)
+                if (col0 + c < n[v]) { const int x = sp[v][col0 + c]; code[v] = x < 4 ? x : kFlagSubject; }
+            sc[c] = AR::codes(code[0], code[1]);
+            T[c] = c_zero;
+            HM[c] = c_mism;
+        }
+        __syncwarp();
+
+        __half2 tl = c_zero, hml = c_mism, hm_diag = c_mism, bestvec = c_zero;
+        int rec0 = 0, rec1 = 0;  // iteration of the latest record, per half
+        const __half2* qrow = &qbuf[gib][P - t];  // row r = it - t lives at index r - 1 + P
+        const int it_end = mm_w + P - 1;
+#pragma unroll 1
+        for (int it = 1; it <= it_end; ++it) {
+            const __half2 q = *qrow++;
+            __half2 hd = hm_diag, left = tl, rm = c_zero;
+#pragma unroll
+            for (int c = 0; c < K; ++c) {
+                const __half2 d = __hfma2_relu(__heq2(q, sc[c]), c_delta, hd);
+                hd = HM[c];
+                const __half2 g = __hmax2(T[c], left);
+                const __half2 h = __hmax2(__hadd2(g, c_nalpha), d);
+                if (GAP == GAP_MERGED) left = __hmax2(__hadd2(g, c_ngamma), d);
+                else left = h;
+                T[c] = left;
+                HM[c] = __hadd2(h, c_mism);
+                rm = __hmax2(rm, h);
+            }
+            record_rows<K>(HM, rm, bestvec, snap_addr, it, rec0, rec1);
+            bestvec = __hmax2(bestvec, rm);
+            // right-most column to the next lane; lane 0 sees the matrix' zero left border
+            __half2 nt = __shfl_up_sync(0xffffffffu, left, 1, P);
+            __half2 nhm = __shfl_up_sync(0xffffffffu, HM[K - 1], 1, P);
+            hm_diag = hml;
+            tl = t == 0 ? c_zero : nt;
+            hml = t == 0 ? c_mism : nhm;
+        }
+
+        // reduce over the group: max value, then smallest row, then smallest strip; the winner resolves its column
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+            int bv = AR::get(bestvec, v);
+            int bi = (v ? rec1 : rec0) - t;
+            int bj = col0;
+            int who = t;
+            if (bi > m[v] || bi < 1) bv = 0;  // cannot happen for a real record; keeps pads out defensively
+#pragma unroll
+            for (int off = P / 2; off >= 1; off >>= 1) {
+                const int ov = __shfl_xor_sync(gmask, bv, off, P);
+                const int oi = __shfl_xor_sync(gmask, bi, off, P);
+                const int oj = __shfl_xor_sync(gmask, bj, off, P);
+                const int ow = __shfl_xor_sync(gmask, who, off, P);
+                if (better_cell(ov, oi, oj, bv, bi, bj)) { bv = ov; bi = oi; bj = oj; who = ow; }
+            }
+            if (t == who && pidx[v] >= 0) {
+                int j = 0;
+                if (bv > 0) {
+                    const int target = bv + mism;
+                    int pos = K;
+#pragma unroll
+                    for (int ch = NCH - 1; ch >= 0; --ch) {
+                        const uint4 w = snap[v][ch][tid];
+                        if (4 * ch + 3 < K && AR::get_bits(w.w, v) == target) pos = 4 * ch + 3;
+                        if (4 * ch + 2 < K && AR::get_bits(w.z, v) == target) pos = 4 * ch + 2;
+                        if (4 * ch + 1 < K && AR::get_bits(w.y, v) == target) pos = 4 * ch + 1;
+                        if (AR::get_bits(w.x, v) == target) pos = 4 * ch;
+                    }
+                    j = bj + pos + 1;
+                } else { bi = 0; }
+                prm.out_score[pidx[v]] = bv;
+                prm.out_i[pidx[v]] = bi;
+                prm.out_j[pidx[v]] = j;
+            }
+        }
+    }
+}
+
+}  // namespace wsb

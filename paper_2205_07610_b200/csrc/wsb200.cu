@@ -3,6 +3,7 @@
 // kernels of score_kernels.cuh / traceback_kernels.cuh.
 #include "../../include/wsb200.h"
 #include "score_kernels.cuh"
+#include "score_short.cuh"
 #include "traceback_kernels.cuh"
 
 #include <cuda_runtime.h>
@@ -325,7 +326,22 @@ template <class AR, int P, int K> static KernelSel pick_gap(int atype, int gap, 
     return {nullptr, 0};  // the packed kernels have no exact three-state model
 }
 
-static KernelSel pick_kernel(int variant, int shape, int atype, int gap, bool masked) {
+template <int P, int K> static KernelSel pick_short(int gap) {
+    if (gap == GAP_LINEAR) return {f16_local_short_kernel<P, K, GAP_LINEAR>, short_smem_bytes<P, K>()};
+    return {f16_local_short_kernel<P, K, GAP_MERGED>, short_smem_bytes<P, K>()};
+}
+
+// short_ok: every unit of the launch fits one stage and the short kernel's query buffer
+static KernelSel pick_kernel(int variant, int shape, int atype, int gap, bool masked, bool short_ok) {
+    static const char* no_short = getenv("WSB_NO_SHORT");  // tuning aid: force the general kernel
+    if (variant == WSB_VARIANT_F16X2 && atype == AT_LOCAL && short_ok && !(no_short && no_short[0])) {
+        switch (shape) {
+            case 0: return pick_short<4, 16>(gap);
+            case 1: return pick_short<8, 19>(gap);
+            case 2: return pick_short<8, 32>(gap);
+            default: return pick_short<4, 38>(gap);
+        }
+    }
     if (variant == WSB_VARIANT_F16X2) {
         switch (shape) {
             case 0: return pick_gap<ArF16, 4, 16>(atype, gap, masked);
@@ -481,7 +497,8 @@ extern "C" int wsb_batch_score(wsb_batch* b, const wsb_scheme* sch, int atype, i
     size_t bnd_need = 0;
     for (const LaunchGroup& g : plan.groups) {
         const Shape sh = g.variant == WSB_VARIANT_F16X2 ? kShapesF16[g.shape] : kShapesI32[g.shape];
-        const KernelSel sel = pick_kernel(g.variant, g.shape, atype, g.gap, sch->mismatch > 0 || sch->match < 0);
+        const bool short_ok = g.max_n <= sh.P * sh.K && g.max_m <= kShortQRows - 64;
+        const KernelSel sel = pick_kernel(g.variant, g.shape, atype, g.gap, sch->mismatch > 0 || sch->match < 0, short_ok);
         KernelFn fn = sel.fn;
         if (!fn) return WSB_E_SCHEME;
         CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel.smem));
