@@ -27,7 +27,7 @@ namespace wsb {
 constexpr int kShortQRows = 320;  // query rows the short kernel can hold per lane group (>= 250 bp reads + P pads)
 
 template <int P, int K> constexpr size_t short_smem_bytes() {
-    return (size_t)2 * ((K + 3) / 4) * kThreads * 16 + (size_t)(kThreads / P) * kShortQRows * 4;
+    return (size_t)2 * (K / 4 + 1) * kThreads * 16 + (size_t)(kThreads / P) * kShortQRows * 4;
 }
 
 __device__ __forceinline__ unsigned h2u(__half2 v) { return *reinterpret_cast<unsigned*>(&v); }
@@ -203,18 +203,20 @@ __device__ __forceinline__ void record_chunks(const unsigned* w, unsigned rm, un
     }
 }
 
+// hm[] row plus the iteration tag in the first spare word after the K columns (the snapshot then also records WHEN).
 template <int K> __device__ __forceinline__ void record_rows(const __half2 (&hm)[K], __half2 rm, __half2 best,
-                                                             unsigned snap_addr, int it, int& rec0, int& rec1) {
-    constexpr int NCH = (K + 3) / 4;
+                                                             unsigned snap_addr, unsigned tag) {
+    constexpr int NCH = K / 4 + 1;  // always at least one spare word for the tag
     unsigned w[NCH * 4];
 #pragma unroll
-    for (int c = 0; c < NCH * 4; ++c) w[c] = c < K ? h2u(hm[c]) : 0u;
+    for (int c = 0; c < NCH * 4; ++c) w[c] = c < K ? h2u(hm[c]) : tag;
     constexpr int FIRST = NCH < 5 ? NCH : 5;
     constexpr unsigned HS = NCH * kThreads * 16;  // byte distance between the two halves' snapshot areas
-    record_chunks<FIRST, true>(w, h2u(rm), h2u(best), snap_addr, snap_addr + HS, it, rec0, rec1);
+    int dummy0 = 0, dummy1 = 0;
+    record_chunks<FIRST, false>(w, h2u(rm), h2u(best), snap_addr, snap_addr + HS, 0, dummy0, dummy1);
     if constexpr (NCH > 5) {
         constexpr int SECOND = NCH - 5 < 5 ? NCH - 5 : 5;
-        record_chunks<SECOND, false>(w + 20, h2u(rm), h2u(best), snap_addr + 5 * 2048, snap_addr + HS + 5 * 2048, it, rec0, rec1);
+        record_chunks<SECOND, false>(w + 20, h2u(rm), h2u(best), snap_addr + 5 * 2048, snap_addr + HS + 5 * 2048, 0, dummy0, dummy1);
         static_assert(NCH <= 10, "strip too wide for the snapshot helper");
     }
 }
@@ -223,7 +225,7 @@ template <int P, int K, int GAP>
 __global__ void __launch_bounds__(kThreads) f16_local_short_kernel(const ScoreParams prm) {
     using AR = ArF16;
     constexpr int GPB = kThreads / P;
-    constexpr int NCH = (K + 3) / 4;
+    constexpr int NCH = K / 4 + 1;
     extern __shared__ uint4 smem_dyn[];
     uint4 (*snap)[NCH][kThreads] = reinterpret_cast<uint4 (*)[NCH][kThreads]>(smem_dyn);
     __half2 (*qbuf)[kShortQRows] = reinterpret_cast<__half2 (*)[kShortQRows]>(smem_dyn + 2 * NCH * kThreads);
@@ -238,11 +240,17 @@ __global__ void __launch_bounds__(kThreads) f16_local_short_kernel(const ScorePa
     const unsigned snap_addr = (unsigned)__cvta_generic_to_shared(&snap[0][0][tid]);
 
     const int mism = prm.mismatch;
+    const int gamma = min(prm.alpha, prm.beta);
     const __half2 c_delta = AR::splat(prm.match - prm.mismatch);
     const __half2 c_mism = AR::splat(mism);
     const __half2 c_nalpha = AR::splat(-prm.alpha);
-    const __half2 c_ngamma = AR::splat(-min(prm.alpha, prm.beta));
+    const __half2 c_ngamma = AR::splat(-gamma);
     const __half2 c_zero = AR::splat(0);
+    // lane 0 sees the matrix' zero left border instead of a neighbour: x * keep + edge on the FMA pipe
+    const __half2 keep = AR::splat(t == 0 ? 0 : 1);
+    const __half2 edge_ta = t == 0 ? c_nalpha : c_zero;  // (T - alpha) of the border, T = 0
+    const __half2 edge_tg = t == 0 ? c_ngamma : c_zero;
+    const __half2 edge_hm = t == 0 ? c_mism : c_zero;
     const int col0 = t * K;
 
     const int64_t rounds = (prm.n_units + n_groups - 1) / n_groups;
@@ -271,17 +279,18 @@ __global__ void __launch_bounds__(kThreads) f16_local_short_kernel(const ScorePa
         const int mm_w = __reduce_max_sync(0xffffffffu, mm);
         if (mm_w == 0) continue;
 
-        // query buffer: P pad rows, then the rows of both queries, pad rows up to the warp's longest query
+        // query buffer: 2P pad rows, the rows of both queries, then pad rows for the ramp-down
         __syncwarp();
-        for (int x = t; x < mm_w + 2 * P; x += P) {  // rows up to mm_w + P - 1 are read during the ramp-down
-            const int row = x - P;
+        for (int x = t; x < mm_w + 4 * P + 2; x += P) {
+            const int row = x - 2 * P;
             int c[2] = {kPadQuery, kPadQuery};
 #pragma unroll
             for (int v = 0; v < 2; ++v)
                 if (row >= 0 && row < m[v]) { const int code = qp[v][row]; c[v] = code < 4 ? code : kFlagQuery; }
             qbuf[gib][x] = AR::codes(c[0], c[1]);
         }
-        __half2 sc[K], T[K], HM[K];
+        // per column: TA = T - alpha, TG = T - gamma (merged model; linear: both are h - alpha), HM = h + mismatch
+        __half2 sc[K], TA[K], TG[GAP == GAP_MERGED ? K : 1], HM[K];
 #pragma unroll
         for (int c = 0; c < K; ++c) {
             int code[2] = {kPadSubject, kPadSubject};
@@ -289,49 +298,85 @@ __global__ void __launch_bounds__(kThreads) f16_local_short_kernel(const ScorePa
             for (int v = 0; v < 2; ++v)
                 if (col0 + c < n[v]) { const int x = sp[v][col0 + c]; code[v] = x < 4 ? x : kFlagSubject; }
             sc[c] = AR::codes(code[0], code[1]);
-            T[c] = c_zero;
+            TA[c] = c_nalpha;
+            if (GAP == GAP_MERGED) TG[c] = c_ngamma;
             HM[c] = c_mism;
         }
         __syncwarp();
 
-        __half2 tl = c_zero, hml = c_mism, hm_diag = c_mism, bestvec = c_zero;
-        int rec0 = 0, rec1 = 0;  // iteration of the latest record, per half
-        const __half2* qrow = &qbuf[gib][P - t];  // row r = it - t lives at index r - 1 + P
-        const int it_end = mm_w + P - 1;
-#pragma unroll 1
-        for (int it = 1; it <= it_end; ++it) {
-            const __half2 q = *qrow++;
-            __half2 hd = hm_diag, left = tl, rm = c_zero;
+        // Two rows per trip: lane t handles rows rA = 2*(trip - t) - 1 and rB = rA + 1, one trip behind lane t-1.  Both
+        // rows take their left border from the previous trip's shuffles, so their cell chains are independent of each
+        // other except cell by cell (row B's cell c needs row A's cell c) and the scheduler can interleave them.
+        __half2 ta_lA = c_nalpha, tg_lA = c_ngamma, hm_lA = c_mism;   // left border of row A: T - alpha, T - gamma, HM
+        __half2 ta_lB = c_nalpha, tg_lB = c_ngamma, hm_lB = c_mism;   // ... of row B
+        __half2 hm_dA = c_mism;                                      // HM(rA - 1, left column): diagonal of row A, cell 0
+        __half2 bestvec = c_zero;
+        // row r lives at qbuf index r - 1 + 2P; the running address doubles as loop counter and record tag
+        const unsigned qbase = (unsigned)__cvta_generic_to_shared(&qbuf[gib][0]);
+        unsigned qaddr = qbase + 4u * (unsigned)(2 * P - 2 * t);
+        const unsigned qend = qaddr + 8u * (unsigned)((mm_w + 1) / 2 + P - 1);
+        __half2 HM2[K];
+
+        auto row = [&](__half2 q, const __half2 (&hin)[K], __half2 (&hout)[K], __half2 hm_diag, __half2& la, __half2& lg,
+                       unsigned tag) {
+            __half2 rm = c_zero;
 #pragma unroll
             for (int c = 0; c < K; ++c) {
-                const __half2 d = __hfma2_relu(__heq2(q, sc[c]), c_delta, hd);
-                hd = HM[c];
-                const __half2 g = __hmax2(T[c], left);
-                const __half2 h = __hmax2(__hadd2(g, c_nalpha), d);
-                if (GAP == GAP_MERGED) left = __hmax2(__hadd2(g, c_ngamma), d);
-                else left = h;
-                T[c] = left;
-                HM[c] = __hadd2(h, c_mism);
+                const __half2 d = __hfma2_relu(__heq2(q, sc[c]), c_delta, c == 0 ? hm_diag : hin[c - 1]);
+                // h = max(d, T_up - alpha, T_left - alpha); T = max(d, T_up - gamma, T_left - gamma)
+                const __half2 h = __hmax2(__hmax2(TA[c], la), d);
+                if (GAP == GAP_MERGED) {
+                    const __half2 tn = __hmax2(__hmax2(TG[c], lg), d);
+                    la = __hadd2(tn, c_nalpha);
+                    lg = __hadd2(tn, c_ngamma);
+                    TG[c] = lg;
+                } else {
+                    la = __hadd2(h, c_nalpha);
+                }
+                TA[c] = la;
+                hout[c] = __hadd2(h, c_mism);
                 rm = __hmax2(rm, h);
             }
-            record_rows<K>(HM, rm, bestvec, snap_addr, it, rec0, rec1);
+            record_rows<K>(hout, rm, bestvec, snap_addr, tag);
             bestvec = __hmax2(bestvec, rm);
-            // right-most column to the next lane; lane 0 sees the matrix' zero left border
-            __half2 nt = __shfl_up_sync(0xffffffffu, left, 1, P);
-            __half2 nhm = __shfl_up_sync(0xffffffffu, HM[K - 1], 1, P);
-            hm_diag = hml;
-            tl = t == 0 ? c_zero : nt;
-            hml = t == 0 ? c_mism : nhm;
+        };
+#pragma unroll 1
+        while (qaddr != qend) {
+            unsigned qa, qb;
+            asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(qa), "=r"(qb) : "r"(qaddr) : "memory");
+            __half2 laA = ta_lA, lgA = tg_lA, laB = ta_lB, lgB = tg_lB;
+            row(u2h(qa), HM, HM2, hm_dA, laA, lgA, qaddr);
+            row(u2h(qb), HM2, HM, hm_lA, laB, lgB, qaddr + 4);
+            qaddr += 8;
+            // right-most columns of both rows to the next lane (used by its next trip)
+            hm_dA = hm_lB;
+            const __half2 s0 = __shfl_up_sync(0xffffffffu, laA, 1, P);
+            const __half2 s1 = __shfl_up_sync(0xffffffffu, HM2[K - 1], 1, P);
+            const __half2 s2 = __shfl_up_sync(0xffffffffu, laB, 1, P);
+            const __half2 s3 = __shfl_up_sync(0xffffffffu, HM[K - 1], 1, P);
+            ta_lA = __hfma2(s0, keep, edge_ta);
+            hm_lA = __hfma2(s1, keep, edge_hm);
+            ta_lB = __hfma2(s2, keep, edge_ta);
+            hm_lB = __hfma2(s3, keep, edge_hm);
+            if (GAP == GAP_MERGED) {
+                const __half2 s4 = __shfl_up_sync(0xffffffffu, lgA, 1, P);
+                const __half2 s5 = __shfl_up_sync(0xffffffffu, lgB, 1, P);
+                tg_lA = __hfma2(s4, keep, edge_tg);
+                tg_lB = __hfma2(s5, keep, edge_tg);
+            }
         }
 
         // reduce over the group: max value, then smallest row, then smallest strip; the winner resolves its column
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
             int bv = AR::get(bestvec, v);
-            int bi = (v ? rec1 : rec0) - t;
-            int bj = col0;
-            int who = t;
-            if (bi > m[v] || bi < 1) bv = 0;  // cannot happen for a real record; keeps pads out defensively
+            int bi = 0, bj = col0, who = t;
+            if (bv > 0) {  // the tag word after the K columns holds the query-buffer address of the record row
+                const uint4 w = snap[v][K / 4][tid];
+                const unsigned tag = (K % 4 == 0) ? w.x : (K % 4 == 1) ? w.y : (K % 4 == 2) ? w.z : w.w;
+                bi = (int)((tag - qbase) >> 2) - 2 * P + 1;  // buffer index -> matrix row
+                if (bi > m[v] || bi < 1) bv = 0;       // cannot happen for a real record; keeps pads out defensively
+            }
 #pragma unroll
             for (int off = P / 2; off >= 1; off >>= 1) {
                 const int ov = __shfl_xor_sync(gmask, bv, off, P);
@@ -346,7 +391,7 @@ __global__ void __launch_bounds__(kThreads) f16_local_short_kernel(const ScorePa
                     const int target = bv + mism;
                     int pos = K;
 #pragma unroll
-                    for (int ch = NCH - 1; ch >= 0; --ch) {
+                    for (int ch = (K - 1) / 4; ch >= 0; --ch) {
                         const uint4 w = snap[v][ch][tid];
                         if (4 * ch + 3 < K && AR::get_bits(w.w, v) == target) pos = 4 * ch + 3;
                         if (4 * ch + 2 < K && AR::get_bits(w.z, v) == target) pos = 4 * ch + 2;

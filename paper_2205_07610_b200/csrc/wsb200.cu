@@ -497,7 +497,7 @@ extern "C" int wsb_batch_score(wsb_batch* b, const wsb_scheme* sch, int atype, i
     size_t bnd_need = 0;
     for (const LaunchGroup& g : plan.groups) {
         const Shape sh = g.variant == WSB_VARIANT_F16X2 ? kShapesF16[g.shape] : kShapesI32[g.shape];
-        const bool short_ok = g.max_n <= sh.P * sh.K && g.max_m <= kShortQRows - 64;
+        const bool short_ok = g.max_n <= sh.P * sh.K && g.max_m <= kShortQRows - 4 * sh.P - 2;
         const KernelSel sel = pick_kernel(g.variant, g.shape, atype, g.gap, sch->mismatch > 0 || sch->match < 0, short_ok);
         KernelFn fn = sel.fn;
         if (!fn) return WSB_E_SCHEME;
