@@ -1,0 +1,275 @@
+"""Batch runner: BatchJob -> GPU shards -> BatchReport.
+
+Drop-in for the reference's thread-pool runner (pkg/src/waveseq/batch.py): same BatchJob / BatchReport / run_batch /
+all_pairs / resolve_workers names, the same validation and error contract (BatchError carries the smallest failing
+pair index, batch.py:179-180, 241-242) and results in per-pair slots, independent of scheduling (batch.py:206).
+
+What replaces the worker pool: the pairs are sharded over the visible GPUs by cell count (native wsb_plan_shards,
+longest-processing-time first), every shard runs on its own context / stream from its own host thread, and the shard
+results are scattered back into the pair slots.  The shards share no state, so there is no collective.
+
+Score-only results follow batch._score_result (batch.py:105-115).  Traceback results follow refdp.ref_traceback (the
+full-matrix walk): see DESIGN.md "CIGAR oracle".
+"""
+from __future__ import annotations
+
+import os
+import threading
+import time
+from collections.abc import Sequence as _SequenceABC
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .core import (AlignConfig, AlignmentResult, BatchError, ScoringScheme, Sequence, validate_config)
+from .engine import EngineTuning, get_context, packed_range_ok
+from .io import unpack_runs
+from .pool import SequencePool
+
+CHUNK_PAIRS = 64  # kept for API compatibility; the GPU planner does its own bucketing
+
+
+def resolve_workers(requested: int = 0) -> int:
+    """WAVESEQ_WORKERS wins, then the request, then the CPU count (reference semantics; the GPU path only validates it)."""
+    env = os.environ.get("WAVESEQ_WORKERS")
+    if env is not None:
+        try:
+            w = int(env)
+        except ValueError:
+            raise ValueError(f"WAVESEQ_WORKERS must be an integer, got {env!r}") from None
+    elif requested:
+        w = requested
+    else:
+        w = os.cpu_count() or 1
+    if w < 1:
+        raise ValueError(f"worker count must be positive, got {w}")
+    return w
+
+
+def resolve_devices(requested=None) -> list[int]:
+    """GPUs a batch is sharded over: explicit list / count, else WAVESEQ_DEVICES (count or comma list), else GPU 0."""
+    if requested is None:
+        env = os.environ.get("WAVESEQ_DEVICES")
+        if env:
+            requested = [int(x) for x in env.split(",")] if "," in env else int(env)
+        else:
+            requested = 1
+    if isinstance(requested, int):
+        if requested < 1:
+            raise ValueError("device count must be positive")
+        return list(range(requested))
+    return [int(d) for d in requested]
+
+
+def all_pairs(queries, subjects) -> list[tuple[int, int]]:
+    """Cartesian product of index pairs, row-major."""
+    if not len(queries) or not len(subjects):
+        raise ValueError("both sequence lists must be non-empty")
+    ns = len(subjects)
+    return [(qi, si) for qi in range(len(queries)) for si in range(ns)]
+
+
+@dataclass
+class BatchJob:
+    """Sequence pools (lists of Sequence or SequencePool), index pairs (list of tuples or (n, 2) array), config, scheme.
+
+    tuning.packed=True forces the packed half2 kernel (pairs outside its range fail like the reference's packed mode
+    would not: the reference silently runs them unpacked, batch.py:136-138, and so does this runner).  workers is
+    accepted for compatibility.  devices (extension) picks the GPUs to shard over.
+    """
+
+    queries: object
+    subjects: object
+    pairs: object
+    cfg: AlignConfig
+    scheme: ScoringScheme
+    tuning: EngineTuning | None = None
+    workers: int = 0
+    devices: object = None
+
+    def __post_init__(self):
+        if len(self.pairs) == 0:
+            raise ValueError("pairs must be non-empty")
+        arr = np.asarray(self.pairs)
+        if arr.ndim != 2 or arr.shape[1] != 2:
+            raise ValueError("pairs must be (query index, subject index) tuples")
+        nq, ns = len(self.queries), len(self.subjects)
+        bad = np.nonzero((arr[:, 0] < 0) | (arr[:, 0] >= nq) | (arr[:, 1] < 0) | (arr[:, 1] >= ns))[0]
+        if len(bad):
+            qi, si = arr[bad[0]]
+            raise ValueError(f"pair ({int(qi)}, {int(si)}) is out of range")
+        self._pair_array = np.ascontiguousarray(arr, np.int32)
+
+
+class ResultArray(_SequenceABC):
+    """results[i] belongs to pairs[i].  Backed by arrays; AlignmentResult objects are built on access so that batches of
+    millions of pairs do not pay for millions of Python objects up front."""
+
+    def __init__(self, score, q_start, q_end, s_start, s_end, cells, runs=None, run_off=None):
+        self.score, self.q_start, self.q_end, self.s_start, self.s_end, self.cells = (
+            score, q_start, q_end, s_start, s_end, cells)
+        self.runs, self.run_off = runs, run_off
+
+    def __len__(self) -> int:
+        return int(self.score.shape[0])
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[k] for k in range(*i.indices(len(self)))]
+        if i < 0:
+            i += len(self)
+        if not 0 <= i < len(self):
+            raise IndexError(i)
+        ops = None
+        if self.runs is not None:
+            ops = unpack_runs(self.runs[int(self.run_off[i]):int(self.run_off[i + 1])])
+        return AlignmentResult(score=int(self.score[i]), q_start=int(self.q_start[i]), q_end=int(self.q_end[i]),
+                               s_start=int(self.s_start[i]), s_end=int(self.s_end[i]), ops=ops,
+                               cells_computed=int(self.cells[i]))
+
+    def __eq__(self, other):
+        if isinstance(other, (list, ResultArray)):
+            return len(self) == len(other) and all(a == b for a, b in zip(self, other))
+        return NotImplemented
+
+
+@dataclass
+class BatchReport:
+    """results[i] belongs to pairs[i]; total_cells = sum of m*n over pairs; wall_time covers upload, kernels, download."""
+
+    results: object
+    wall_time: float
+    total_cells: int
+    kernel_ms: float = 0.0          # device time of the alignment kernels (max over shards)
+    gpu_launches: int = 0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+    shard_cells: list = field(default_factory=list)
+
+    @property
+    def gcups(self) -> float:
+        return self.total_cells / max(self.wall_time, 1e-12) / 1e9
+
+
+def plan_shards(queries: SequencePool, subjects: SequencePool, pair_array: np.ndarray, n_shards: int):
+    """Cell-count balanced shard of every pair (native longest-processing-time planner)."""
+    return N.plan_shards(queries.len, subjects.len, pair_array[:, 0], pair_array[:, 1], n_shards)
+
+
+def _variant_for(job: BatchJob, cfg: AlignConfig) -> str:
+    if job.tuning is not None and job.tuning.packed and cfg.result_mode == "score_only":
+        return "auto"  # packed where exact, int32 elsewhere: the reference's _plan_units falls back the same way
+    env = os.environ.get("WSB_VARIANT")
+    return env if env in ("auto", "f16x2", "i32") else "auto"
+
+
+def _run_shard(device: int, queries: SequencePool, subjects: SequencePool, pair_array: np.ndarray, cfg: AlignConfig,
+               scheme: ScoringScheme, variant: str, out: dict):
+    try:
+        ctx = get_context(device)
+        batch = N.Batch(ctx, queries.codes, queries.off, queries.len, subjects.codes, subjects.off, subjects.len,
+                        pair_array[:, 0], pair_array[:, 1])
+        try:
+            out["h2d"] = batch.h2d_bytes
+            if cfg.result_mode == "traceback":
+                out["ms"], out["launches"] = batch.traceback(scheme, cfg.align_type)
+                out["tb"] = batch.fetch_traceback()
+            else:
+                out["ms"], out["launches"] = batch.score(scheme, cfg.align_type, variant)
+                out["scores"] = batch.fetch_scores()
+        finally:
+            batch.close()
+    except BaseException as exc:  # re-raised by the caller in the submitting thread
+        out["error"] = exc
+
+
+def run_batch(job: BatchJob) -> BatchReport:
+    """Align every pair of the job on the GPU(s); results keep the pairs' order.
+
+    A failing pair aborts the batch with BatchError carrying its index (the smallest one if several fail).
+    """
+    cfg = validate_config(job.cfg, job.scheme)
+    resolve_workers(job.workers)
+    devices = resolve_devices(job.devices)
+    queries = SequencePool.from_sequences(job.queries)
+    subjects = SequencePool.from_sequences(job.subjects)
+    pairs = job._pair_array
+    n = len(pairs)
+    variant = _variant_for(job, cfg)
+    m_arr = queries.len[pairs[:, 0]].astype(np.int64)
+    n_arr = subjects.len[pairs[:, 1]].astype(np.int64)
+    cells = m_arr * n_arr
+
+    t0 = time.perf_counter()
+    if len(devices) == 1:
+        shard_index = [np.arange(n)]
+        shard_cells = [int(cells.sum())]
+    else:
+        shard_of, sc = plan_shards(queries, subjects, pairs, len(devices))
+        shard_index = [np.nonzero(shard_of == k)[0] for k in range(len(devices))]
+        shard_cells = [int(x) for x in sc]
+    outs = [dict() for _ in devices]
+    threads = []
+    for dev, idx, out in zip(devices, shard_index, outs):
+        if len(idx) == 0:
+            continue
+        sub_pairs = pairs if len(devices) == 1 else np.ascontiguousarray(pairs[idx])
+        th = threading.Thread(target=_run_shard, name=f"waveseq-gpu-{dev}",
+                              args=(dev, queries, subjects, sub_pairs, cfg, job.scheme, variant, out))
+        threads.append(th)
+        th.start()
+    for th in threads:
+        th.join()
+    wall = time.perf_counter() - t0
+    for out in outs:
+        if "error" in out:
+            raise out["error"]
+
+    score = np.empty(n, np.int32); qs = np.zeros(n, np.int32); qe = np.empty(n, np.int32)
+    ss = np.zeros(n, np.int32); se = np.empty(n, np.int32); status = np.zeros(n, np.int32)
+    runs = run_off = None
+    if cfg.result_mode == "traceback":
+        counts = np.zeros(n, np.int64)
+        for idx, out in zip(shard_index, outs):
+            if len(idx) == 0:
+                continue
+            tb = out["tb"]
+            score[idx], qs[idx], qe[idx], ss[idx], se[idx], status[idx] = (
+                tb["score"], tb["q_start"], tb["q_end"], tb["s_start"], tb["s_end"], tb["status"])
+            counts[idx] = np.diff(tb["cigar_off"])
+        run_off = np.zeros(n + 1, np.int64)
+        np.cumsum(counts, out=run_off[1:])
+        runs = np.empty(int(run_off[-1]), np.uint32)
+        for idx, out in zip(shard_index, outs):
+            if len(idx) == 0:
+                continue
+            tb = out["tb"]
+            if len(devices) == 1:
+                runs[:] = tb["cigar"]
+            else:
+                for k, p in enumerate(idx):
+                    runs[run_off[p]:run_off[p + 1]] = tb["cigar"][tb["cigar_off"][k]:tb["cigar_off"][k + 1]]
+    else:
+        for idx, out in zip(shard_index, outs):
+            if len(idx) == 0:
+                continue
+            sc_, ei, ej, st = out["scores"]
+            score[idx], qe[idx], se[idx], status[idx] = sc_, ei, ej, st
+        if cfg.align_type == "global":
+            qe[:] = m_arr; se[:] = n_arr
+        else:  # start is unknown without a traceback pass: both span ends carry the argmax cell (batch.py:111-115)
+            qs[:] = qe; ss[:] = se
+    bad = np.nonzero(status)[0]
+    if len(bad):
+        i = int(bad[0])
+        raise BatchError(i, N.status_exception(int(status[i]), f"problem of size {int(m_arr[i])}x{int(n_arr[i])}"))
+
+    results = ResultArray(score, qs, qe, ss, se, cells, runs, run_off)
+    if n <= 100_000:
+        results = list(results)
+    d2h = sum(4 * 4 * len(idx) for idx in shard_index) + (runs.nbytes if runs is not None else 0)
+    return BatchReport(results=results, wall_time=wall, total_cells=int(cells.sum()),
+                       kernel_ms=max((o.get("ms", 0.0) for o in outs), default=0.0),
+                       gpu_launches=sum(o.get("launches", 0) for o in outs),
+                       h2d_bytes=sum(o.get("h2d", 0) for o in outs), d2h_bytes=d2h, shard_cells=shard_cells)

@@ -1,0 +1,115 @@
+"""GPU: the reference-facing Python API (run_batch, engine_score, align, ...) behaves like the reference's."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2205_07610_b200 as W
+from conftest import COMBOS, load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _seqs(texts):
+    return [W.encode_sequence(f"s{i}", t) for i, t in enumerate(texts)]
+
+
+def test_frozen_kats_through_public_api():
+    # pkg/tests/test_refdp.py:18-72 restated against the GPU path
+    lin = W.ScoringScheme(2, -1, 1, 1, "linear")
+    aff = W.ScoringScheme(2, -1, 2, 1, "affine")
+    q, s = _seqs(["ACGT", "AGT"])
+    assert W.engine_score(q, s, W.AlignConfig("global", "linear"), lin) == (5, (4, 3), 12)
+    r = W.align_traceback(q, s, W.AlignConfig("global", "linear", "traceback"), lin)
+    assert r.ops == [("M", 1), ("I", 1), ("M", 2)] and r.score == 5 and W.rescore_alignment(r, q, s, lin) == 5
+    q, s = _seqs(["AAAA", "AA"])
+    assert W.engine_score(q, s, W.AlignConfig("global", "affine"), aff)[:2] == (1, (4, 2))
+    r = W.align("ACG", "TTACGTT", "semiglobal", aff)
+    assert (r.score, r.ops, r.q_start, r.q_end, r.s_start, r.s_end) == (6, [("M", 3)], 0, 3, 2, 5)
+    r = W.align("TTACGTT", "ACG", "local", aff)
+    assert (r.score, r.ops, r.q_start) == (6, [("M", 3)], 2)
+    r = W.align("TTTT", "CCCC", "local", aff)
+    assert (r.score, r.ops) == (0, []) and r.q_start == r.q_end
+    r = W.align("AA", "A", "global", lin)
+    assert (r.score, r.ops) == (1, [("I", 1), ("M", 1)])
+    assert W.cigar_string(r) == "1I1M"
+    r = W.align("ACGT", "ACGT", "global", lin, traceback=False)
+    assert (r.score, r.q_end, r.s_end, r.ops) == (8, 4, 4, None)
+
+
+@pytest.mark.parametrize("align_type,gap_model", COMBOS)
+def test_run_batch_matches_oracle_and_single_pair_api(align_type, gap_model):
+    rng = np.random.default_rng(9)
+    bases = np.array(list("ACGT"))
+    qs = _seqs(["".join(bases[rng.integers(0, 4, int(rng.integers(5, 200)))]) for _ in range(6)])
+    ss = _seqs(["".join(bases[rng.integers(0, 4, int(rng.integers(5, 200)))]) for _ in range(5)])
+    scheme = W.ScoringScheme(2, -1, 2, 1, "affine") if gap_model == "affine" else W.ScoringScheme(2, -1, 1, 1, "linear")
+    pairs = W.all_pairs(qs, ss)
+    assert pairs[:6] == [(0, 0), (0, 1), (0, 2), (0, 3), (0, 4), (1, 0)]
+    rep = W.run_batch(W.BatchJob(qs, ss, pairs, W.AlignConfig(align_type, gap_model), scheme))
+    assert rep.total_cells == sum(len(qs[a]) * len(ss[b]) for a, b in pairs)
+    for (a, b), res in zip(pairs, rep.results):
+        score, end = oracle.ref_score(qs[a].device_codes(), ss[b].device_codes(), align_type, gap_model == "affine",
+                                      scheme.match_score, scheme.mismatch_score, scheme.gap_open, scheme.gap_extend)
+        assert res.score == score and res.ops is None and res.cells_computed == len(qs[a]) * len(ss[b])
+        if align_type == "global":
+            assert (res.q_start, res.q_end, res.s_start, res.s_end) == (0, len(qs[a]), 0, len(ss[b]))
+        else:
+            assert (res.q_start, res.q_end, res.s_start, res.s_end) == (end[0], end[0], end[1], end[1])
+        single = W.engine_score(qs[a], ss[b], W.AlignConfig(align_type, gap_model), scheme)
+        assert single == (score, end, len(qs[a]) * len(ss[b]))
+    # packed tuning gives the same results (tests/test_batch.py:102-113)
+    rep2 = W.run_batch(W.BatchJob(qs, ss, pairs, W.AlignConfig(align_type, gap_model), scheme, tuning=W.EngineTuning(packed=True)))
+    assert rep2.results == rep.results
+    # traceback mode follows ref_traceback
+    rep3 = W.run_batch(W.BatchJob(qs, ss, pairs[:8], W.AlignConfig(align_type, gap_model, "traceback"), scheme))
+    for (a, b), res in zip(pairs[:8], rep3.results):
+        want = oracle.ref_traceback(qs[a].device_codes(), ss[b].device_codes(), align_type, gap_model == "affine",
+                                    scheme.match_score, scheme.mismatch_score, scheme.gap_open, scheme.gap_extend)
+        assert (res.score, res.q_start, res.q_end, res.s_start, res.s_end, res.ops) == (
+            want["score"], want["q_start"], want["q_end"], want["s_start"], want["s_end"], want["ops"])
+        assert W.rescore_alignment(res, qs[a], ss[b], scheme) == res.score
+
+
+def test_packed_engine_and_errors():
+    aff = W.ScoringScheme(2, -1, 2, 1, "affine")
+    cfg = W.AlignConfig("local", "affine")
+    for rec in load_golden("random_small.json")["packed"][:12]:
+        scheme = W.ScoringScheme(*rec["scheme"], rec["gap_model"])
+        c = W.AlignConfig(rec["align_type"], rec["gap_model"])
+        qa, sa, qb, sb = _seqs([rec["qa"], rec["sa"], rec["qb"], rec["sb"]])
+        ra, rb, cells = W.engine_score_packed((qa, sa), (qb, sb), c, scheme)
+        assert [ra[0], ra[1][0], ra[1][1]] == rec["a"] and [rb[0], rb[1][0], rb[1][1]] == rec["b"] and cells == rec["cells"]
+    big = _seqs(["A" * 5000, "A" * 5000])
+    with pytest.raises(W.PackedRangeOverflow):
+        W.engine_score_packed((big[0], big[1]), (big[0], big[1]), cfg, aff)
+    with pytest.raises(ValueError):
+        q, s = _seqs(["ACGT", "ACGT"])
+        W.engine_score_packed((q, s), (q, s), cfg, W.ScoringScheme(2, -9, 2, 1, "affine"))
+    with pytest.raises(W.ConfigMismatch):
+        W.engine_score(*_seqs(["AC", "AC"]), W.AlignConfig("local", "linear"), aff)
+    with pytest.raises(ValueError):
+        W.BatchJob(_seqs(["AC"]), _seqs(["AC"]), [(0, 1)], cfg, aff)
+    with pytest.raises(ValueError):
+        W.BatchJob(_seqs(["AC"]), _seqs(["AC"]), [], cfg, aff)
+
+
+def test_flagged_symbols_never_match():
+    aff = W.ScoringScheme(2, -1, 2, 1, "affine")
+    q, s = _seqs(["NNNN", "NNNN"])
+    assert W.engine_score(q, s, W.AlignConfig("local", "affine"), aff)[0] == 0
+    q, s = _seqs(["ACNGT", "ACNGT"])
+    assert W.engine_score(q, s, W.AlignConfig("global", "affine"), aff)[0] == 2 * 4 - 1
+
+
+def test_pool_inputs_and_lazy_results():
+    rng = np.random.default_rng(1)
+    n = 120_001
+    q = rng.integers(0, 4, (n, 40), dtype=np.uint8); s = rng.integers(0, 4, (n, 40), dtype=np.uint8)
+    job = W.BatchJob(W.SequencePool.from_uniform(q), W.SequencePool.from_uniform(s), np.stack([np.arange(n), np.arange(n)], 1),
+                     W.AlignConfig("local", "affine"), W.ScoringScheme())
+    rep = W.run_batch(job)
+    assert isinstance(rep.results, W.ResultArray) and len(rep.results) == n
+    for k in (0, 1, n // 2, n - 1):
+        score, end = oracle.ref_score(q[k], s[k], "local", True, 2, -1, 2, 1)
+        assert (rep.results[k].score, rep.results[k].q_end, rep.results[k].s_end) == (score, end[0], end[1])
+    assert rep.gpu_launches >= 1 and rep.h2d_bytes > 2 * n * 40 and rep.kernel_ms > 0

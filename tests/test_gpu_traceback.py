@@ -1,0 +1,117 @@
+"""GPU parity: spans + CIGARs of the direction-code traceback (through the C ABI) == oracle ref_traceback, bit-exact."""
+import numpy as np
+import pytest
+
+import oracle
+from conftest import AFFINE_SCHEMES, COMBOS, LINEAR_SCHEMES, cigar_of, codes, load_golden, mutate_codes, random_codes
+from helpers import make_pool, scheme_of
+from paper_2205_07610_b200 import _native as N
+from paper_2205_07610_b200.io import unpack_runs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = N.Context(0)
+    yield c
+    c.close()
+
+
+def gpu_traceback(ctx, qs, ss, pairs, scheme, align_type):
+    qc, qo, ql = make_pool(qs); sc, so, sl = make_pool(ss)
+    pq = np.array([p[0] for p in pairs], np.int32); ps = np.array([p[1] for p in pairs], np.int32)
+    b = N.Batch(ctx, qc, qo, ql, sc, so, sl, pq, ps)
+    try:
+        b.traceback(scheme, align_type)
+        return b.fetch_traceback()
+    finally:
+        b.close()
+
+
+def oracle_traceback(qs, ss, pairs, scheme, align_type):
+    qc, qo, ql = make_pool(qs); sc, so, sl = make_pool(ss)
+    pq = np.array([p[0] for p in pairs], np.int32); ps = np.array([p[1] for p in pairs], np.int32)
+    return oracle.traceback_batch(qc, qo, ql, sc, so, sl, pq, ps, align_type, scheme.gap_model == "affine",
+                                  scheme.match_score, scheme.mismatch_score, scheme.gap_open, scheme.gap_extend)
+
+
+def assert_tb_equal(got, want, msg=""):
+    n = len(want["score"])
+    for key in ("score", "q_start", "q_end", "s_start", "s_end"):
+        bad = np.nonzero(got[key] != want[key])[0]
+        assert len(bad) == 0, f"{msg}: {key} differs at pair {bad[0]}: got {got[key][bad[0]]} want {want[key][bad[0]]}"
+    for k in range(n):
+        runs = unpack_runs(got["cigar"][int(got["cigar_off"][k]):int(got["cigar_off"][k + 1])])
+        assert runs == want["ops"][k], f"{msg}: CIGAR differs at pair {k}: got {cigar_of(runs)} want {cigar_of(want['ops'][k])}"
+
+
+@pytest.mark.parametrize("align_type,gap_model", COMBOS)
+def test_golden_cigars(ctx, align_type, gap_model):
+    recs = [r for name in ("kat.json", "adversarial.json") for r in load_golden(name)]
+    recs += load_golden("random_small.json")["pairs"]
+    recs = [r for r in recs if r["align_type"] == align_type and r["gap_model"] == gap_model and "tb" in r]
+    assert recs
+    by_scheme = {}
+    for r in recs:
+        by_scheme.setdefault(tuple(r["scheme"]), []).append(r)
+    for sch, rs in by_scheme.items():
+        scheme = scheme_of(sch, gap_model)
+        got = gpu_traceback(ctx, [codes(r["q"]) for r in rs], [codes(r["s"]) for r in rs], [(i, i) for i in range(len(rs))],
+                            scheme, align_type)
+        for k, r in enumerate(rs):
+            runs = unpack_runs(got["cigar"][int(got["cigar_off"][k]):int(got["cigar_off"][k + 1])])
+            t = r["tb"]
+            assert int(got["score"][k]) == r["score"], (sch, k)
+            assert (int(got["q_start"][k]), int(got["q_end"][k]), int(got["s_start"][k]), int(got["s_end"][k])) == (
+                t["q_start"], t["q_end"], t["s_start"], t["s_end"]), (sch, k, r["q"], r["s"])
+            assert cigar_of(runs) == t["cigar"], (sch, k, r["q"], r["s"])
+
+
+@pytest.mark.parametrize("align_type,gap_model", COMBOS)
+def test_random_vs_oracle(ctx, align_type, gap_model):
+    rng = np.random.default_rng(2026)
+    pool = AFFINE_SCHEMES + [(2, -9, 2, 1), (2, -1, 1, 3)] if gap_model == "affine" else LINEAR_SCHEMES
+    for sch in pool:
+        scheme = scheme_of(sch, gap_model)
+        qs, ss = [], []
+        for k in range(200):
+            q = random_codes(rng, int(rng.integers(1, 280)))
+            s = mutate_codes(rng, q, 0.06, 0.03, 0.03) if k % 2 else random_codes(rng, int(rng.integers(1, 280)))
+            if k % 7 == 0:
+                q = q.copy(); q[rng.integers(0, len(q))] = 4
+            qs.append(q); ss.append(s)
+        pairs = [(i, i) for i in range(len(qs))]
+        assert_tb_equal(gpu_traceback(ctx, qs, ss, pairs, scheme, align_type), oracle_traceback(qs, ss, pairs, scheme, align_type),
+                        f"{align_type}/{gap_model}/{sch}")
+
+
+def test_uniform_250bp_semiglobal_affine_cfg3_shape(ctx):
+    rng = np.random.default_rng(220507613)
+    scheme = scheme_of((2, -1, 2, 1), "affine")
+    n = 3000
+    qs = [random_codes(rng, 250) for _ in range(n)]
+    ss = []
+    for i, q in enumerate(qs):
+        if i % 2:
+            s = mutate_codes(rng, q, 0.03, 0.01, 0.01)[:250]
+            s = np.concatenate([s, random_codes(rng, 250 - len(s))])
+        else:
+            s = random_codes(rng, 250)
+        ss.append(s)
+    pairs = [(i, i) for i in range(n)]
+    assert_tb_equal(gpu_traceback(ctx, qs, ss, pairs, scheme, "semiglobal"), oracle_traceback(qs, ss, pairs, scheme, "semiglobal"), "cfg3")
+
+
+def test_multi_stage_and_chunked(ctx, monkeypatch):
+    monkeypatch.setenv("WSB_TB_SCRATCH_MB", "1")  # force several chunks
+    rng = np.random.default_rng(77)
+    scheme = scheme_of((2, -1, 2, 1), "affine")
+    qs, ss = [], []
+    for L in (600, 900, 1300, 513, 40, 700):
+        q = random_codes(rng, L)
+        qs.append(q); ss.append(mutate_codes(rng, q, 0.08, 0.04, 0.04))
+    qs.append(random_codes(rng, 30)); ss.append(random_codes(rng, 1500))
+    pairs = [(i, i) for i in range(len(qs))]
+    for at in ("global", "local", "semiglobal"):
+        assert_tb_equal(gpu_traceback(ctx, qs, ss, pairs, scheme, at), oracle_traceback(qs, ss, pairs, scheme, at), at)
