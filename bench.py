@@ -1,0 +1,320 @@
+#!/usr/bin/env python
+"""Benchmark of the batched pairwise-alignment hot path (BASELINE.json metric: GCUPS).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2] [--impl reference]
+
+A step is one pass of the score kernels over one synthetic batch.  At N = 1 the workload is cfg2, the configuration the
+metric is quoted on: 4 M pairs of 150 bp reads, local alignment, affine gaps (2/-1/2/1), score-only, packed half2
+kernel.  With N > 1 (torchrun, one rank per GPU) every rank aligns its own batch of the same size (weak scaling, no
+data-path collective; gloo carries the barrier and the max-over-ranks of the step time).
+
+value   whole-job GCUPS with the pools resident in HBM, timed with CUDA events on the launching stream (C ABI).
+e2e     the same metric through the public API (run_batch on host buffers): H2D of the pools + kernels + D2H of the
+        results inside the timed region.
+roofline ALU-issue roofline of the dominant kernel: N_SM * 128 thread-instr/clk * f * W / I_cell.
+cpu_baseline / --impl reference: the oracle port of the reference's DP (oracle/wsoracle.c, OpenMP, all host cores) on a
+        bounded sample of the same workload.
+"""
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (pairs, length, align_type, gap_model, scheme, result_mode, ops per cell of the reference's count)
+    "cfg1": dict(pairs=10_000, length=150, align_type="global", gap_model="linear", scheme=(2, -1, 1, 1), i_cell=5),
+    "cfg2": dict(pairs=4_000_000, length=150, align_type="local", gap_model="affine", scheme=(2, -1, 2, 1), i_cell=8),
+    "cfg2_i32": dict(pairs=1_000_000, length=150, align_type="local", gap_model="affine", scheme=(2, -1, 2, 1), i_cell=8,
+                     variant="i32"),
+    "cfg3": dict(pairs=200_000, length=250, align_type="semiglobal", gap_model="affine", scheme=(2, -1, 2, 1), i_cell=8,
+                 traceback=True),
+}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except OSError:
+        return {}
+
+
+def make_batch(cfg, seed):
+    """Synthetic random-ACGT pools (uniform symbols, no flags), pair i = (query i, subject i)."""
+    rng = np.random.default_rng(seed)
+    n, L = cfg["pairs"], cfg["length"]
+    q = rng.integers(0, 4, (n, L), dtype=np.uint8)
+    s = rng.integers(0, 4, (n, L), dtype=np.uint8)
+    return q, s
+
+
+def pinned(arr):
+    """Copy into page-locked host memory (torch is plumbing here: it owns the pinned allocation)."""
+    import torch
+    t = torch.empty(arr.shape, dtype=torch.uint8, pin_memory=torch.cuda.is_available())
+    out = t.numpy()
+    out[...] = arr
+    out_t = (out, t)  # keep the tensor alive with the view
+    return out_t
+
+
+class ClockSampler(threading.Thread):
+    """SM clock + throttle reasons during the timed region (nvidia-ml-py)."""
+
+    def __init__(self, index):
+        super().__init__(daemon=True)
+        self.index, self.samples, self.reasons, self.max_mhz = index, [], set(), None
+        self._stop_evt = threading.Event()
+
+    def run(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            names = {nv.nvmlClocksThrottleReasonHwSlowdown: "hw_slowdown",
+                     nv.nvmlClocksThrottleReasonHwThermalSlowdown: "hw_thermal_slowdown",
+                     nv.nvmlClocksThrottleReasonSwThermalSlowdown: "sw_thermal_slowdown",
+                     nv.nvmlClocksThrottleReasonSwPowerCap: "sw_power_cap"}
+            while not self._stop_evt.is_set():
+                self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                for bit, name in names.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+                time.sleep(0.02)
+        except Exception as exc:  # no NVML: report nothing rather than guess
+            self.reasons.add(f"nvml_unavailable:{type(exc).__name__}")
+
+    def stop(self):
+        self._stop_evt.set()
+        self.join(timeout=2)
+        med = float(np.median(self.samples)) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    return rank, local, world
+
+
+def dist_barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def dist_max(x, world):
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t[0])
+    return x
+
+
+def dist_sum(x, world):
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t[0])
+    return x
+
+
+def cpu_sample(cfg, seconds_target=12.0, seed=7):
+    """Oracle port (plain C restatement of refdp, OpenMP over pairs) on a bounded sample of the workload."""
+    import oracle
+    threads = oracle.max_threads()
+    L = cfg["length"]
+    sch = cfg["scheme"]
+
+    def run(npairs):
+        q, s = make_batch(dict(pairs=npairs, length=L), seed)
+        off = np.arange(npairs, dtype=np.int64) * L
+        ln = np.full(npairs, L, np.int32)
+        idx = np.arange(npairs, dtype=np.int32)
+        t0 = time.perf_counter()
+        if cfg.get("traceback"):
+            oracle.traceback_batch(q.reshape(-1), off, ln, s.reshape(-1), off, ln, idx, idx, cfg["align_type"],
+                                   cfg["gap_model"] == "affine", *sch, threads=threads)
+        else:
+            oracle.score_batch(q.reshape(-1), off, ln, s.reshape(-1), off, ln, idx, idx, cfg["align_type"],
+                               cfg["gap_model"] == "affine", *sch, threads=threads)
+        dt = time.perf_counter() - t0
+        return npairs * L * L / dt / 1e9, dt
+
+    probe_pairs = max(64, int(2e8 / (L * L)))
+    rate, dt = run(probe_pairs)
+    pairs = int(min(cfg["pairs"], max(probe_pairs, rate * 1e9 * seconds_target / (L * L))))
+    rate, dt = run(pairs)
+    return rate, threads, pairs, dt
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the reference's CPU algorithm (oracle port, all host threads); rank 0 only."""
+    if rank != 0:
+        return
+    rates = []
+    info = None
+    for step in range(args.warmup + args.steps):
+        rate, threads, pairs, dt = cpu_sample(cfg, seconds_target=max(2.0, 20.0 / max(args.steps + args.warmup, 1)), seed=11 + step)
+        info = (threads, pairs, dt)
+        if step >= args.warmup:
+            rates.append(rate)
+    value = float(np.mean(rates))
+    threads, pairs, dt = info
+    sample = f"{pairs} pairs of {cfg['length']} bp per step ({dt:.2f} s), {cfg['align_type']}/{cfg['gap_model']}"
+    line = {"impl": "reference", "metric": "GCUPS", "value": value, "unit": "GCUPS", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "int32", "data": "synthetic",
+            "config": {"workload": args.workload, "pairs_per_step": pairs, "read_length": cfg["length"],
+                       "align_type": cfg["align_type"], "gap_model": cfg["gap_model"], "scheme": list(cfg["scheme"])},
+            "cpu_baseline": {"value": value, "unit": "GCUPS", "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--pairs", type=int, default=0, help="override pairs per GPU (debug)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = dict(WORKLOADS[args.workload])
+    if args.pairs:
+        cfg["pairs"] = args.pairs
+    rank, local, world = dist_setup()
+
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+
+    import paper_2205_07610_b200 as W
+    from paper_2205_07610_b200 import _native as N
+
+    ndev = N.device_count()
+    if ndev < 1:
+        raise SystemExit("bench.py needs a CUDA device: the alignment path has no CPU fallback")
+    device = local % ndev
+    scheme = W.ScoringScheme(*cfg["scheme"], cfg["gap_model"])
+    variant = cfg.get("variant", "f16x2")
+    q, s = make_batch(cfg, 220507610 + 2 + rank)
+    n, L = cfg["pairs"], cfg["length"]
+    (q_pin, q_keep), (s_pin, s_keep) = pinned(q), pinned(s)
+    off = np.arange(n, dtype=np.int64) * L
+    ln = np.full(n, L, np.int32)
+    idx = np.arange(n, dtype=np.int32)
+    ctx = W.get_context(device)
+    batch = N.Batch(ctx, q_pin.reshape(-1), off, ln, s_pin.reshape(-1), off, ln, idx, idx)
+    cells = batch.total_cells
+    traceback = bool(cfg.get("traceback"))
+
+    def step():
+        if traceback:
+            return batch.traceback(scheme, cfg["align_type"])
+        return batch.score(scheme, cfg["align_type"], variant)
+
+    for _ in range(args.warmup):
+        step()
+    sampler = ClockSampler(device)
+    sampler.start()
+    dist_barrier(world)
+    step_ms, launches = [], 0
+    t_wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        ms, nl = step()          # CUDA events on the launching stream bracket the kernels; synchronised before return
+        step_ms.append(ms)
+        launches += nl
+    dist_barrier(world)
+    wall = time.perf_counter() - t_wall0
+    clocks = sampler.stop()
+    total_ms = dist_max(float(np.sum(step_ms)), world)      # slowest rank
+    total_cells = dist_sum(float(cells), world) * args.steps
+    value = total_cells / (total_ms * 1e-3) / 1e9
+    launches = int(dist_sum(float(launches), world))
+
+    # end to end through the public API: host buffers in, host results out, every step
+    pool_q, pool_s = W.SequencePool(q_pin.reshape(-1), off, ln), W.SequencePool(s_pin.reshape(-1), off, ln)
+    pair_arr = np.stack([idx, idx], 1)
+    job = W.BatchJob(pool_q, pool_s, pair_arr, W.AlignConfig(cfg["align_type"], cfg["gap_model"],
+                                                           "traceback" if traceback else "score_only"),
+                     scheme, tuning=W.EngineTuning(packed=(variant != "i32")), devices=[device])
+    if variant == "i32":
+        os.environ["WSB_VARIANT"] = "i32"
+    e2e_steps = max(1, min(args.steps, 3))
+    rep = W.run_batch(job)  # warm
+    dist_barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        rep = W.run_batch(job)
+        _ = int(rep.results.score[0]) if isinstance(rep.results, W.ResultArray) else rep.results[0].score
+    e2e_time = dist_max(time.perf_counter() - t0, world)
+    e2e_value = total_cells / args.steps * e2e_steps / e2e_time / 1e9
+
+    # roofline: ALU-issue bound of the dominant kernel
+    peaks = measured_peaks()
+    f_ghz = float(peaks.get("sm_max_mhz", 1965.0)) / 1e3
+    n_sm = ctx.sm_count
+    width = 1 if variant == "i32" else 2
+    peak = n_sm * 128 * f_ghz * width / cfg["i_cell"]
+    per_gpu = value / world
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            traffic = json.load(fh).get(args.workload)
+    except OSError:
+        pass
+    roofline = {"bound": "alu_issue", "achieved": per_gpu, "peak": peak, "unit": "GCUPS", "frac": per_gpu / peak,
+                "traffic": traffic, "peak_source": "N_SM*128*f_SM*W/I_cell with f_SM = sm_max_mhz of MEASURED_PEAKS.json",
+                "i_cell": cfg["i_cell"], "cells_per_thread_instr": width, "n_sm": n_sm, "f_ghz": f_ghz}
+    if clocks.get("sm_mhz"):
+        cyc_peak = n_sm * 128 * clocks["sm_mhz"] / 1e3 * width / cfg["i_cell"]
+        roofline["frac_at_measured_clock"] = per_gpu / cyc_peak
+
+    if rank == 0:
+        line = {"metric": "GCUPS", "value": value, "unit": "GCUPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "i32" if variant == "i32" else "f16x2", "data": "synthetic",
+                "config": {"workload": args.workload, "pairs_per_gpu": n, "read_length": L, "align_type": cfg["align_type"],
+                           "gap_model": cfg["gap_model"], "scheme": list(cfg["scheme"]),
+                           "result_mode": "traceback" if traceback else "score_only", "variant": variant,
+                           "l2": f"inputs {2 * n * L / 1e6:.0f} MB per GPU vs 126 MB L2 (no flush needed)",
+                           "sharding": "independent pairs per rank, no collective; gloo for barrier/max only"},
+                "roofline": roofline,
+                "e2e": {"value": e2e_value, "unit": "GCUPS", "h2d_bytes_per_step": int(rep.h2d_bytes) * world,
+                        "d2h_bytes_per_step": int(rep.d2h_bytes) * world, "steps": e2e_steps},
+                "gpu_launches": launches, "clocks": clocks, "wall_s_timed_region": wall}
+        if not args.no_cpu_baseline:
+            rate, threads, pairs, dt = cpu_sample(cfg)
+            line["cpu_baseline"] = {"value": rate, "unit": "GCUPS", "cores": threads, "kind": "port",
+                                    "sample": f"{pairs} pairs of {L} bp ({dt:.1f} s), oracle/wsoracle.c with OpenMP"}
+        print(json.dumps(line))
+    batch.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
