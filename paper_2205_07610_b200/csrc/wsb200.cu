@@ -279,11 +279,13 @@ extern "C" int64_t wsb_batch_total_cells(const wsb_batch* b) { return b ? b->tot
 
 // ------------------------------------------------------------------------------------------------ kernel shapes
 struct Shape { int P, K; };
-// packed half2 shapes: short reads in a single stage; (8,32) also chains stages for longer packed reads
+// packed half2 shapes: short reads in a single stage; (8,32) also chains stages for longer packed reads.
+// (4,38) halves the wavefront ramp of 150 bp reads but needs ~200 registers: measured slower than (8,19) on B200
+// (2 instead of 4 resident blocks per SM), so it is only reachable through WSB_FORCE_SHAPE=3.
 static const Shape kShapesF16[] = {{4, 16}, {8, 19}, {8, 32}, {4, 38}};
 // int32 shapes: narrow groups for short reads, full warps with wide stages for long reads
 static const Shape kShapesI32[] = {{8, 16}, {16, 16}, {32, 16}};
-constexpr int kNumShapesF16 = 4, kNumShapesI32 = 3;
+constexpr int kNumShapesF16 = 3, kNumShapesI32 = 3;  // shapes the planner may choose
 constexpr int kNumShapes = 4;  // bucket array bound
 
 static double padded_cost(const Shape& s, int m, int n) {
@@ -292,9 +294,9 @@ static double padded_cost(const Shape& s, int m, int n) {
     return (double)(m + s.P - 1) * stages * w;
 }
 
-static int best_shape(const Shape* shapes, int count, int m, int n) {
+static int best_shape(const Shape* shapes, int count, int table_size, int m, int n) {
     static const char* force = getenv("WSB_FORCE_SHAPE");  // tuning aid: index into the shape table
-    if (force && force[0]) return std::min(count - 1, std::max(0, atoi(force)));
+    if (force && force[0]) return std::min(table_size - 1, std::max(0, atoi(force)));
     int best = 0;
     double bc = padded_cost(shapes[0], m, n);
     for (int k = 1; k < count; ++k) {
@@ -381,8 +383,8 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
         if ((int64_t)ms * ((int64_t)m + n) >= (1ll << 29)) { status = WSB_E_LENGTH; return; }
         const bool fits = f16_scheme_ok && wsb_f16_range_ok(sch, m, n);
         if (variant == WSB_VARIANT_F16X2 && !fits) { status = WSB_E_RANGE; return; }
-        if (variant != WSB_VARIANT_I32 && fits) { var = WSB_VARIANT_F16X2; shape = best_shape(kShapesF16, kNumShapesF16, m, n); }
-        else { var = WSB_VARIANT_I32; shape = best_shape(kShapesI32, kNumShapesI32, m, n); }
+        if (variant != WSB_VARIANT_I32 && fits) { var = WSB_VARIANT_F16X2; shape = best_shape(kShapesF16, kNumShapesF16, 4, m, n); }
+        else { var = WSB_VARIANT_I32; shape = best_shape(kShapesI32, kNumShapesI32, 3, m, n); }
     };
 
     if (b->uniform) {
