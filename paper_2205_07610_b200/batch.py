@@ -197,8 +197,8 @@ def run_batch(job: BatchJob) -> BatchReport:
     pairs = job._pair_array
     n = len(pairs)
     variant = _variant_for(job, cfg)
-    m_arr = queries.len[pairs[:, 0]].astype(np.int64)
-    n_arr = subjects.len[pairs[:, 1]].astype(np.int64)
+    m_arr = queries.len.take(pairs[:, 0]).astype(np.int64)
+    n_arr = subjects.len.take(pairs[:, 1]).astype(np.int64)
     cells = m_arr * n_arr
 
     t0 = time.perf_counter()
@@ -215,6 +215,9 @@ def run_batch(job: BatchJob) -> BatchReport:
         if len(idx) == 0:
             continue
         sub_pairs = pairs if len(devices) == 1 else np.ascontiguousarray(pairs[idx])
+        if len(devices) == 1:  # no thread hop for the common single-GPU case
+            _run_shard(dev, queries, subjects, sub_pairs, cfg, job.scheme, variant, out)
+            continue
         th = threading.Thread(target=_run_shard, name=f"waveseq-gpu-{dev}",
                               args=(dev, queries, subjects, sub_pairs, cfg, job.scheme, variant, out))
         threads.append(th)
@@ -226,10 +229,21 @@ def run_batch(job: BatchJob) -> BatchReport:
         if "error" in out:
             raise out["error"]
 
-    score = np.empty(n, np.int32); qs = np.zeros(n, np.int32); qe = np.empty(n, np.int32)
-    ss = np.zeros(n, np.int32); se = np.empty(n, np.int32); status = np.zeros(n, np.int32)
+    single = len(devices) == 1
     runs = run_off = None
-    if cfg.result_mode == "traceback":
+    if single and cfg.result_mode != "traceback":  # one shard: the fetched arrays are the result arrays
+        score, qe, se, status = outs[0]["scores"]
+        if cfg.align_type == "global":
+            qs = np.zeros(n, np.int32); ss = qs
+            qe = m_arr.astype(np.int32); se = n_arr.astype(np.int32)
+        else:
+            qs, ss = qe, se
+    else:
+        score = np.empty(n, np.int32); qs = np.zeros(n, np.int32); qe = np.empty(n, np.int32)
+        ss = np.zeros(n, np.int32); se = np.empty(n, np.int32); status = np.zeros(n, np.int32)
+    if single and cfg.result_mode != "traceback":
+        pass
+    elif cfg.result_mode == "traceback":
         counts = np.zeros(n, np.int64)
         for idx, out in zip(shard_index, outs):
             if len(idx) == 0:

@@ -77,8 +77,8 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
     const int64_t bnd_rows = multi_stage ? (int64_t)max_m + 2 : 0;
     const size_t bnd_need = (size_t)bnd_rows * sizeof(int2) * (size_t)max_grid * gpb;
     if (bnd_need > b->bnd_bytes) {
-        if (b->d_bnd) { cudaFree(b->d_bnd); b->d_bnd = nullptr; b->bnd_bytes = 0; }
-        CUDA_TRY(ctx, cudaMalloc(&b->d_bnd, bnd_need));
+        if (b->d_bnd) { ctx->release(b->d_bnd); b->d_bnd = nullptr; b->bnd_bytes = 0; }
+        CUDA_TRY(ctx, ctx->alloc(&b->d_bnd, bnd_need));
         b->bnd_bytes = bnd_need;
     }
 

@@ -30,6 +30,40 @@ struct wsb_ctx {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::string last_error;
+    // Device-memory cache: batches come and go with every run_batch call, and cudaMalloc/cudaFree of GB-sized pools
+    // cost tens of milliseconds each, so freed blocks are kept (size-bucketed, 2 MiB granularity) and reused.
+    std::multimap<size_t, void*> free_blocks;
+    std::map<void*, size_t> live_blocks;
+    size_t cached_bytes = 0;
+
+    cudaError_t alloc(void** out, size_t bytes) {
+        const size_t gran = (size_t)2 << 20;
+        const size_t want = std::max<size_t>(gran, (bytes + gran - 1) / gran * gran);
+        auto it = free_blocks.lower_bound(want);
+        if (it != free_blocks.end() && it->first <= want + want / 4) {
+            *out = it->second; live_blocks[*out] = it->first; cached_bytes -= it->first; free_blocks.erase(it);
+            return cudaSuccess;
+        }
+        cudaError_t e = cudaMalloc(out, want);
+        if (e != cudaSuccess) {  // give the cache back and retry once
+            (void)cudaGetLastError();
+            trim();
+            e = cudaMalloc(out, want);
+        }
+        if (e == cudaSuccess) live_blocks[*out] = want;
+        return e;
+    }
+    void release(void* p) {
+        if (!p) return;
+        auto it = live_blocks.find(p);
+        if (it == live_blocks.end()) { cudaFree(p); return; }
+        free_blocks.emplace(it->second, p); cached_bytes += it->second; live_blocks.erase(it);
+        if (cached_bytes > ((size_t)24 << 30)) trim();
+    }
+    void trim() {
+        for (auto& kv : free_blocks) cudaFree(kv.second);
+        free_blocks.clear(); cached_bytes = 0;
+    }
 };
 
 struct LaunchGroup {  // pairs that run in one kernel launch
@@ -175,6 +209,7 @@ extern "C" int wsb_ctx_create(int device, wsb_ctx** out) {
 extern "C" void wsb_ctx_destroy(wsb_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
+    c->trim();
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -188,7 +223,7 @@ extern "C" int wsb_ctx_sm_count(const wsb_ctx* c) { return c ? c->sm_count : 0; 
 template <class T> static int upload(wsb_ctx* ctx, T** dst, const T* src, int64_t count) {
     *dst = nullptr;
     const size_t bytes = sizeof(T) * (size_t)std::max<int64_t>(count, 1);
-    CUDA_TRY(ctx, cudaMalloc((void**)dst, bytes));
+    CUDA_TRY(ctx, ctx->alloc((void**)dst, bytes));
     if (count > 0) CUDA_TRY(ctx, cudaMemcpyAsync(*dst, src, sizeof(T) * (size_t)count, cudaMemcpyHostToDevice, ctx->stream));
     return WSB_OK;
 }
@@ -200,7 +235,7 @@ extern "C" void wsb_batch_destroy(wsb_batch* b) {
     for (void* p : {(void*)b->d_qcodes, (void*)b->d_scodes, (void*)b->d_qoff, (void*)b->d_soff, (void*)b->d_qlen,
                     (void*)b->d_slen, (void*)b->d_pq, (void*)b->d_ps, (void*)b->d_score, (void*)b->d_i, (void*)b->d_j,
                     b->d_bnd})
-        if (p) cudaFree(p);
+        if (p) b->ctx->release(p);
     for (auto& kv : b->plans) if (kv.second.d_units) cudaFree(kv.second.d_units);
     b->tb.release();
     delete b;
@@ -266,7 +301,7 @@ extern "C" int wsb_batch_create(wsb_ctx* ctx, const uint8_t* q_codes, const int6
     UP(d_pq, pair_q, n_pairs) UP(d_ps, pair_s, n_pairs)
 #undef UP
     for (int32_t** p : {&b->d_score, &b->d_i, &b->d_j}) {
-        cudaError_t e = cudaMalloc((void**)p, sizeof(int32_t) * (size_t)n_pairs);
+        cudaError_t e = ctx->alloc((void**)p, sizeof(int32_t) * (size_t)n_pairs);
         if (e != cudaSuccess) { ctx->last_error = cudaGetErrorString(e); wsb_batch_destroy(b); return WSB_E_NOMEM; }
     }
     cudaError_t e = cudaStreamSynchronize(ctx->stream);  // host arrays may be reused by the caller after return
@@ -516,8 +551,8 @@ extern "C" int wsb_batch_score(wsb_batch* b, const wsb_scheme* sch, int atype, i
         bnd_need = std::max(bnd_need, (size_t)rows * 8u * (size_t)grid * gpb);
     }
     if (bnd_need > b->bnd_bytes) {
-        if (b->d_bnd) { cudaFree(b->d_bnd); b->d_bnd = nullptr; b->bnd_bytes = 0; }
-        CUDA_TRY(ctx, cudaMalloc(&b->d_bnd, bnd_need));
+        if (b->d_bnd) { ctx->release(b->d_bnd); b->d_bnd = nullptr; b->bnd_bytes = 0; }
+        CUDA_TRY(ctx, ctx->alloc(&b->d_bnd, bnd_need));
         b->bnd_bytes = bnd_need;
     }
 
