@@ -317,11 +317,11 @@ struct Shape { int P, K; };
 // packed half2 shapes: short reads in a single stage; (8,32) also chains stages for longer packed reads.
 // (4,38) halves the wavefront ramp of 150 bp reads but needs ~200 registers: measured slower than (8,19) on B200
 // (2 instead of 4 resident blocks per SM), so it is only reachable through WSB_FORCE_SHAPE=3.
-static const Shape kShapesF16[] = {{4, 16}, {8, 19}, {8, 32}, {4, 38}};
+static const Shape kShapesF16[] = {{4, 16}, {8, 19}, {8, 32}, {4, 38}, {16, 16}};
 // int32 shapes: narrow groups for short reads, full warps with wide stages for long reads
 static const Shape kShapesI32[] = {{8, 16}, {16, 16}, {32, 16}};
 constexpr int kNumShapesF16 = 3, kNumShapesI32 = 3;  // shapes the planner may choose
-constexpr int kNumShapes = 4;  // bucket array bound
+constexpr int kNumShapes = 5;  // bucket array bound
 
 static double padded_cost(const Shape& s, int m, int n) {
     const int w = s.P * s.K;
@@ -376,7 +376,8 @@ static KernelSel pick_kernel(int variant, int shape, int atype, int gap, bool ma
             case 0: return pick_short<4, 16>(gap);
             case 1: return pick_short<8, 19>(gap);
             case 2: return pick_short<8, 32>(gap);
-            default: return pick_short<4, 38>(gap);
+            case 3: return pick_short<4, 38>(gap);
+            default: return pick_short<16, 16>(gap);
         }
     }
     if (variant == WSB_VARIANT_F16X2) {
@@ -384,7 +385,8 @@ static KernelSel pick_kernel(int variant, int shape, int atype, int gap, bool ma
             case 0: return pick_gap<ArF16, 4, 16>(atype, gap, masked);
             case 1: return pick_gap<ArF16, 8, 19>(atype, gap, masked);
             case 2: return pick_gap<ArF16, 8, 32>(atype, gap, masked);
-            default: return pick_gap<ArF16, 4, 38>(atype, gap, masked);
+            case 3: return pick_gap<ArF16, 4, 38>(atype, gap, masked);
+            default: return pick_gap<ArF16, 16, 16>(atype, gap, masked);
         }
     }
     switch (shape) {
@@ -418,7 +420,7 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
         if ((int64_t)ms * ((int64_t)m + n) >= (1ll << 29)) { status = WSB_E_LENGTH; return; }
         const bool fits = f16_scheme_ok && wsb_f16_range_ok(sch, m, n);
         if (variant == WSB_VARIANT_F16X2 && !fits) { status = WSB_E_RANGE; return; }
-        if (variant != WSB_VARIANT_I32 && fits) { var = WSB_VARIANT_F16X2; shape = best_shape(kShapesF16, kNumShapesF16, 4, m, n); }
+        if (variant != WSB_VARIANT_I32 && fits) { var = WSB_VARIANT_F16X2; shape = best_shape(kShapesF16, kNumShapesF16, 5, m, n); }
         else { var = WSB_VARIANT_I32; shape = best_shape(kShapesI32, kNumShapesI32, 3, m, n); }
     };
 
