@@ -27,6 +27,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd = [nvcc, *NVCC_FLAGS, "-o", LIB_PATH, *[os.path.join(CSRC, s) for s in SOURCES]]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
+        extra = os.environ.get("WSB_NVCC_EXTRA", "").split()   # tuning aid, e.g. -DWSB_TG_ONLY
+        cmd[1:1] = extra
         subprocess.check_call(cmd, cwd=CSRC)
     return LIB_PATH
 

@@ -222,7 +222,11 @@ template <int K> __device__ __forceinline__ void record_rows(const __half2 (&hm)
 }
 
 template <int P, int K, int GAP>
+#ifdef WSB_SHORT_MINB
+__global__ void __launch_bounds__(kThreads, (K <= 20 ? WSB_SHORT_MINB : 1)) f16_local_short_kernel(const ScoreParams prm) {
+#else
 __global__ void __launch_bounds__(kThreads) f16_local_short_kernel(const ScoreParams prm) {
+#endif
     using AR = ArF16;
     constexpr int GPB = kThreads / P;
     constexpr int NCH = K / 4 + 1;
@@ -245,7 +249,9 @@ __global__ void __launch_bounds__(kThreads) f16_local_short_kernel(const ScorePa
     const __half2 c_mism = AR::splat(mism);
     const __half2 c_nalpha = AR::splat(-prm.alpha);
     const __half2 c_ngamma = AR::splat(-gamma);
+    const __half2 c_ndelta = AR::splat(gamma - prm.alpha);  // -(alpha - gamma)
     const __half2 c_zero = AR::splat(0);
+    (void)c_ndelta;
     // lane 0 sees the matrix' zero left border instead of a neighbour: x * keep + edge on the FMA pipe
     const __half2 keep = AR::splat(t == 0 ? 0 : 1);
     const __half2 edge_ta = t == 0 ? c_nalpha : c_zero;  // (T - alpha) of the border, T = 0
@@ -331,12 +337,26 @@ __global__ void __launch_bounds__(kThreads) f16_local_short_kernel(const ScorePa
         __half2 HM2[K];
 
         auto row = [&](__half2 q, const __half2 (&hin)[K], __half2 (&hout)[K], __half2 hm_diag, __half2& la, __half2& lg,
-                       unsigned tag) {
-            __half2 rm = c_zero;
+                       __half2& rm) {
+            rm = c_zero;
 #pragma unroll
             for (int c = 0; c < K; ++c) {
                 const __half2 d = __hfma2_relu(__heq2(q, sc[c]), c_delta, c == 0 ? hm_diag : hin[c - 1]);
                 // h = max(d, T_up - alpha, T_left - alpha); T = max(d, T_up - gamma, T_left - gamma)
+#ifdef WSB_TG_ONLY
+                __half2 h;
+                if (GAP == GAP_MERGED) {   // one gap array: M = max(T_up, T_left) - gamma; T = max(M, d); h = max(M - (alpha-gamma), d)
+                    const __half2 mx = __hmax2(TG[c], lg);
+                    const __half2 tn = __hmax2(mx, d);
+                    h = __hmax2(__hadd2(mx, c_ndelta), d);
+                    lg = __hadd2(tn, c_ngamma);
+                    TG[c] = lg;
+                } else {
+                    h = __hmax2(__hmax2(TA[c], la), d);
+                    la = __hadd2(h, c_nalpha);
+                    TA[c] = la;
+                }
+#else
                 const __half2 h = __hmax2(__hmax2(TA[c], la), d);
                 if (GAP == GAP_MERGED) {
                     const __half2 tn = __hmax2(__hmax2(TG[c], lg), d);
@@ -347,11 +367,10 @@ __global__ void __launch_bounds__(kThreads) f16_local_short_kernel(const ScorePa
                     la = __hadd2(h, c_nalpha);
                 }
                 TA[c] = la;
+#endif
                 hout[c] = __hadd2(h, c_mism);
                 rm = __hmax2(rm, h);
             }
-            record_rows<K>(hout, rm, bestvec, snap_addr, tag);
-            bestvec = __hmax2(bestvec, rm);
         };
         unsigned qa_next, qb_next;  // query symbols are fetched one trip ahead of their use
         asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(qa_next), "=r"(qb_next) : "r"(qaddr) : "memory");
@@ -359,23 +378,31 @@ __global__ void __launch_bounds__(kThreads) f16_local_short_kernel(const ScorePa
         while (qaddr != qend) {
             const unsigned qa = qa_next, qb = qb_next;
             asm volatile("ld.shared.v2.b32 {%0, %1}, [%2+8];" : "=r"(qa_next), "=r"(qb_next) : "r"(qaddr) : "memory");
-            __half2 laA = ta_lA, lgA = tg_lA, laB = ta_lB, lgB = tg_lB;
-            row(u2h(qa), HM, HM2, hm_dA, laA, lgA, qaddr);
-            row(u2h(qb), HM2, HM, hm_lA, laB, lgB, qaddr + 4);
-            qaddr += 8;
-            // right-most columns of both rows to the next lane (used by its next trip)
+            __half2 laA = ta_lA, lgA = tg_lA, laB = ta_lB, lgB = tg_lB, rmA, rmB;
+            row(u2h(qa), HM, HM2, hm_dA, laA, lgA, rmA);
+            record_rows<K>(HM2, rmA, bestvec, snap_addr, qaddr);
+            bestvec = __hmax2(bestvec, rmA);
+            row(u2h(qb), HM2, HM, hm_lA, laB, lgB, rmB);
+            // right-most columns of both rows to the next lane (used by its next trip).  The shuffles go out before
+            // row B's snapshot stores so that they do not queue behind them in the shared-memory pipe.
             hm_dA = hm_lB;
             const __half2 s0 = __shfl_up_sync(0xffffffffu, laA, 1, P);
             const __half2 s1 = __shfl_up_sync(0xffffffffu, HM2[K - 1], 1, P);
             const __half2 s2 = __shfl_up_sync(0xffffffffu, laB, 1, P);
             const __half2 s3 = __shfl_up_sync(0xffffffffu, HM[K - 1], 1, P);
+            __half2 s4 = c_zero, s5 = c_zero;
+            if (GAP == GAP_MERGED) {
+                s4 = __shfl_up_sync(0xffffffffu, lgA, 1, P);
+                s5 = __shfl_up_sync(0xffffffffu, lgB, 1, P);
+            }
+            record_rows<K>(HM, rmB, bestvec, snap_addr, qaddr + 4);
+            bestvec = __hmax2(bestvec, rmB);
+            qaddr += 8;
             ta_lA = __hfma2(s0, keep, edge_ta);
             hm_lA = __hfma2(s1, keep, edge_hm);
             ta_lB = __hfma2(s2, keep, edge_ta);
             hm_lB = __hfma2(s3, keep, edge_hm);
             if (GAP == GAP_MERGED) {
-                const __half2 s4 = __shfl_up_sync(0xffffffffu, lgA, 1, P);
-                const __half2 s5 = __shfl_up_sync(0xffffffffu, lgB, 1, P);
                 tg_lA = __hfma2(s4, keep, edge_tg);
                 tg_lB = __hfma2(s5, keep, edge_tg);
             }
