@@ -1,0 +1,260 @@
+// score_long.cuh -- int32 score kernel for long reads (1 kbp .. 100 kbp+): column stages of one pair are pipelined
+// over the warps of a block, only the stage borders leave the register file.
+//
+// A pair's matrix is cut into column stages of 32 lanes x 16 columns = 512 columns.  Warp w of a block of NW warps owns
+// stages w, w + NW, w + 2 NW, ... and sweeps each of them top to bottom as a lane wavefront (lane t computes row it - t
+// at iteration it, exactly like score_kernels.cuh).  A stage's right-most column {T - gamma, H} is the only state the
+// next stage needs; lane 31 streams it row by row into a global scratch column (8 bytes per row, L2 resident), and
+// the warp owning the next stage follows 64-96 rows behind: it polls a shared-memory progress counter once per 32 rows,
+// pulls the next 32 border rows with one coalesced 256-byte load, parks them in shared memory and feeds lane 0 from
+// there.  So a 100 kbp x 100 kbp pair keeps up to 16 warps busy instead of one, a 10 kbp pair four, and no lane ever
+// waits on a per-row global load.  NW + 1 scratch columns per block make the reuse of a column race-free by
+// construction: the warp that overwrites column (s mod (NW+1)) with stage s + NW + 1 is the warp that consumed it.
+//
+// Blocks take pairs from a work queue (atomic counter) over a work-descending list, i.e. longest-processing-time-first.
+//
+// Cell update (reference: _kernels.py:259-276 merged affine, :113-126 linear; same algebra as score_kernels.cuh, with
+// TA = T - alpha and TG = T - gamma kept per column so that both maxima are single 3-input DPX instructions):
+//     sigma = PRMT(profile[c], query selector)                 ALU   profile word = sigma for query symbols 0..3
+//     d     = H_diag + sigma                                   IMAD  (FMA pipe)
+//     h     = max3(TA_up, TA_left, d [,0])                     VIMNMX3[.RELU]
+//     tn    = max3(TG_up, TG_left, d [,0])                     VIMNMX3[.RELU]
+//     TA    = tn - alpha ; TG = tn - gamma                     2 x IMAD/IADD
+// = 3 ALU + 3 FMA-pipe instructions per cell (the reference counts 7, local 8: _kernels.py:277-279).
+#pragma once
+#include "score_kernels.cuh"
+
+namespace wsb {
+
+constexpr int kLongK = 16;
+constexpr int kLongW = 32 * kLongK;
+constexpr int kLongMaxWarps = 16;
+
+struct LongParams {
+    const uint8_t* q_codes; const int64_t* q_off; const int32_t* q_len;
+    const uint8_t* s_codes; const int64_t* s_off; const int32_t* s_len;
+    const int32_t* pair_q; const int32_t* pair_s;
+    const int32_t* units;  // pair indices, work-descending
+    int64_t n_units;
+    int32_t* out_score; int32_t* out_i; int32_t* out_j;
+    int32_t match, mismatch, alpha, beta;  // beta == alpha for the linear model
+    int2* bnd;             // per block: (NW + 1) border columns of bnd_rows entries {T - gamma, H}
+    int64_t bnd_rows;
+    unsigned int* queue;   // work queue head, zeroed before the launch
+    int32_t one;           // 1, opaque to the compiler: keeps selected adds on the FMA pipe as IMAD
+};
+
+__device__ __forceinline__ int prmt(unsigned a, unsigned b, unsigned sel) {
+    unsigned d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return (int)d;
+}
+// a * one + b with one == 1 at run time: an add that issues on the FMA pipe
+__device__ __forceinline__ int fma_add(int a, int one, int b) {
+    int d;
+    asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(one), "r"(b));
+    return d;
+}
+
+template <int ATYPE, int GAP>
+__global__ void __launch_bounds__(kLongMaxWarps * 32) score_long_kernel(const LongParams prm) {
+    constexpr int K = kLongK, W = kLongW;
+    constexpr bool LOCAL = ATYPE == AT_LOCAL;
+    constexpr bool SEMI = ATYPE == AT_SEMI;
+    constexpr bool GLOBAL_EDGES = ATYPE == AT_GLOBAL;
+    constexpr bool MERGED = GAP == GAP_MERGED;
+    static_assert(GAP == GAP_LINEAR || GAP == GAP_MERGED, "the exact three-state model stays in score_kernel");
+
+    __shared__ int s_prog[kLongMaxWarps];           // border rows published by each warp, summed over its stages
+    __shared__ int s_unit;
+    __shared__ int s_red[kLongMaxWarps][3];
+    __shared__ int2 s_in[kLongMaxWarps][64];        // two chunks of 32 incoming border rows per warp
+
+    const int NW = blockDim.x >> 5;
+    const int w = threadIdx.x >> 5;
+    const int t = threadIdx.x & 31;
+    const int alpha = prm.alpha, beta = prm.beta, mism = prm.mismatch, one = prm.one;
+    const int gamma = MERGED ? min(alpha, beta) : alpha;
+    const int nalpha = -alpha, ngamma = -gamma;
+    const unsigned mism4 = (unsigned)(mism & 0xff) * 0x01010101u;
+    int2* const bnd_block = prm.bnd + (int64_t)blockIdx.x * (NW + 1) * prm.bnd_rows;
+    volatile int* prog = s_prog;
+
+    for (;;) {
+        __syncthreads();  // previous pair fully retired (progress counters, reduction slots)
+        if (threadIdx.x == 0) s_unit = (int)atomicAdd(prm.queue, 1u);
+        if (threadIdx.x < kLongMaxWarps) s_prog[threadIdx.x] = 0;
+        __syncthreads();
+        const int64_t u = s_unit;
+        if (u >= prm.n_units) break;
+        const int p = prm.units[u];
+        const int qa = prm.pair_q[p], sb = prm.pair_s[p];
+        const int m = prm.q_len[qa], n = prm.s_len[sb];
+        const uint8_t* qp = prm.q_codes + prm.q_off[qa];
+        const uint8_t* sp = prm.s_codes + prm.s_off[sb];
+        const int nstages = (n + W - 1) / W;
+
+        int best_v = GLOBAL_EDGES ? kNeg32 : 0, best_i = 0, best_j = SEMI ? n : 0;
+
+        int k_local = 0;
+        for (int st = w; st < nstages; st += NW, ++k_local) {
+            const bool first = st == 0, last = st + 1 == nstages;
+            const int col0 = st * W + t * K;  // this strip holds matrix columns col0+1 .. col0+K
+            unsigned prof[K];
+            int TA[K], H[K], TG[MERGED ? K : 1];
+#pragma unroll
+            for (int c = 0; c < K; ++c) {
+                unsigned pw = mism4;  // pad / flagged subject: never matches
+                if (col0 + c < n) {
+                    const int x = sp[col0 + c];
+                    if (x < 4) pw = (mism4 & ~(0xffu << (8 * x))) | ((unsigned)(prm.match & 0xff) << (8 * x));
+                }
+                prof[c] = pw;
+                const int h0 = edge_h(GLOBAL_EDGES, col0 + c + 1, alpha, beta);
+                H[c] = h0; TA[c] = h0 - alpha;
+                if (MERGED) TG[c] = h0 - gamma;
+            }
+            const int h_top = edge_h(GLOBAL_EDGES, col0, alpha, beta);  // H(0, col0): diagonal of this strip's row 1
+            int hdiag = h_top;
+            int tg_l = kNeg32, h_l = kNeg32;        // left border {T - gamma, H} of the row this lane computes next
+            int edge = edge_h(GLOBAL_EDGES, 1, alpha, beta);   // stage 0: H(r, 0) of lane 0's next row
+            // incoming border column (stage st - 1) and its producer
+            const int2* in_col = bnd_block + (int64_t)((st + NW) % (NW + 1)) * prm.bnd_rows;   // (st - 1) mod (NW + 1)
+            int2* out_col = bnd_block + (int64_t)(st % (NW + 1)) * prm.bnd_rows;
+            const int pw_id = (w + NW - 1) % NW;
+            const int p_base = (w == 0 ? k_local - 1 : k_local) * m;  // producer's published rows before its stage
+            int2 pre = make_int2(kNeg32, kNeg32);
+            auto fetch_chunk = [&](int chunk) {   // rows 32*chunk+1 .. 32*chunk+32 of the incoming column -> pre
+                const int row0 = 32 * chunk;
+                if (row0 >= m) return;
+                const int need = p_base + min(m, row0 + 32);
+                while (prog[pw_id] < need) __nanosleep(40);
+                __threadfence_block();
+                pre = __ldcg(in_col + row0 + t);
+            };
+            if (!first) {
+                fetch_chunk(0);
+                s_in[w][t] = pre;
+                fetch_chunk(1);
+                __syncwarp();
+                if (t == 0) { const int2 b = s_in[w][0]; tg_l = b.x; h_l = b.y; }
+            } else if (t == 0) {
+                h_l = edge; tg_l = edge - gamma;
+            }
+            const int cap_rel = n - 1 - col0;  // register index of matrix column n, if inside this strip
+            const bool has_cap = last && cap_rel >= 0 && cap_rel < K;
+
+            // query symbols, fetched two iterations ahead (row of iteration it is it - t)
+            auto qsel_at = [&](int it) {
+                const int row = min(max(it - t - 1, 0), m - 1);
+                return (int)qp[row];
+            };
+            int q_cur = qsel_at(1), q_nxt = qsel_at(2);
+
+            const int it_end = m + 31;
+#pragma unroll 1
+            for (int it = 1; it <= it_end; ++it) {
+                const int q_nn = qsel_at(it + 2);
+                if (!first && (it & 31) == 0) {  // park the prefetched chunk, start fetching the one after it
+                    s_in[w][(it & 63) + t] = pre;
+                    fetch_chunk((it >> 5) + 1);
+                    __syncwarp();
+                }
+                const int r = it - t;
+                int out_tg = tg_l, out_h = h_l;
+                if ((unsigned)(r - 1) < (unsigned)m) {
+                    const unsigned sel = (unsigned)min(q_cur, 4) * 0x1111u + 0x8880u;
+                    int hd = hdiag;
+                    int la = MERGED ? tg_l + (gamma - alpha) : h_l - alpha;   // T_left - alpha
+                    int lg = tg_l;
+                    int rm = 0;
+#pragma unroll
+                    for (int c = 0; c < K; ++c) {
+                        const int d = fma_add(prmt(prof[c], mism4, sel), one, hd);
+                        hd = H[c];
+                        const int h = LOCAL ? __vimax3_s32_relu(TA[c], la, d) : __vimax3_s32(TA[c], la, d);
+                        if (MERGED) {
+                            const int tn = LOCAL ? __vimax3_s32_relu(TG[c], lg, d) : __vimax3_s32(TG[c], lg, d);
+                            la = fma_add(tn, one, nalpha);
+                            lg = tn + ngamma;
+                            TG[c] = lg;
+                        } else {
+                            la = h + nalpha;
+                        }
+                        TA[c] = la;
+                        H[c] = h;
+                        if (LOCAL) {
+                            if (c & 1) rm = __vimax3_s32(rm, H[c - 1], h);
+                        }
+                    }
+                    out_tg = lg; out_h = H[K - 1];
+                    if (LOCAL) {
+                        if (rm >= best_v && rm > 0 && (rm > best_v || r < best_i)) {  // rare: a new record row
+                            int pos = K - 1;
+#pragma unroll
+                            for (int c = K - 2; c >= 0; --c) if (H[c] == rm) pos = c;
+                            best_v = rm; best_i = r; best_j = col0 + pos + 1;
+                        }
+                    }
+                    if (SEMI && has_cap && r < m) {  // last matrix column, rows above the last one
+                        const int hv = select_reg<int, K>(H, cap_rel);
+                        if (better_cell(hv, r, n, best_v, best_i, best_j)) { best_v = hv; best_i = r; best_j = n; }
+                    }
+                    if (t == 31 && !last) {
+                        out_col[r - 1] = make_int2(out_tg, out_h);
+                        if ((r & 31) == 0 || r == m) {
+                            __threadfence_block();
+                            prog[w] = k_local * m + r;
+                        }
+                    }
+                }
+                // right-most column to the next lane; lane 0 takes the stage's left border of row it + 1
+                int ntg = __shfl_up_sync(0xffffffffu, out_tg, 1);
+                int nh = __shfl_up_sync(0xffffffffu, out_h, 1);
+                hdiag = h_l;
+                if (first) {
+                    if (GLOBAL_EDGES) edge -= beta;
+                    if (t == 0) { nh = edge; ntg = edge - gamma; }
+                } else {
+                    const int2 b = s_in[w][it & 63];  // row it + 1 sits in slot (it + 1 - 1) & 63
+                    if (t == 0) { ntg = b.x; nh = b.y; }
+                }
+                tg_l = ntg; h_l = nh;
+                if (r == 0) hdiag = h_top;
+                q_cur = q_nxt; q_nxt = q_nn;
+            }
+            // rows are complete: every lane's registers hold row m of its strip
+            if (SEMI) {
+#pragma unroll
+                for (int c = 0; c < K; ++c)
+                    if (col0 + c < n && better_cell(H[c], m, col0 + c + 1, best_v, best_i, best_j)) {
+                        best_v = H[c]; best_i = m; best_j = col0 + c + 1;
+                    }
+            }
+            if (GLOBAL_EDGES && has_cap) { best_v = select_reg<int, K>(H, cap_rel); best_i = m; best_j = n; }
+            __syncwarp();
+        }
+
+        // reduce over lanes, then over warps: larger value, then smaller row, then smaller column
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+            const int ov = __shfl_xor_sync(0xffffffffu, best_v, off);
+            const int oi = __shfl_xor_sync(0xffffffffu, best_i, off);
+            const int oj = __shfl_xor_sync(0xffffffffu, best_j, off);
+            if (better_cell(ov, oi, oj, best_v, best_i, best_j)) { best_v = ov; best_i = oi; best_j = oj; }
+        }
+        if (t == 0) { s_red[w][0] = best_v; s_red[w][1] = best_i; s_red[w][2] = best_j; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int bv = s_red[0][0], bi = s_red[0][1], bj = s_red[0][2];
+            for (int x = 1; x < NW; ++x)
+                if (better_cell(s_red[x][0], s_red[x][1], s_red[x][2], bv, bi, bj)) {
+                    bv = s_red[x][0]; bi = s_red[x][1]; bj = s_red[x][2];
+                }
+            if (LOCAL && bv <= 0) { bv = 0; bi = 0; bj = 0; }
+            prm.out_score[p] = bv; prm.out_i[p] = bi; prm.out_j[p] = bj;
+        }
+    }
+}
+
+}  // namespace wsb

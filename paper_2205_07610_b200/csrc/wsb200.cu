@@ -4,6 +4,7 @@
 #include "../../include/wsb200.h"
 #include "score_kernels.cuh"
 #include "score_short.cuh"
+#include "score_long.cuh"
 #include "traceback_kernels.cuh"
 
 #include <cuda_runtime.h>
@@ -29,6 +30,11 @@ struct wsb_ctx {
     int sm_count = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // launch groups of the long-read kernel run side by side on these streams (fork after ev0, join before ev1)
+    static constexpr int kAux = 6;
+    cudaStream_t aux[kAux] = {};
+    cudaEvent_t aux_done[kAux] = {};
+    unsigned int* d_queues = nullptr;  // work-queue heads of the long-read launches
     std::string last_error;
     // Device-memory cache: batches come and go with every run_batch call, and cudaMalloc/cudaFree of GB-sized pools
     // cost tens of milliseconds each, so freed blocks are kept (size-bucketed, 2 MiB granularity) and reused.
@@ -73,6 +79,7 @@ struct LaunchGroup {  // pairs that run in one kernel launch
     int64_t n_units = 0;
     int64_t unit_off = 0;  // offset (in int32) into the plan's unit array; -1 = identity mapping
     int max_m = 0, max_n = 0;
+    int long_nw = 0;       // > 0: long-read kernel with this many warps per pair (score_long.cuh)
 };
 
 struct Plan {
@@ -202,6 +209,11 @@ extern "C" int wsb_ctx_create(int device, wsb_ctx** out) {
         delete c;
         return WSB_E_CUDA;
     }
+    bool ok = cudaMalloc((void**)&c->d_queues, 64 * sizeof(unsigned int)) == cudaSuccess;
+    for (int k = 0; k < wsb_ctx::kAux && ok; ++k)
+        ok = cudaStreamCreateWithFlags(&c->aux[k], cudaStreamNonBlocking) == cudaSuccess &&
+             cudaEventCreateWithFlags(&c->aux_done[k], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) { (void)cudaGetLastError(); wsb_ctx_destroy(c); return WSB_E_CUDA; }
     *out = c;
     return WSB_OK;
 }
@@ -212,6 +224,11 @@ extern "C" void wsb_ctx_destroy(wsb_ctx* c) {
     c->trim();
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
+    for (int k = 0; k < wsb_ctx::kAux; ++k) {
+        if (c->aux[k]) cudaStreamDestroy(c->aux[k]);
+        if (c->aux_done[k]) cudaEventDestroy(c->aux_done[k]);
+    }
+    if (c->d_queues) cudaFree(c->d_queues);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -368,6 +385,20 @@ template <int P, int K> static KernelSel pick_short(int gap) {
     return {f16_local_short_kernel<P, K, GAP_MERGED>, short_smem_bytes<P, K>()};
 }
 
+using LongFn = void (*)(const LongParams);
+template <int GAP> static LongFn pick_long_atype(int atype) {
+    switch (atype) {
+        case AT_GLOBAL: return score_long_kernel<AT_GLOBAL, GAP>;
+        case AT_LOCAL: return score_long_kernel<AT_LOCAL, GAP>;
+        default: return score_long_kernel<AT_SEMI, GAP>;
+    }
+}
+static LongFn pick_long(int atype, int gap) {
+    if (gap == GAP_LINEAR) return pick_long_atype<GAP_LINEAR>(atype);
+    if (gap == GAP_MERGED) return pick_long_atype<GAP_MERGED>(atype);
+    return nullptr;
+}
+
 // short_ok: every unit of the launch fits one stage and the short kernel's query buffer
 static KernelSel pick_kernel(int variant, int shape, int atype, int gap, bool masked, bool short_ok) {
     static const char* no_short = getenv("WSB_NO_SHORT");  // tuning aid: force the general kernel
@@ -423,39 +454,97 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
         if (variant != WSB_VARIANT_I32 && fits) { var = WSB_VARIANT_F16X2; shape = best_shape(kShapesF16, kNumShapesF16, 5, m, n); }
         else { var = WSB_VARIANT_I32; shape = best_shape(kShapesI32, kNumShapesI32, 3, m, n); }
     };
+    // The long-read kernel (score_long.cuh) takes the int32 pairs that would otherwise run full-warp stages: it needs
+    // byte-sized substitution scores, the merged (or linear) gap state and, for local alignment, non-improving pads.
+    static const char* no_long = getenv("WSB_NO_LONG");
+    const bool long_scheme_ok = !(no_long && no_long[0]) && gap_i32 != GAP_EXACT && std::abs(sch->match) <= 127 &&
+                                std::abs(sch->mismatch) <= 127 && (atype != AT_LOCAL || (sch->mismatch <= 0 && sch->match >= 0));
+    auto long_ok = [&](int var, int shape, int m, int n) {
+        (void)shape;
+        static const char* thr = getenv("WSB_LONG_MIN_N");  // tuning aid
+        const int min_n = thr && thr[0] ? atoi(thr) : 512;
+        return long_scheme_ok && var == WSB_VARIANT_I32 && m >= 64 && n > min_n;
+    };
 
     if (b->uniform) {
         int var, shape, status;
         classify(b->m[0], b->n[0], var, shape, status);
         if (status) { std::fill(plan.status.begin(), plan.status.end(), status); plan.any_error = true; return WSB_OK; }
         if (var < 0) return WSB_OK;
-        LaunchGroup g;
-        g.variant = var; g.shape = shape; g.gap = var == WSB_VARIANT_F16X2 ? gap_f16 : gap_i32;
-        g.n_units = var == WSB_VARIANT_F16X2 ? (np + 1) / 2 : np;
-        g.unit_off = -1; g.max_m = b->m[0]; g.max_n = b->n[0];
-        plan.groups.push_back(g);
-        return WSB_OK;
+        if (!long_ok(var, shape, b->m[0], b->n[0])) {
+            LaunchGroup g;
+            g.variant = var; g.shape = shape; g.gap = var == WSB_VARIANT_F16X2 ? gap_f16 : gap_i32;
+            g.n_units = var == WSB_VARIANT_F16X2 ? (np + 1) / 2 : np;
+            g.unit_off = -1; g.max_m = b->m[0]; g.max_n = b->n[0];
+            plan.groups.push_back(g);
+            return WSB_OK;
+        }
     }
 
     // general path: bucket, sort by work (descending), pair neighbours
     std::vector<int64_t> bucket[2][kNumShapes];
+    std::vector<int64_t> long_pairs;
+    double long_iters = 0.0;  // single-warp iterations of all long-class pairs
     for (int64_t p = 0; p < np; ++p) {
         int var, shape, status;
         classify(b->m[p], b->n[p], var, shape, status);
         if (status) { plan.status[p] = status; plan.any_error = true; continue; }
         if (var < 0) continue;
-        bucket[var == WSB_VARIANT_F16X2 ? 0 : 1][shape].push_back(p);
+        if (long_ok(var, shape, b->m[p], b->n[p])) {
+            long_pairs.push_back(p);
+            long_iters += (double)((b->n[p] + kLongW - 1) / kLongW) * (b->m[p] + 31);
+        } else {
+            bucket[var == WSB_VARIANT_F16X2 ? 0 : 1][shape].push_back(p);
+        }
     }
     std::vector<int32_t> units;
+    auto by_work = [&](int64_t x, int64_t y) {
+        const int64_t cx = (int64_t)b->m[x] * b->n[x], cy = (int64_t)b->m[y] * b->n[y];
+        if (cx != cy) return cx > cy;
+        return b->n[x] > b->n[y];
+    };
+    // long-read pairs: warps per pair.  A pair must not outlast a fraction of the whole launch's makespan (so the
+    // giants of a skewed batch get up to 16 warps), beyond that the cheapest count in warp-iterations wins (pipeline
+    // fill of ~80 rows per extra warp, idle warps when the stage count is not a multiple).
+    if (!long_pairs.empty()) {
+        std::vector<int64_t> by_nw[kLongMaxWarps + 1];
+        const double machine_warps = (double)ctx->sm_count * 20.0;
+        const double makespan = std::max(long_iters / machine_warps, 1.0);
+        for (int64_t p : long_pairs) {
+            const int stages = (b->n[p] + kLongW - 1) / kLongW;
+            const double t1 = (double)stages * (b->m[p] + 31);
+            int lo = (int)std::min<double>(kLongMaxWarps, std::ceil(t1 / (0.25 * makespan)));
+            lo = std::max(1, std::min(lo, stages));
+            const int hi = std::min({kLongMaxWarps, stages, 2 * lo + 1});
+            int best_nw = lo;
+            double best_cost = 1e300;
+            for (int nw = lo; nw <= hi; ++nw) {
+                const double rounds = (double)((stages + nw - 1) / nw);
+                const double cost = nw * (rounds * (b->m[p] + 31) + (nw - 1) * 80.0);
+                if (cost < best_cost * 0.999) { best_cost = cost; best_nw = nw; }
+            }
+            by_nw[best_nw].push_back(p);
+        }
+        for (int nw = kLongMaxWarps; nw >= 1; --nw) {
+            auto& v = by_nw[nw];
+            if (v.empty()) continue;
+            std::stable_sort(v.begin(), v.end(), by_work);
+            LaunchGroup g;
+            g.variant = WSB_VARIANT_I32; g.shape = 2; g.gap = gap_i32; g.long_nw = nw;
+            g.unit_off = (int64_t)units.size();
+            g.n_units = (int64_t)v.size();
+            for (int64_t p : v) {
+                g.max_m = std::max(g.max_m, b->m[p]); g.max_n = std::max(g.max_n, b->n[p]);
+                units.push_back((int32_t)p);
+            }
+            plan.groups.push_back(g);
+        }
+    }
     for (int cls = 0; cls < 2; ++cls)
         for (int s = 0; s < kNumShapes; ++s) {
             auto& v = bucket[cls][s];
             if (v.empty()) continue;
-            std::stable_sort(v.begin(), v.end(), [&](int64_t x, int64_t y) {
-                const int64_t cx = (int64_t)b->m[x] * b->n[x], cy = (int64_t)b->m[y] * b->n[y];
-                if (cx != cy) return cx > cy;
-                return b->n[x] > b->n[y];
-            });
+            std::stable_sort(v.begin(), v.end(), by_work);
             LaunchGroup g;
             g.variant = cls == 0 ? WSB_VARIANT_F16X2 : WSB_VARIANT_I32;
             g.shape = s; g.gap = cls == 0 ? gap_f16 : gap_i32;
@@ -530,11 +619,23 @@ extern "C" int wsb_batch_score(wsb_batch* b, const wsb_scheme* sch, int atype, i
     const Plan& plan = it->second;
     b->last_plan = &plan;
 
-    // launch geometry + border scratch
-    struct Geo { KernelFn fn; size_t smem; int grid; int64_t bnd_rows; };
+    // launch geometry + border scratch (every launch group owns a slice: long-read groups run concurrently)
+    struct Geo { KernelFn fn; LongFn lfn; size_t smem; int grid; int64_t bnd_rows; size_t bnd_off; };
     std::vector<Geo> geo;
     size_t bnd_need = 0;
     for (const LaunchGroup& g : plan.groups) {
+        if (g.long_nw > 0) {
+            LongFn lfn = pick_long(atype, g.gap);
+            if (!lfn) return WSB_E_SCHEME;
+            int per_sm = 0;
+            CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lfn, g.long_nw * 32, 0));
+            per_sm = std::max(per_sm, 1);
+            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(g.n_units, (int64_t)ctx->sm_count * per_sm));
+            const int64_t rows = ((int64_t)g.max_m + 31) / 32 * 32 + 64;
+            geo.push_back({nullptr, lfn, 0, grid, rows, bnd_need});
+            bnd_need += (size_t)rows * sizeof(int2) * (size_t)(g.long_nw + 1) * (size_t)grid;
+            continue;
+        }
         const Shape sh = g.variant == WSB_VARIANT_F16X2 ? kShapesF16[g.shape] : kShapesI32[g.shape];
         const bool short_ok = g.max_n <= sh.P * sh.K && g.max_m <= kShortQRows - 4 * sh.P - 2;
         const KernelSel sel = pick_kernel(g.variant, g.shape, atype, g.gap, sch->mismatch > 0 || sch->match < 0, short_ok);
@@ -549,19 +650,39 @@ extern "C" int wsb_batch_score(wsb_batch* b, const wsb_scheme* sch, int atype, i
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(blocks_needed, (int64_t)ctx->sm_count * per_sm));
         const bool multi_stage = g.max_n > sh.P * sh.K;
         const int64_t rows = multi_stage ? (int64_t)g.max_m + 2 : 0;
-        geo.push_back({fn, sel.smem, grid, rows});
-        bnd_need = std::max(bnd_need, (size_t)rows * 8u * (size_t)grid * gpb);
+        geo.push_back({fn, nullptr, sel.smem, grid, rows, bnd_need});
+        bnd_need += ((size_t)rows * 8u * (size_t)grid * gpb + 255) / 256 * 256;
     }
     if (bnd_need > b->bnd_bytes) {
         if (b->d_bnd) { ctx->release(b->d_bnd); b->d_bnd = nullptr; b->bnd_bytes = 0; }
         CUDA_TRY(ctx, ctx->alloc(&b->d_bnd, bnd_need));
         b->bnd_bytes = bnd_need;
     }
+    if (plan.groups.size() > 64) return WSB_E_ARG;  // cannot happen: at most 16 + 10 launch groups per plan
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_queues, 0, 64 * sizeof(unsigned int), ctx->stream));
 
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
-    int launches = 0;
+    int launches = 0, n_aux = 0;
+    bool aux_used[wsb_ctx::kAux] = {};
     for (size_t k = 0; k < plan.groups.size(); ++k) {
         const LaunchGroup& g = plan.groups[k];
+        if (g.long_nw > 0) {  // long-read groups, largest warps-per-pair first, each on its own stream
+            const int a = n_aux++ % wsb_ctx::kAux;
+            if (!aux_used[a]) { CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->aux[a], ctx->ev0, 0)); aux_used[a] = true; }
+            LongParams lp;
+            lp.q_codes = b->d_qcodes; lp.q_off = b->d_qoff; lp.q_len = b->d_qlen;
+            lp.s_codes = b->d_scodes; lp.s_off = b->d_soff; lp.s_len = b->d_slen;
+            lp.pair_q = b->d_pq; lp.pair_s = b->d_ps;
+            lp.units = plan.d_units + g.unit_off; lp.n_units = g.n_units;
+            lp.out_score = b->d_score; lp.out_i = b->d_i; lp.out_j = b->d_j;
+            lp.match = sch->match; lp.mismatch = sch->mismatch; lp.alpha = sch->gap_open; lp.beta = beta_eff;
+            lp.bnd = reinterpret_cast<int2*>((char*)b->d_bnd + geo[k].bnd_off); lp.bnd_rows = geo[k].bnd_rows;
+            lp.queue = ctx->d_queues + k; lp.one = 1;
+            geo[k].lfn<<<geo[k].grid, g.long_nw * 32, 0, ctx->aux[a]>>>(lp);
+            CUDA_TRY(ctx, cudaGetLastError());
+            ++launches;
+            continue;
+        }
         ScoreParams prm;
         prm.q_codes = b->d_qcodes; prm.q_off = b->d_qoff; prm.q_len = b->d_qlen;
         prm.s_codes = b->d_scodes; prm.s_off = b->d_soff; prm.s_len = b->d_slen;
@@ -570,11 +691,16 @@ extern "C" int wsb_batch_score(wsb_batch* b, const wsb_scheme* sch, int atype, i
         prm.n_units = g.n_units; prm.n_pairs = b->n_pairs;
         prm.out_score = b->d_score; prm.out_i = b->d_i; prm.out_j = b->d_j;
         prm.match = sch->match; prm.mismatch = sch->mismatch; prm.alpha = sch->gap_open; prm.beta = beta_eff;
-        prm.bnd = geo[k].bnd_rows ? b->d_bnd : nullptr; prm.bnd_rows = geo[k].bnd_rows;
+        prm.bnd = geo[k].bnd_rows ? (char*)b->d_bnd + geo[k].bnd_off : nullptr; prm.bnd_rows = geo[k].bnd_rows;
         geo[k].fn<<<geo[k].grid, kThreads, geo[k].smem, ctx->stream>>>(prm);
         CUDA_TRY(ctx, cudaGetLastError());
         ++launches;
     }
+    for (int a = 0; a < wsb_ctx::kAux; ++a)
+        if (aux_used[a]) {
+            CUDA_TRY(ctx, cudaEventRecord(ctx->aux_done[a], ctx->aux[a]));
+            CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->aux_done[a], 0));
+        }
     {  // empty-side pairs (only possible for non-uniform batches or a uniform batch of empties)
         bool any_empty = false;
         if (b->uniform) any_empty = b->m[0] == 0 || b->n[0] == 0;

@@ -118,3 +118,52 @@ def test_forced_f16_reports_range_status(ctx):
     assert got[3][0] == 0 and got[3][1] == N.WSB_E_RANGE
     with pytest.raises(ValueError):
         gpu_scores(ctx, qs, ss, [(0, 0)], scheme_of((2, -9, 2, 1), "affine"), "local", "f16x2")
+
+
+@pytest.mark.parametrize("align_type,gap_model", COMBOS)
+def test_long_read_kernel_mixed_lengths(ctx, align_type, gap_model):
+    """Pipelined long-read kernel (score_long.cuh): skewed lengths so that several warps-per-pair classes launch side
+    by side, flagged symbols, related and unrelated pairs, lengths straddling the 512-column stage width."""
+    rng = np.random.default_rng(2205)
+    pool = AFFINE_SCHEMES[:2] if gap_model == "affine" else LINEAR_SCHEMES[:2]
+    lens = [257, 300, 511, 512, 513, 1023, 1024, 1025, 1536, 2049, 3000, 4100, 64, 65, 9000, 12000]
+    qs, ss = [], []
+    for L in lens:
+        q = random_codes(rng, L)
+        s = mutate_codes(rng, q, 0.08, 0.03, 0.03) if rng.random() < 0.6 else random_codes(rng, int(L * rng.uniform(0.8, 1.25)))
+        if rng.random() < 0.3:
+            q = q.copy(); q[rng.integers(0, len(q), 3)] = 4
+            s = s.copy(); s[rng.integers(0, len(s), 3)] = 4
+        qs.append(q); ss.append(s)
+    for _ in range(40):
+        L = int(rng.integers(260, 2000))
+        qs.append(random_codes(rng, L)); ss.append(mutate_codes(rng, qs[-1], 0.1, 0.05, 0.05))
+    qs.append(random_codes(rng, 70)); ss.append(random_codes(rng, 5000))    # wide and flat
+    qs.append(random_codes(rng, 5000)); ss.append(random_codes(rng, 300))   # tall and narrow
+    pairs = [(i, i) for i in range(len(qs))]
+    for sch in pool:
+        scheme = scheme_of(sch, gap_model)
+        want = oracle_scores(qs, ss, pairs, scheme, align_type)
+        got = gpu_scores(ctx, qs, ss, pairs, scheme, align_type, "auto")
+        assert_scores_equal(got, want, f"long {align_type}/{gap_model}/{sch}")
+
+
+@pytest.mark.parametrize("align_type", ["global", "local", "semiglobal"])
+def test_long_read_kernel_uniform_batch(ctx, align_type):
+    rng = np.random.default_rng(77)
+    scheme = scheme_of((2, -1, 2, 1), "affine")
+    qs = [random_codes(rng, 2600) for _ in range(48)]
+    ss = [np.resize(mutate_codes(rng, q, 0.05, 0.02, 0.02), 2600) if i % 2 else random_codes(rng, 2600) for i, q in enumerate(qs)]
+    pairs = [(i, i) for i in range(len(qs))]
+    assert_scores_equal(gpu_scores(ctx, qs, ss, pairs, scheme, align_type), oracle_scores(qs, ss, pairs, scheme, align_type),
+                        f"uniform long {align_type}")
+
+
+def test_long_reads_with_non_merged_scheme_use_exact_model(ctx):
+    rng = np.random.default_rng(78)
+    scheme = scheme_of((2, -9, 2, 1), "affine")   # merged state not exact -> three-state kernel
+    qs = [random_codes(rng, 1400) for _ in range(6)]
+    ss = [mutate_codes(rng, q, 0.1, 0.05, 0.05) for q in qs]
+    pairs = [(i, i) for i in range(len(qs))]
+    for at in ("global", "local", "semiglobal"):
+        assert_scores_equal(gpu_scores(ctx, qs, ss, pairs, scheme, at), oracle_scores(qs, ss, pairs, scheme, at), at)
