@@ -24,6 +24,8 @@
 #pragma once
 #include "score_kernels.cuh"
 
+#include <type_traits>
+
 namespace wsb {
 
 constexpr int kLongK = 16;
@@ -68,7 +70,7 @@ __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long_kernel(const Lo
     __shared__ int s_prog[kLongMaxWarps];           // border rows published by each warp, summed over its stages
     __shared__ int s_unit;
     __shared__ int s_red[kLongMaxWarps][3];
-    __shared__ int2 s_in[kLongMaxWarps][64];        // two chunks of 32 incoming border rows per warp
+    __shared__ int4 s_in[kLongMaxWarps][64];        // two chunks of 32 rows of lane-0 inputs per warp: {T - gamma, H, selector}
 
     const int NW = blockDim.x >> 5;
     const int w = threadIdx.x >> 5;
@@ -117,53 +119,48 @@ __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long_kernel(const Lo
             const int h_top = edge_h(GLOBAL_EDGES, col0, alpha, beta);  // H(0, col0): diagonal of this strip's row 1
             int hdiag = h_top;
             int tg_l = kNeg32, h_l = kNeg32;        // left border {T - gamma, H} of the row this lane computes next
-            int edge = edge_h(GLOBAL_EDGES, 1, alpha, beta);   // stage 0: H(r, 0) of lane 0's next row
+            unsigned sel = 0x8880u;                 // PRMT selector of that row's query symbol
+            int edge = edge_h(GLOBAL_EDGES, 1, alpha, beta);   // stage 0: H(r, 0) of lane 0's current row
             // incoming border column (stage st - 1) and its producer
             const int2* in_col = bnd_block + (int64_t)((st + NW) % (NW + 1)) * prm.bnd_rows;   // (st - 1) mod (NW + 1)
-            int2* out_col = bnd_block + (int64_t)(st % (NW + 1)) * prm.bnd_rows;
+            int2* out_ptr = bnd_block + (int64_t)(st % (NW + 1)) * prm.bnd_rows - 32;  // lane 31: row it - 31 -> slot it - 32
             const int pw_id = (w + NW - 1) % NW;
             const int p_base = (w == 0 ? k_local - 1 : k_local) * m;  // producer's published rows before its stage
-            int2 pre = make_int2(kNeg32, kNeg32);
-            auto fetch_chunk = [&](int chunk) {   // rows 32*chunk+1 .. 32*chunk+32 of the incoming column -> pre
-                const int row0 = 32 * chunk;
-                if (row0 >= m) return;
-                const int need = p_base + min(m, row0 + 32);
-                while (prog[pw_id] < need) __nanosleep(40);
-                __threadfence_block();
-                pre = __ldcg(in_col + row0 + t);
-            };
-            if (!first) {
-                fetch_chunk(0);
-                s_in[w][t] = pre;
-                fetch_chunk(1);
-                __syncwarp();
-                if (t == 0) { const int2 b = s_in[w][0]; tg_l = b.x; h_l = b.y; }
-            } else if (t == 0) {
-                h_l = edge; tg_l = edge - gamma;
-            }
+            const bool do_out = t == 31 && !last;
             const int cap_rel = n - 1 - col0;  // register index of matrix column n, if inside this strip
             const bool has_cap = last && cap_rel >= 0 && cap_rel < K;
 
-            // query symbols, fetched two iterations ahead (row of iteration it is it - t)
-            auto qsel_at = [&](int it) {
-                const int row = min(max(it - t - 1, 0), m - 1);
-                return (int)qp[row];
-            };
-            int q_cur = qsel_at(1), q_nxt = qsel_at(2);
-
-            const int it_end = m + 31;
-#pragma unroll 1
-            for (int it = 1; it <= it_end; ++it) {
-                const int q_nn = qsel_at(it + 2);
-                if (!first && (it & 31) == 0) {  // park the prefetched chunk, start fetching the one after it
-                    s_in[w][(it & 63) + t] = pre;
-                    fetch_chunk((it >> 5) + 1);
-                    __syncwarp();
+            // Rows 32c+1 .. 32c+32 of lane 0's inputs (incoming border + query selector) are fetched one chunk ahead
+            // with coalesced loads, parked in shared memory, and read back one row per iteration.
+            int2 pre = make_int2(kNeg32, kNeg32);
+            unsigned pre_sel = 0x8880u;
+            auto fetch_chunk = [&](int chunk) {
+                const int row0 = 32 * chunk;
+                if (row0 >= m) return;
+                const int q = qp[min(row0 + t, m - 1)];
+                pre_sel = (unsigned)min(q, 4) * 0x1111u + 0x8880u;
+                if (!first) {
+                    const int need = p_base + min(m, row0 + 32);
+                    while (prog[pw_id] < need) __nanosleep(40);
+                    __threadfence_block();
+                    pre = __ldcg(in_col + row0 + t);
                 }
+            };
+            fetch_chunk(0);
+
+            // one row of the strip; CHECK = the row may lie outside 1..m (ramp-up / ramp-down chunks)
+            auto iteration = [&](int it, auto check_tag) {
+                constexpr bool CHECK = decltype(check_tag)::value;
+                const int4 in = s_in[w][(it - 1) & 63];   // lane 0's inputs for row it
+                if (t == 0) {
+                    sel = (unsigned)in.z;
+                    if (first) { h_l = edge; tg_l = edge - gamma; }
+                    else { tg_l = in.x; h_l = in.y; }
+                }
+                if (first && GLOBAL_EDGES) edge -= beta;
                 const int r = it - t;
                 int out_tg = tg_l, out_h = h_l;
-                if ((unsigned)(r - 1) < (unsigned)m) {
-                    const unsigned sel = (unsigned)min(q_cur, 4) * 0x1111u + 0x8880u;
+                if (!CHECK || (unsigned)(r - 1) < (unsigned)m) {
                     int hd = hdiag;
                     int la = MERGED ? tg_l + (gamma - alpha) : h_l - alpha;   // T_left - alpha
                     int lg = tg_l;
@@ -176,10 +173,10 @@ __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long_kernel(const Lo
                         if (MERGED) {
                             const int tn = LOCAL ? __vimax3_s32_relu(TG[c], lg, d) : __vimax3_s32(TG[c], lg, d);
                             la = fma_add(tn, one, nalpha);
-                            lg = tn + ngamma;
+                            lg = fma_add(tn, one, ngamma);
                             TG[c] = lg;
                         } else {
-                            la = h + nalpha;
+                            la = fma_add(h, one, nalpha);
                         }
                         TA[c] = la;
                         H[c] = h;
@@ -200,28 +197,35 @@ __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long_kernel(const Lo
                         const int hv = select_reg<int, K>(H, cap_rel);
                         if (better_cell(hv, r, n, best_v, best_i, best_j)) { best_v = hv; best_i = r; best_j = n; }
                     }
-                    if (t == 31 && !last) {
-                        out_col[r - 1] = make_int2(out_tg, out_h);
-                        if ((r & 31) == 0 || r == m) {
-                            __threadfence_block();
-                            prog[w] = k_local * m + r;
-                        }
-                    }
+                    if (do_out) out_ptr[it] = make_int2(out_tg, out_h);
                 }
-                // right-most column to the next lane; lane 0 takes the stage's left border of row it + 1
-                int ntg = __shfl_up_sync(0xffffffffu, out_tg, 1);
-                int nh = __shfl_up_sync(0xffffffffu, out_h, 1);
+                // right-most column and the row's selector move to the next lane
                 hdiag = h_l;
-                if (first) {
-                    if (GLOBAL_EDGES) edge -= beta;
-                    if (t == 0) { nh = edge; ntg = edge - gamma; }
+                tg_l = __shfl_up_sync(0xffffffffu, out_tg, 1);
+                h_l = __shfl_up_sync(0xffffffffu, out_h, 1);
+                sel = __shfl_up_sync(0xffffffffu, sel, 1);
+                if (CHECK && r == 0) hdiag = h_top;
+            };
+
+            const int it_end = m + 31;
+            const int nchunks = (it_end + 31) / 32;
+#pragma unroll 1
+            for (int c = 0; c < nchunks; ++c) {
+                s_in[w][(c & 1) * 32 + t] = make_int4(pre.x, pre.y, (int)pre_sel, 0);
+                __syncwarp();
+                fetch_chunk(c + 1);
+                const int it0 = 32 * c + 1, it1 = min(it0 + 31, it_end);
+                if (c >= 1 && it1 <= m) {   // every lane's row is inside the matrix
+#pragma unroll 1
+                    for (int it = it0; it <= it1; ++it) iteration(it, std::false_type{});
                 } else {
-                    const int2 b = s_in[w][it & 63];  // row it + 1 sits in slot (it + 1 - 1) & 63
-                    if (t == 0) { ntg = b.x; nh = b.y; }
+#pragma unroll 1
+                    for (int it = it0; it <= it1; ++it) iteration(it, std::true_type{});
                 }
-                tg_l = ntg; h_l = nh;
-                if (r == 0) hdiag = h_top;
-                q_cur = q_nxt; q_nxt = q_nn;
+                if (do_out) {  // publish the border rows lane 31 has completed
+                    __threadfence_block();
+                    prog[w] = k_local * m + min(max(it1 - 31, 0), m);
+                }
             }
             // rows are complete: every lane's registers hold row m of its strip
             if (SEMI) {

@@ -22,7 +22,8 @@ enum Op { OP_IADD3, OP_IMAD, OP_LOP3, OP_PRMT, OP_IMNMX, OP_VIMNMX3, OP_VIADDMNM
           MIX_VIMNMX16_HFMA2, MIX_HMNMX2_HFMA2, MIX_VIADDMNMX16_IMAD, MIX_HMNMX2_VIMNMX16, MIX_VIMNMX16_VIADD16,
           MIX_PRMT_VIMNMX16, MIX_PRMT_HFMA2, MIX_IMNMX_IMAD, MIX_HMNMX2_HADD2_SHFL, MIX_VIMNMX16_IMAD,
           MIX_HSET2_HFMA2, MIX_HSET2_HMNMX2, MIX_CELL_DPX, MIX_CELL_H2, MIX_VIADD16_IMAD, MIX_LDS_VIMNMX16,
-          MIX_SHFL_VIMNMX16, MIX_IADD3_IMAD, MIX_LOP3_IMAD, OP_COUNT };
+          MIX_SHFL_VIMNMX16, MIX_IADD3_IMAD, MIX_LOP3_IMAD,
+          OP_IDP4A, OP_VIADD32, MIX_IDP_VIMNMX3, MIX_CELL_I32_IDP, MIX_CELL_I32_PRMT, MIX_CELL_S16_PRMT, OP_COUNT };
 
 static const char* names[] = {"IADD3","IMAD","LOP3","PRMT","IMNMX(VIMNMX.S32)","VIMNMX3","VIADDMNMX","VIADDMNMX.RELU",
   "VIMNMX.S16x2","VIMNMX3.S16x2","VIADDMNMX.S16x2","VIADDMNMX.S16x2.RELU","VIADD.16x2",
@@ -31,10 +32,11 @@ static const char* names[] = {"IADD3","IMAD","LOP3","PRMT","IMNMX(VIMNMX.S32)","
   "mix VIMNMX16+HFMA2","mix HMNMX2+HFMA2","mix VIADDMNMX16+IMAD","mix HMNMX2+VIMNMX16","mix VIMNMX16+VIADD16",
   "mix PRMT+VIMNMX16","mix PRMT+HFMA2","mix IMNMX+IMAD","mix 4xHMNMX2+4xHADD2+1SHFL(per 9)","mix VIMNMX16+IMAD",
   "mix HSET2+HFMA2","mix HSET2+HMNMX2","mix DPX cell(PRMT,2VIMNMX,VIADDMNMX,VIADD,VIADDMNMX.RELU)","mix H2 cell(HSET2,HFMA2.RELU,4HMNMX2,3HADD2)",
-  "mix VIADD16+IMAD","mix LDS+3xVIMNMX16","mix SHFL+7xVIMNMX16","mix IADD3+IMAD","mix LOP3+IMAD"};
+  "mix VIADD16+IMAD","mix LDS+3xVIMNMX16","mix SHFL+7xVIMNMX16","mix IADD3+IMAD","mix LOP3+IMAD",
+  "IDP.4A.S8.S8","VIADD(s32 +imm)","mix IDP4A+VIMNMX3","mix i32 cell(IDP4A,2VIMNMX3,2IMAD)","mix i32 cell(PRMT,IMAD,2VIMNMX3,2IMAD)","mix s16x2 cell(2PRMT,LOP3,VIADD16,2VIMNMX3.16,2VIADD16)"};
 // instructions counted per chain step
 static const int per_step[] = {1,1,1,1,1,1,1,1, 1,1,1,1,1, 1,1,1,1,1,1,1,1,1,1, 1,1,1,2,
-  2,2,2,2,2, 2,2,2,9,2, 2,2,6,9, 2,4,8,2,2};
+  2,2,2,2,2, 2,2,2,9,2, 2,2,6,9, 2,4,8,2,2, 1,1,2,5,6,8};
 
 __device__ __forceinline__ uint32_t h2max(uint32_t a, uint32_t b){ uint32_t d; asm volatile("max.f16x2 %0,%1,%2;" : "=r"(d) : "r"(a),"r"(b)); return d; }
 __device__ __forceinline__ uint32_t h2add(uint32_t a, uint32_t b){ uint32_t d; asm volatile("add.f16x2 %0,%1,%2;" : "=r"(d) : "r"(a),"r"(b)); return d; }
@@ -126,6 +128,35 @@ __global__ void __launch_bounds__(1024, 1) bench(uint32_t* out, const uint32_t* 
           v = __vmaxs2(v,y); BAR(v); v = __vmaxs2(v,z); BAR(v); v = __vmaxs2(v,w); BAR(v); }
         else if (OP == MIX_IADD3_IMAD) { asm volatile("add.s32 %0,%0,%1;" : "+r"(v) : "r"(y)); asm volatile("mad.lo.s32 %0,%0,%1,%2;" : "+r"(v) : "r"(y),"r"(z)); }
         else if (OP == MIX_LOP3_IMAD) { asm volatile("lop3.b32 %0,%0,%1,%2,0x96;" : "+r"(v) : "r"(y),"r"(z)); asm volatile("mad.lo.s32 %0,%0,%1,%2;" : "+r"(v) : "r"(y),"r"(z)); }
+        else if (OP == OP_IDP4A) { v = __dp4a((int)y, (int)z, (int)v); BAR(v); }
+        else if (OP == OP_VIADD32) { v = v + 12345u; BAR(v); }
+        else if (OP == MIX_IDP_VIMNMX3) { v = __dp4a((int)y, (int)z, (int)v); BAR(v); v = __vimax3_s32((int)v,(int)y,(int)w); BAR(v); }
+        else if (OP == MIX_CELL_I32_IDP) {
+          int d = __dp4a((int)y, (int)z, (int)v); BAR(d);
+          int h = __vimax3_s32((int)w, (int)v, d); BAR(h);
+          int tn = __vimax3_s32((int)z, (int)v, d); BAR(tn);
+          int la; asm volatile("mad.lo.s32 %0,%1,%2,%3;" : "=r"(la) : "r"(tn),"r"(w),"r"(y));
+          int lg; asm volatile("mad.lo.s32 %0,%1,%2,%3;" : "=r"(lg) : "r"(h),"r"(w),"r"(z));
+          v = la ^ lg; // counted as free-ish (LOP3 extra, not in per_step)
+        }
+        else if (OP == MIX_CELL_I32_PRMT) {
+          uint32_t s; asm volatile("prmt.b32 %0,%1,%2,%3;" : "=r"(s) : "r"(y),"r"(z),"r"(v));
+          int d; asm volatile("mad.lo.s32 %0,%1,%2,%3;" : "=r"(d) : "r"(s),"r"(w),"r"(v));
+          int h = __vimax3_s32((int)w, (int)v, d); BAR(h);
+          int tn = __vimax3_s32((int)z, (int)v, d); BAR(tn);
+          int la; asm volatile("mad.lo.s32 %0,%1,%2,%3;" : "=r"(la) : "r"(tn),"r"(w),"r"(y));
+          asm volatile("mad.lo.s32 %0,%1,%2,%3;" : "=r"(v) : "r"(h),"r"(w),"r"(la));
+        }
+        else if (OP == MIX_CELL_S16_PRMT) {
+          uint32_t s0; asm volatile("prmt.b32 %0,%1,%2,%3;" : "=r"(s0) : "r"(y),"r"(z),"r"(v));
+          uint32_t s1; asm volatile("prmt.b32 %0,%1,%2,%3;" : "=r"(s1) : "r"(z),"r"(w),"r"(v));
+          uint32_t sg; asm volatile("lop3.b32 %0,%1,%2,%3,0xe8;" : "=r"(sg) : "r"(s0),"r"(s1),"r"(w));
+          uint32_t d = __vadd2(sg, v); BAR(d);
+          uint32_t h = __vimax3_s16x2(w, v, d); BAR(h);
+          uint32_t tn = __vimax3_s16x2(z, v, d); BAR(tn);
+          uint32_t la = __vadd2(tn, y); BAR(la);
+          v = __vadd2(h, la); BAR(v);
+        }
         x[j] = v;
       }
     }
