@@ -15,12 +15,12 @@
 //
 // Cell update (reference: _kernels.py:259-276 merged affine, :113-126 linear; same algebra as score_kernels.cuh, with
 // TA = T - alpha and TG = T - gamma kept per column so that both maxima are single 3-input DPX instructions):
-//     sigma = PRMT(profile[c], query selector)                 ALU   profile word = sigma for query symbols 0..3
-//     d     = H_diag + sigma                                   IMAD  (FMA pipe)
-//     h     = max3(TA_up, TA_left, d [,0])                     VIMNMX3[.RELU]
-//     tn    = max3(TG_up, TG_left, d [,0])                     VIMNMX3[.RELU]
-//     TA    = tn - alpha ; TG = tn - gamma                     2 x IMAD/IADD
-// = 3 ALU + 3 FMA-pipe instructions per cell (the reference counts 7, local 8: _kernels.py:277-279).
+//     d     = H_diag + sigma = dp4a(profile[c], onehot(q), H_diag)   IDP.4A   profile bytes = sigma(a, s_c), a = 0..3
+//     h     = max3(TA_up, TA_left, d [,0])                           VIMNMX3[.RELU]
+//     tn    = max3(TG_up, TG_left, d [,0])                           VIMNMX3[.RELU]
+//     TA    = tn - alpha ; TG = tn - gamma                           2 x IMAD
+// = 5 instructions per cell (the reference counts 7, local 8: _kernels.py:277-279).  A flagged query symbol (one-hot
+// word 0) takes a lane-divergent copy of the row with sigma = mismatch.
 #pragma once
 #include "score_kernels.cuh"
 
@@ -119,11 +119,11 @@ __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long_kernel(const Lo
             const int h_top = edge_h(GLOBAL_EDGES, col0, alpha, beta);  // H(0, col0): diagonal of this strip's row 1
             int hdiag = h_top;
             int tg_l = kNeg32, h_l = kNeg32;        // left border {T - gamma, H} of the row this lane computes next
-            unsigned sel = 0x8880u;                 // PRMT selector of that row's query symbol
+            unsigned sel = 0u;                      // that row's query symbol, one-hot in bytes (0 = flagged)
             int edge = edge_h(GLOBAL_EDGES, 1, alpha, beta);   // stage 0: H(r, 0) of lane 0's current row
             // incoming border column (stage st - 1) and its producer
             const int2* in_col = bnd_block + (int64_t)((st + NW) % (NW + 1)) * prm.bnd_rows;   // (st - 1) mod (NW + 1)
-            int2* out_ptr = bnd_block + (int64_t)(st % (NW + 1)) * prm.bnd_rows - 32;  // lane 31: row it - 31 -> slot it - 32
+            int2* out_ptr = bnd_block + (int64_t)(st % (NW + 1)) * prm.bnd_rows - 31;  // lane 31 at iteration it: row it - 31 -> slot it - 32 (it starts at 1)
             const int pw_id = (w + NW - 1) % NW;
             const int p_base = (w == 0 ? k_local - 1 : k_local) * m;  // producer's published rows before its stage
             const bool do_out = t == 31 && !last;
@@ -133,12 +133,12 @@ __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long_kernel(const Lo
             // Rows 32c+1 .. 32c+32 of lane 0's inputs (incoming border + query selector) are fetched one chunk ahead
             // with coalesced loads, parked in shared memory, and read back one row per iteration.
             int2 pre = make_int2(kNeg32, kNeg32);
-            unsigned pre_sel = 0x8880u;
+            unsigned pre_sel = 0u;
             auto fetch_chunk = [&](int chunk) {
                 const int row0 = 32 * chunk;
                 if (row0 >= m) return;
                 const int q = qp[min(row0 + t, m - 1)];
-                pre_sel = (unsigned)min(q, 4) * 0x1111u + 0x8880u;
+                pre_sel = q < 4 ? 1u << (8 * q) : 0u;
                 if (!first) {
                     const int need = p_base + min(m, row0 + 32);
                     while (prog[pw_id] < need) __nanosleep(40);
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long_kernel(const Lo
             // one row of the strip; CHECK = the row may lie outside 1..m (ramp-up / ramp-down chunks)
             auto iteration = [&](int it, auto check_tag) {
                 constexpr bool CHECK = decltype(check_tag)::value;
-                const int4 in = s_in[w][(it - 1) & 63];   // lane 0's inputs for row it
+                const int4 in = s_in[w][(it - 1) & 63];   // lane 0's inputs for row it (broadcast load)
                 if (t == 0) {
                     sel = (unsigned)in.z;
                     if (first) { h_l = edge; tg_l = edge - gamma; }
@@ -165,25 +165,30 @@ __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long_kernel(const Lo
                     int la = MERGED ? tg_l + (gamma - alpha) : h_l - alpha;   // T_left - alpha
                     int lg = tg_l;
                     int rm = 0;
+                    auto cells = [&](auto flagged_tag) {
+                        constexpr bool FLAGGED = decltype(flagged_tag)::value;  // flagged query symbol: sigma = mismatch
 #pragma unroll
-                    for (int c = 0; c < K; ++c) {
-                        const int d = fma_add(prmt(prof[c], mism4, sel), one, hd);
-                        hd = H[c];
-                        const int h = LOCAL ? __vimax3_s32_relu(TA[c], la, d) : __vimax3_s32(TA[c], la, d);
-                        if (MERGED) {
-                            const int tn = LOCAL ? __vimax3_s32_relu(TG[c], lg, d) : __vimax3_s32(TG[c], lg, d);
-                            la = fma_add(tn, one, nalpha);
-                            lg = fma_add(tn, one, ngamma);
-                            TG[c] = lg;
-                        } else {
-                            la = fma_add(h, one, nalpha);
+                        for (int c = 0; c < K; ++c) {
+                            const int d = FLAGGED ? fma_add(hd, one, mism) : __dp4a((int)prof[c], (int)sel, hd);
+                            hd = H[c];
+                            const int h = LOCAL ? __vimax3_s32_relu(TA[c], la, d) : __vimax3_s32(TA[c], la, d);
+                            if (MERGED) {
+                                const int tn = LOCAL ? __vimax3_s32_relu(TG[c], lg, d) : __vimax3_s32(TG[c], lg, d);
+                                la = fma_add(tn, one, nalpha);
+                                lg = fma_add(tn, one, ngamma);
+                                TG[c] = lg;
+                            } else {
+                                la = fma_add(h, one, nalpha);
+                            }
+                            TA[c] = la;
+                            H[c] = h;
+                            if (LOCAL) {
+                                if (c & 1) rm = __vimax3_s32(rm, H[c - 1], h);
+                            }
                         }
-                        TA[c] = la;
-                        H[c] = h;
-                        if (LOCAL) {
-                            if (c & 1) rm = __vimax3_s32(rm, H[c - 1], h);
-                        }
-                    }
+                    };
+                    if (sel != 0u) cells(std::false_type{});
+                    else cells(std::true_type{});
                     out_tg = lg; out_h = H[K - 1];
                     if (LOCAL) {
                         if (rm >= best_v && rm > 0 && (rm > best_v || r < best_i)) {  // rare: a new record row
@@ -197,7 +202,7 @@ __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long_kernel(const Lo
                         const int hv = select_reg<int, K>(H, cap_rel);
                         if (better_cell(hv, r, n, best_v, best_i, best_j)) { best_v = hv; best_i = r; best_j = n; }
                     }
-                    if (do_out) out_ptr[it] = make_int2(out_tg, out_h);
+                    if (do_out) *out_ptr = make_int2(out_tg, out_h);
                 }
                 // right-most column and the row's selector move to the next lane
                 hdiag = h_l;
@@ -205,6 +210,7 @@ __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long_kernel(const Lo
                 h_l = __shfl_up_sync(0xffffffffu, out_h, 1);
                 sel = __shfl_up_sync(0xffffffffu, sel, 1);
                 if (CHECK && r == 0) hdiag = h_top;
+                ++out_ptr;
             };
 
             const int it_end = m + 31;

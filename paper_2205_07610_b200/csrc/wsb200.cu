@@ -513,14 +513,14 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
         for (int64_t p : long_pairs) {
             const int stages = (b->n[p] + kLongW - 1) / kLongW;
             const double t1 = (double)stages * (b->m[p] + 31);
-            int lo = (int)std::min<double>(kLongMaxWarps, std::ceil(t1 / (0.25 * makespan)));
-            lo = std::max(1, std::min(lo, stages));
-            const int hi = std::min({kLongMaxWarps, stages, 2 * lo + 1});
+            // warps per pair come from {1, 2, 4, 8, 16}: blocks then spread evenly over the four schedulers of an SM
+            int lo = 1;
+            while (lo < kLongMaxWarps && lo < stages && t1 / lo > 0.25 * makespan) lo *= 2;
             int best_nw = lo;
             double best_cost = 1e300;
-            for (int nw = lo; nw <= hi; ++nw) {
+            for (int nw = lo; nw <= std::min(kLongMaxWarps, 2 * lo); nw *= 2) {
                 const double rounds = (double)((stages + nw - 1) / nw);
-                const double cost = nw * (rounds * (b->m[p] + 31) + (nw - 1) * 80.0);
+                const double cost = nw * (rounds * (b->m[p] + 31) + (nw - 1) * 100.0);
                 if (cost < best_cost * 0.999) { best_cost = cost; best_nw = nw; }
             }
             by_nw[best_nw].push_back(p);
