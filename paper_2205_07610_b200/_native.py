@@ -9,7 +9,7 @@ import numpy as np
 
 from .core import DeviceError, LengthOverflow, PackedRangeOverflow, WaveseqError
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libwsb200.so")
+_LIB_PATH = os.environ.get("WSB_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libwsb200.so")  # WSB_LIB: tuning aid
 _lib = None
 
 ALIGN_TYPE_ID = {"global": 0, "local": 1, "semiglobal": 2}

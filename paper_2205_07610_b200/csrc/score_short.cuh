@@ -254,9 +254,11 @@ __global__ void __launch_bounds__(kThreads) f16_local_short_kernel(const ScorePa
     (void)c_ndelta;
     // lane 0 sees the matrix' zero left border instead of a neighbour: x * keep + edge on the FMA pipe
     const __half2 keep = AR::splat(t == 0 ? 0 : 1);
+    (void)keep;
     const __half2 edge_ta = t == 0 ? c_nalpha : c_zero;  // (T - alpha) of the border, T = 0
     const __half2 edge_tg = t == 0 ? c_ngamma : c_zero;
     const __half2 edge_hm = t == 0 ? c_mism : c_zero;
+    (void)edge_ta; (void)edge_tg; (void)edge_hm;
     const int col0 = t * K;
 
     const int64_t rounds = (prm.n_units + n_groups - 1) / n_groups;
@@ -374,30 +376,44 @@ __global__ void __launch_bounds__(kThreads) f16_local_short_kernel(const ScorePa
         };
         unsigned qa_next, qb_next;  // query symbols are fetched one trip ahead of their use
         asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(qa_next), "=r"(qb_next) : "r"(qaddr) : "memory");
+#ifdef WSB_UNROLL2
+#pragma unroll 2
+#else
 #pragma unroll 1
+#endif
         while (qaddr != qend) {
             const unsigned qa = qa_next, qb = qb_next;
             asm volatile("ld.shared.v2.b32 {%0, %1}, [%2+8];" : "=r"(qa_next), "=r"(qb_next) : "r"(qaddr) : "memory");
             __half2 laA = ta_lA, lgA = tg_lA, laB = ta_lB, lgB = tg_lB, rmA, rmB;
             row(u2h(qa), HM, HM2, hm_dA, laA, lgA, rmA);
+            // row A's right-most column leaves for the next lane as soon as it exists: the next trip's row A needs it
+            // first, and the shuffle latency then hides behind row B.
+#ifdef WSB_EARLY_SHFL
+            __half2 s0 = __shfl_up_sync(0xffffffffu, laA, 1, P);
+            __half2 s1 = __shfl_up_sync(0xffffffffu, HM2[K - 1], 1, P);
+            __half2 s4 = c_zero;
+            if (GAP == GAP_MERGED) s4 = __shfl_up_sync(0xffffffffu, lgA, 1, P);
+#endif
             record_rows<K>(HM2, rmA, bestvec, snap_addr, qaddr);
             bestvec = __hmax2(bestvec, rmA);
             row(u2h(qb), HM2, HM, hm_lA, laB, lgB, rmB);
-            // right-most columns of both rows to the next lane (used by its next trip).  The shuffles go out before
-            // row B's snapshot stores so that they do not queue behind them in the shared-memory pipe.
             hm_dA = hm_lB;
-            const __half2 s0 = __shfl_up_sync(0xffffffffu, laA, 1, P);
-            const __half2 s1 = __shfl_up_sync(0xffffffffu, HM2[K - 1], 1, P);
-            const __half2 s2 = __shfl_up_sync(0xffffffffu, laB, 1, P);
-            const __half2 s3 = __shfl_up_sync(0xffffffffu, HM[K - 1], 1, P);
-            __half2 s4 = c_zero, s5 = c_zero;
-            if (GAP == GAP_MERGED) {
-                s4 = __shfl_up_sync(0xffffffffu, lgA, 1, P);
-                s5 = __shfl_up_sync(0xffffffffu, lgB, 1, P);
-            }
+#ifndef WSB_EARLY_SHFL
+            __half2 s0 = __shfl_up_sync(0xffffffffu, laA, 1, P);
+            __half2 s1 = __shfl_up_sync(0xffffffffu, HM2[K - 1], 1, P);
+            __half2 s4 = c_zero;
+            if (GAP == GAP_MERGED) s4 = __shfl_up_sync(0xffffffffu, lgA, 1, P);
+#endif
+            __half2 s2 = __shfl_up_sync(0xffffffffu, laB, 1, P);
+            __half2 s3 = __shfl_up_sync(0xffffffffu, HM[K - 1], 1, P);
+            __half2 s5 = c_zero;
+            if (GAP == GAP_MERGED) s5 = __shfl_up_sync(0xffffffffu, lgB, 1, P);
             record_rows<K>(HM, rmB, bestvec, snap_addr, qaddr + 4);
             bestvec = __hmax2(bestvec, rmB);
             qaddr += 8;
+#ifndef WSB_BORDER_SEL
+            // lane 0 sees the matrix' zero left border instead of a neighbour: x * keep + edge.  (Integer selects and
+            // earlier shuffles were measured slower: ptxas then rotates the strip registers with ~40 moves per trip.)
             ta_lA = __hfma2(s0, keep, edge_ta);
             hm_lA = __hfma2(s1, keep, edge_hm);
             ta_lB = __hfma2(s2, keep, edge_ta);
@@ -406,6 +422,16 @@ __global__ void __launch_bounds__(kThreads) f16_local_short_kernel(const ScorePa
                 tg_lA = __hfma2(s4, keep, edge_tg);
                 tg_lB = __hfma2(s5, keep, edge_tg);
             }
+#else
+            ta_lA = t == 0 ? c_nalpha : s0;
+            hm_lA = t == 0 ? c_mism : s1;
+            ta_lB = t == 0 ? c_nalpha : s2;
+            hm_lB = t == 0 ? c_mism : s3;
+            if (GAP == GAP_MERGED) {
+                tg_lA = t == 0 ? c_ngamma : s4;
+                tg_lB = t == 0 ? c_ngamma : s5;
+            }
+#endif
         }
 
         // reduce over the group: max value, then smallest row, then smallest strip; the winner resolves its column
