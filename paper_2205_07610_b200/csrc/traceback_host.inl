@@ -42,6 +42,11 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
     CUDA_TRY(ctx, cudaSetDevice(ctx->device));
     const bool affine = sch->gap_model == WSB_GAP_AFFINE;
     const int beta_eff = affine ? sch->gap_extend : sch->gap_open;
+    // the fill kernel looks sigma + alpha up in a signed-byte profile
+    if (std::abs(sch->match + sch->gap_open) > 127 || std::abs(sch->mismatch + sch->gap_open) > 127) {
+        b->ctx->last_error = "traceback needs |match + gap_open| and |mismatch + gap_open| <= 127";
+        return WSB_E_SCHEME;
+    }
     const int64_t np = b->n_pairs;
     TracebackState& tb = b->tb;
     tb.valid = false;
@@ -49,7 +54,9 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
     // 1. end cells with the score kernels (identical tie-break); per-pair length faults surface here
     float score_ms = 0.f;
     int32_t score_launches = 0;
-    rc = wsb_batch_score(b, sch, atype, WSB_VARIANT_AUTO, kernel_ms ? &score_ms : nullptr, &score_launches);
+    // (global / semiglobal: the fill kernel finds them itself, only the plan and the empty-side pairs are needed)
+    rc = batch_score_impl(b, sch, atype, WSB_VARIANT_AUTO, kernel_ms ? &score_ms : nullptr, &score_launches,
+                          /*plan_only=*/atype != AT_LOCAL);
     if (rc) return rc;
     const Plan* score_plan = b->last_plan;
 
@@ -161,6 +168,7 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
         prm.match = sch->match; prm.mismatch = sch->mismatch; prm.alpha = sch->gap_open; prm.beta = beta_eff;
         prm.bnd = bnd_rows ? (int2*)b->d_bnd : nullptr; prm.bnd_rows = bnd_rows;
         prm.end_i = b->d_i; prm.end_j = b->d_j; prm.start_i = tb.d_qs; prm.start_j = tb.d_ss;
+        prm.w_score = b->d_score; prm.w_i = b->d_i; prm.w_j = b->d_j;
         prm.n_runs = d_cnt; prm.run_off = d_chunk_off; prm.runs = nullptr;
         prm.tb_p = P; prm.tb_k = K;
 

@@ -2,13 +2,15 @@
 //
 // Fill: the same lane-group wavefront as the score kernels (lane t owns K columns, row r = it - t), int32, exact
 // three-state Gotoh (H, E, F kept apart because the walk must tell "came from E" from "came from F" and "gap extended"
-// from "gap opened").  Every cell emits one 4-bit code:
-//     bits 1:0  origin of H   0 = stop (local, H == 0)   1 = diagonal (M)   2 = E, vertical (I)   3 = F, horizontal (D)
-//     bit  2    E(i,j) == E(i-1,j) - beta   (the vertical gap arriving here is an extension)
-//     bit  3    F(i,j) == F(i,j-1) - beta
+// from "gap opened").  Every cell emits four bits, stored as bit planes of eight cells per 32-bit word:
+//     byte 0  diagonal >= E            byte 1  max(diagonal, E) >= F      (origin of H: diagonal, E = vertical/I, F = horizontal/D)
+//     byte 2  E(i,j) == E(i-1,j) - beta (the vertical gap arriving here is an extension)
+//     byte 3  F(i,j) == F(i,j-1) - beta
+// (local: H == 0 is stored as byte-1 bit clear + byte-0 bit set, a pattern the other modes read as plain "F").
 // Priorities are the reference walk's: diagonal, then E, then F; extension before open (refdp.py:162-165, 196-220).
-// The DPX max-with-predicate instructions (__vibmax_s32 -> VIMNMX + predicate) give value and "which side won" in one
-// issue slot.  Codes leave the SM in wavefront order -- the lane group writes P*K/2 contiguous bytes per iteration --
+// Per cell: one IDP.4A (H_diag + sigma from a byte profile, as in score_long.cuh), four DPX max-with-predicate
+// instructions (__vibmax_s32 -> VIMNMX + predicate: value and "which side won" in one issue slot), four predicated
+// adds that set the plane bits, three adds (E - beta, F - beta, H - alpha).  Codes leave the SM in wavefront order -- the lane group writes P*K/2 contiguous bytes per iteration --
 // so the only HBM traffic of the fill is 0.5 byte per cell of coalesced 8/16-byte stores.
 //
 // Walk: one thread per pair starts at the end cell the score kernels found (same tie-break) and follows the codes as
@@ -18,6 +20,8 @@
 #include "score_kernels.cuh"
 
 #include <cuda_runtime.h>
+
+#include <type_traits>
 
 namespace wsb {
 
@@ -33,7 +37,8 @@ struct TbParams {
     int2* bnd;                 // stage border scratch: per lane group bnd_rows x {H, F - beta}
     int64_t bnd_rows;
     // walk
-    const int32_t* end_i; const int32_t* end_j;   // end cells from the score pass
+    const int32_t* end_i; const int32_t* end_j;   // end cells (score pass, or this fill for global / semiglobal)
+    int32_t* w_score; int32_t* w_i; int32_t* w_j; // global / semiglobal: the fill writes score and end cell itself
     int32_t* start_i; int32_t* start_j;           // out: alignment start (0-based span starts)
     int32_t* n_runs;                              // per pair of the launch
     const int64_t* run_off;                       // exclusive prefix of n_runs, relative to the launch
@@ -46,6 +51,17 @@ __host__ __device__ inline int64_t tb_code_words(int m, int n, int P, int K) {
     const int W = P * K;
     const int stages = (n + W - 1) / W;
     return (int64_t)stages * (m + P - 1) * P * (K / 8);
+}
+
+// max(a, b) with "a wins ties", and the plane bit added to w when a wins: compare, select, predicated add
+__device__ __forceinline__ int max_mark(int a, int b, uint32_t& w, uint32_t bit) {
+    int r;
+    asm("{\n\t.reg .pred p;\n\t"
+        "setp.ge.s32 p, %2, %3;\n\t"
+        "selp.s32 %0, %2, %3, p;\n\t"
+        "@p add.u32 %1, %1, %4;\n\t"
+        "}" : "=r"(r), "+r"(w) : "r"(a), "r"(b), "r"(bit));
+    return r;
 }
 
 template <int P, int K, int ATYPE, bool AFFINE>
@@ -63,7 +79,10 @@ __global__ void __launch_bounds__(kThreads) tb_fill_kernel(const TbParams prm) {
     const int64_t group_global = (int64_t)blockIdx.x * GPB + gib;
     const int64_t n_groups = (int64_t)gridDim.x * GPB;
     int2* bnd = prm.bnd ? prm.bnd + group_global * prm.bnd_rows : nullptr;
-    const int alpha = prm.alpha, beta = prm.beta, match = prm.match, mism = prm.mismatch;
+    const int alpha = prm.alpha, beta = prm.beta, mism = prm.mismatch;
+    // profile bytes hold sigma + alpha, so that the diagonal candidate comes straight from the stored H - alpha
+    const unsigned miss4 = (unsigned)((mism + alpha) & 0xff) * 0x01010101u;
+    const unsigned hit = (unsigned)((prm.match + alpha) & 0xff);
 
     const int64_t rounds = (prm.n_pairs + n_groups - 1) / n_groups;
     for (int64_t rd = 0; rd < rounds; ++rd) {
@@ -88,93 +107,165 @@ __global__ void __launch_bounds__(kThreads) tb_fill_kernel(const TbParams prm) {
         const int nstages_w = (nn_w + W - 1) / W;
         const int nstages = (n + W - 1) / W;
         const int iters = m + P - 1;  // rows of this pair's code block per stage
+        // global / semiglobal: score and end cell come out of this fill (same rule as the score kernels: larger value,
+        // then smaller row, then smaller column); local alignments take them from the packed score pass
+        int best_v = GLOBAL_EDGES ? kNeg32 : 0, best_i = 0, best_j = ATYPE == AT_SEMI ? n : 0;
 
         for (int st = 0; st < nstages_w; ++st) {
             const int col0 = st * W + t * K;
-            int sc[K], H[K], EP[AFFINE ? K : 1];
+            // per column: profile word (sigma + alpha for query symbols 0..3), AL = H - alpha, EP = E - beta
+            unsigned prof[K];
+            int AL[K], EP[AFFINE ? K : 1];
 #pragma unroll
             for (int c = 0; c < K; ++c) {
-                int x = kPadSubject;
-                if (col0 + c < n) { x = sp[col0 + c]; x = x < 4 ? x : kFlagSubject; }
-                sc[c] = x;
-                H[c] = edge_h(GLOBAL_EDGES, col0 + c + 1, alpha, beta);
+                unsigned pw = miss4;
+                if (col0 + c < n) {
+                    const int x = sp[col0 + c];
+                    if (x < 4) pw = (miss4 & ~(0xffu << (8 * x))) | (hit << (8 * x));
+                }
+                prof[c] = pw;
+                AL[c] = edge_h(GLOBAL_EDGES, col0 + c + 1, alpha, beta) - alpha;
                 if (AFFINE) EP[c] = kNeg32;
             }
-            const int h0 = edge_h(GLOBAL_EDGES, col0, alpha, beta);
-            int hdiag = h0, hl = kNeg32, fpl = kNeg32;  // left border of the strip at the current row
+            const int al_top = edge_h(GLOBAL_EDGES, col0, alpha, beta) - alpha;   // H(0, col0) - alpha
+            int al_diag = al_top, all = kNeg32, fpl = kNeg32;  // left border {H - alpha, F - beta} of the current row
             int edge = edge_h(GLOBAL_EDGES, 1, alpha, beta);
             if (t == 0) {
-                if (st == 0) { hl = edge; fpl = kNeg32; }
-                else if (m >= 1 && st < nstages) { const int2 b = bnd[1]; hl = b.x; fpl = b.y; }
+                if (st == 0) { all = edge - alpha; fpl = kNeg32; }
+                else if (m >= 1 && st < nstages) { const int2 b = bnd[1]; all = b.x; fpl = b.y; }
             }
+            const int cap_rel = n - 1 - col0;   // register index of matrix column n, if inside this strip
+            const bool has_cap = !LOCAL && st + 1 == nstages && cap_rel >= 0 && cap_rel < K;
+            auto q_at = [&](int it) { return m > 0 ? (int)qp[min(max(it - t - 1, 0), m - 1)] : 4; };
+            int q_cur = q_at(1), q_nxt = q_at(2);
             const int it_end = mm_w + P - 1;
             for (int it = 1; it <= it_end; ++it) {
+                const int q_nn = q_at(it + 2);
                 const int r = it - t;
-                int out_h = hl, out_fp = fpl;
+                int out_al = all, out_fp = fpl;
                 if (r >= 1 && r <= m && st < nstages) {
-                    int q = qp[r - 1];
-                    q = q < 4 ? q : kFlagQuery;
-                    int hd = hdiag, left_h = hl, fl = fpl;
-                    int al = left_h - alpha;
+                    const unsigned qsel = q_cur < 4 ? 1u << (8 * q_cur) : 0u;   // one-hot bytes; 0 = flagged
+                    int ad = al_diag, fl = fpl, al = all;
                     uint32_t words[NW];
+                    auto cells = [&](auto flagged_tag) {
+                        constexpr bool FLAGGED = decltype(flagged_tag)::value;
 #pragma unroll
-                    for (int w = 0; w < NW; ++w) words[w] = 0u;
+                        for (int w8 = 0; w8 < NW; ++w8) {
+                            // bit planes of eight cells: byte 0 "diagonal >= E", byte 1 "max(diagonal, E) >= F",
+                            // byte 2 "E extends", byte 3 "F extends" (ties: diagonal, then E, then F; extension first)
+                            uint32_t wd = 0u, wm = 0u, we = 0u, wf = 0u;
 #pragma unroll
-                    for (int c = 0; c < K; ++c) {
-                        const int d = hd + ((q == sc[c]) ? match : mism);
-                        hd = H[c];
-                        const int au = H[c] - alpha;
-                        bool xe = false, xf = false, pd, pm;
-                        int e, f;
-                        if (AFFINE) {
-                            e = __vibmax_s32(EP[c], au, &xe);   // xe: extension wins ties (refdp.py:207)
-                            f = __vibmax_s32(fl, al, &xf);
-                        } else {
-                            e = au; f = al;
+                            for (int c8 = 0; c8 < 8; ++c8) {
+                                const int c = w8 * 8 + c8;
+                                const int d = FLAGGED ? ad + (mism + alpha) : __dp4a((int)prof[c], (int)qsel, ad);
+                                ad = AL[c];
+                                int h;
+                                if (LOCAL) {
+                                    bool xe = false, xf = false, pd, pm;
+                                    int e, f;
+                                    if (AFFINE) {
+                                        e = __vibmax_s32(EP[c], AL[c], &xe);
+                                        f = __vibmax_s32(fl, al, &xf);
+                                    } else {
+                                        e = AL[c]; f = al;
+                                    }
+                                    const int m1 = __vibmax_s32(d, e, &pd);
+                                    h = __vibmax_s32(m1, f, &pm);
+                                    // H == 0 stops the walk: encoded as "F wins" with the diagonal bit set
+                                    const bool stop = h <= 0;
+                                    h = max(h, 0);
+                                    pd = (pd && pm) || stop;
+                                    pm = pm && !stop;
+                                    if (pd) wd += 1u << c8;
+                                    if (pm) wm += 1u << (8 + c8);
+                                    if (AFFINE) {
+                                        if (xe) we += 1u << (16 + c8);
+                                        if (xf) wf += 1u << (24 + c8);
+                                        EP[c] = e - beta; fl = f - beta;
+                                    }
+                                } else {
+                                    int e, f;
+                                    if (AFFINE) {
+                                        e = max_mark(EP[c], AL[c], we, 1u << (16 + c8));
+                                        f = max_mark(fl, al, wf, 1u << (24 + c8));
+                                        EP[c] = e - beta; fl = f - beta;
+                                    } else {
+                                        e = AL[c]; f = al;
+                                    }
+                                    const int m1 = max_mark(d, e, wd, 1u << c8);
+                                    h = max_mark(m1, f, wm, 1u << (8 + c8));
+                                }
+                                al = h - alpha;
+                                AL[c] = al;
+                            }
+                            words[w8] = (wd | wm) | (we | wf);
                         }
-                        const int m1 = __vibmax_s32(d, e, &pd);  // pd: diagonal wins ties over E
-                        int h = __vibmax_s32(m1, f, &pm);        // pm: (diag | E) wins ties over F
-                        uint32_t cd = pm ? (pd ? 1u : 2u) : 3u;
-                        if (LOCAL && h <= 0) { h = 0; cd = 0u; }
-                        if (AFFINE) cd |= (xe ? 4u : 0u) | (xf ? 8u : 0u);
-                        words[c / 8] |= cd << (4 * (c % 8));
-                        H[c] = h;
-                        if (AFFINE) { EP[c] = e - beta; fl = f - beta; }
-                        al = h - alpha;
-                    }
+                    };
+                    if (qsel != 0u) cells(std::false_type{});
+                    else cells(std::true_type{});
                     // wavefront-major: iteration it of stage st, lane t
                     uint32_t* dst = code + (((int64_t)st * iters + (it - 1)) * P + t) * NW;
                     if (NW == 2) *reinterpret_cast<uint2*>(dst) = make_uint2(words[0], words[1]);
                     else if (NW == 4) *reinterpret_cast<uint4*>(dst) = make_uint4(words[0], words[1], words[2], words[NW - 1]);
                     else {
 #pragma unroll
-                        for (int w = 0; w < NW; ++w) dst[w] = words[w];
+                        for (int w8 = 0; w8 < NW; ++w8) dst[w8] = words[w8];
                     }
-                    out_h = H[K - 1];
+                    out_al = al;
                     out_fp = AFFINE ? fl : kNeg32;
-                    if (t == P - 1 && st + 1 < nstages) bnd[r] = make_int2(out_h, out_fp);
+                    if (ATYPE == AT_SEMI && has_cap && r < m) {   // last matrix column, rows above the last one
+                        const int hv = select_reg<int, K>(AL, cap_rel) + alpha;
+                        if (better_cell(hv, r, n, best_v, best_i, best_j)) { best_v = hv; best_i = r; best_j = n; }
+                    }
+                    if (t == P - 1 && st + 1 < nstages) bnd[r] = make_int2(out_al, out_fp);
                 }
-                int nh = __shfl_up_sync(0xffffffffu, out_h, 1, P);
+                int nal = __shfl_up_sync(0xffffffffu, out_al, 1, P);
                 int nfp = __shfl_up_sync(0xffffffffu, out_fp, 1, P);
-                hdiag = hl;
+                al_diag = all;
                 if (t == 0) {
                     if (st == 0) {
                         if (GLOBAL_EDGES) edge -= beta;
-                        nh = edge; nfp = kNeg32;
+                        nal = edge - alpha; nfp = kNeg32;
                     } else if (r + 1 <= m && st < nstages) {
                         const int2 b = bnd[r + 1];
-                        nh = b.x; nfp = b.y;
+                        nal = b.x; nfp = b.y;
                     }
                 }
-                hl = nh; fpl = nfp;
-                if (r == 0) hdiag = h0;
+                all = nal; fpl = nfp;
+                if (r == 0) al_diag = al_top;
+                q_cur = q_nxt; q_nxt = q_nn;
             }
+            // every lane's registers now hold row m of its strip
+            if (ATYPE == AT_SEMI && st < nstages) {
+#pragma unroll
+                for (int c = 0; c < K; ++c)
+                    if (col0 + c < n && better_cell(AL[c] + alpha, m, col0 + c + 1, best_v, best_i, best_j)) {
+                        best_v = AL[c] + alpha; best_i = m; best_j = col0 + c + 1;
+                    }
+            }
+            if (GLOBAL_EDGES && has_cap) { best_v = select_reg<int, K>(AL, cap_rel) + alpha; best_i = m; best_j = n; }
             __syncwarp();
+        }
+        if (!LOCAL) {
+            const unsigned gmask = group_mask<P>(tid & 31);
+#pragma unroll
+            for (int off = P / 2; off >= 1; off >>= 1) {
+                const int ov = __shfl_xor_sync(gmask, best_v, off, P);
+                const int oi = __shfl_xor_sync(gmask, best_i, off, P);
+                const int oj = __shfl_xor_sync(gmask, best_j, off, P);
+                if (better_cell(ov, oi, oj, best_v, best_i, best_j)) { best_v = ov; best_i = oi; best_j = oj; }
+            }
+            if (t == 0 && m > 0 && n > 0) {
+                const int64_t p = prm.first_pair + u;
+                prm.w_score[p] = best_v; prm.w_i[p] = best_i; prm.w_j[p] = best_j;
+            }
         }
     }
 }
 
-// 4-bit code of cell (i, j), 1 <= i <= m, 1 <= j <= n
+// code of cell (i, j), 1 <= i <= m, 1 <= j <= n, translated from the fill's bit planes to
+//   bits 1:0 origin of H (0 stop, 1 diagonal, 2 E, 3 F), bit 2 "E extends", bit 3 "F extends"
+template <bool LOCAL>
 __device__ __forceinline__ uint32_t tb_code_at(const uint32_t* code, int i, int j, int m, int P, int K) {
     const int W = P * K;
     const int st = (j - 1) / W;
@@ -182,7 +273,10 @@ __device__ __forceinline__ uint32_t tb_code_at(const uint32_t* code, int i, int 
     const int t = col / K, c = col - t * K;
     const int it = i + t;
     const int64_t word = (((int64_t)st * (m + P - 1) + (it - 1)) * P + t) * (K / 8) + c / 8;
-    return (code[word] >> (4 * (c % 8))) & 15u;
+    const uint32_t bits = code[word] >> (c % 8);
+    const bool pd = bits & 1u, pm = bits & 0x100u;
+    const uint32_t origin = pm ? (pd ? 1u : 2u) : ((LOCAL && pd) ? 0u : 3u);   // local: "F wins" + diagonal bit = stop
+    return origin | ((bits >> 14) & 4u) | ((bits >> 21) & 8u);
 }
 
 // PASS 1 counts the runs and records the start cell; PASS 2 writes the runs in forward order.
@@ -219,14 +313,14 @@ __global__ void tb_walk_kernel(const TbParams prm) {
                     if (i == 0) { emit(2, j); j = 0; break; }
                     if (j == 0) { emit(1, i); i = 0; break; }
                 } else if (i == 0 || j == 0) break;  // local: H == 0 on the edges; semiglobal: free edges
-                const uint32_t cd = tb_code_at(code, i, j, m, P, K);
+                const uint32_t cd = tb_code_at<ATYPE == AT_LOCAL>(code, i, j, m, P, K);
                 const uint32_t origin = cd & 3u;
                 if (origin == 0u) break;                        // local stop: H(i, j) == 0
                 if (origin == 1u) { emit(0, 1); --i; --j; continue; }
                 state = origin == 2u ? 1 : 2;
                 continue;
             }
-            const uint32_t cd = tb_code_at(code, i, j, m, P, K);
+            const uint32_t cd = tb_code_at<ATYPE == AT_LOCAL>(code, i, j, m, P, K);
             if (state == 1) { emit(1, 1); const bool ext = cd & 4u; --i; if (!ext) state = 0; }
             else { emit(2, 1); const bool ext = cd & 8u; --j; if (!ext) state = 0; }
         }

@@ -597,8 +597,10 @@ static int check_scheme(const wsb_scheme* s, int atype) {
     return WSB_OK;
 }
 
-extern "C" int wsb_batch_score(wsb_batch* b, const wsb_scheme* sch, int atype, int variant, float* kernel_ms,
-                               int32_t* n_launches) {
+// plan_only: build (or reuse) the plan and resolve empty-side pairs, but launch no score kernel (the traceback fill of
+// global / semiglobal alignments produces score and end cell itself)
+static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int variant, float* kernel_ms,
+                            int32_t* n_launches, bool plan_only) {
     if (!b) return WSB_E_ARG;
     int rc = check_scheme(sch, atype);
     if (rc) return rc;
@@ -664,7 +666,7 @@ extern "C" int wsb_batch_score(wsb_batch* b, const wsb_scheme* sch, int atype, i
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
     int launches = 0, n_aux = 0;
     bool aux_used[wsb_ctx::kAux] = {};
-    for (size_t k = 0; k < plan.groups.size(); ++k) {
+    for (size_t k = 0; k < plan.groups.size() && !plan_only; ++k) {
         const LaunchGroup& g = plan.groups[k];
         if (g.long_nw > 0) {  // long-read groups, largest warps-per-pair first, each on its own stream
             const int a = n_aux++ % wsb_ctx::kAux;
@@ -721,6 +723,11 @@ extern "C" int wsb_batch_score(wsb_batch* b, const wsb_scheme* sch, int atype, i
     }
     if (n_launches) *n_launches = launches;
     return WSB_OK;
+}
+
+extern "C" int wsb_batch_score(wsb_batch* b, const wsb_scheme* sch, int atype, int variant, float* kernel_ms,
+                               int32_t* n_launches) {
+    return batch_score_impl(b, sch, atype, variant, kernel_ms, n_launches, false);
 }
 
 extern "C" int wsb_batch_fetch_scores(wsb_batch* b, int32_t* out_score, int32_t* out_i, int32_t* out_j, int32_t* status) {
