@@ -28,13 +28,19 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
-    # name: (pairs, length, align_type, gap_model, scheme, result_mode, ops per cell of the reference's count)
-    "cfg1": dict(pairs=10_000, length=150, align_type="global", gap_model="linear", scheme=(2, -1, 1, 1), i_cell=5),
-    "cfg2": dict(pairs=4_000_000, length=150, align_type="local", gap_model="affine", scheme=(2, -1, 2, 1), i_cell=8),
+    # BASELINE.json configs.  i_cell = the reference's instrumented score ops per cell; width = cells per
+    # thread instruction of the dominant kernel (2 = packed half2, 1 = int32).
+    "cfg1": dict(pairs=10_000, length=150, align_type="global", gap_model="linear", scheme=(2, -1, 1, 1), i_cell=5, variant="auto"),
+    "cfg2": dict(pairs=4_000_000, length=150, align_type="local", gap_model="affine", scheme=(2, -1, 2, 1), i_cell=8, variant="f16x2"),
     "cfg2_i32": dict(pairs=1_000_000, length=150, align_type="local", gap_model="affine", scheme=(2, -1, 2, 1), i_cell=8,
                      variant="i32"),
-    "cfg3": dict(pairs=200_000, length=250, align_type="semiglobal", gap_model="affine", scheme=(2, -1, 2, 1), i_cell=8,
-                 traceback=True),
+    "cfg3": dict(pairs=1_000_000, length=250, align_type="semiglobal", gap_model="affine", scheme=(2, -1, 2, 1), i_cell=8,
+                 variant="auto", traceback=True, related=0.5),
+    "cfg4": dict(pairs=10_000, length=10_000, align_type="global", gap_model="affine", scheme=(2, -1, 2, 1), i_cell=7,
+                 variant="auto"),
+    # cfg5: 100 000 pairs in total (strong scaling: sharded over the ranks by cell count), truncated-Pareto lengths
+    "cfg5": dict(pairs=100_000, length=None, align_type="local", gap_model="affine", scheme=(2, -1, 2, 1), i_cell=8,
+                 variant="auto", pareto=True),
 }
 
 
@@ -52,7 +58,29 @@ def make_batch(cfg, seed):
     n, L = cfg["pairs"], cfg["length"]
     q = rng.integers(0, 4, (n, L), dtype=np.uint8)
     s = rng.integers(0, 4, (n, L), dtype=np.uint8)
+    if cfg.get("related"):  # cfg3: every second subject is a mutated copy of its query (3 % sub, 1 % ins, 1 % del)
+        k = np.arange(0, n, 2)
+        sub = rng.random((len(k), L)) < 0.03
+        s[k] = np.where(sub, (q[k] + rng.integers(1, 4, (len(k), L), dtype=np.uint8)) % 4, q[k])
+        shift = rng.random(len(k)) < 0.8   # one indel somewhere: shift the tail by one symbol either way
+        pos = rng.integers(20, L - 20, len(k))
+        for row, p_, left in zip(k[shift][:50_000], pos[shift][:50_000], rng.random(int(shift.sum()))[:50_000] < 0.5):
+            s[row, p_:] = np.roll(s[row, p_:], 1 if left else -1)
     return q, s
+
+
+def make_pareto(n, seed, cap=100_000):
+    """cfg5: L = min(cap, floor(100/(1-u))), n = clip(round(L*v), 100, cap), v ~ U[0.8, 1.25]."""
+    rng = np.random.default_rng(seed)
+    u = rng.random(n)
+    L = np.minimum(cap, np.floor(100.0 / (1.0 - u))).astype(np.int64)
+    M = np.clip(np.rint(L * rng.uniform(0.8, 1.25, n)), 100, cap).astype(np.int64)
+
+    def pool(lens):
+        off = np.zeros(n, np.int64)
+        off[1:] = np.cumsum(lens[:-1])
+        return rng.integers(0, 4, int(lens.sum()), dtype=np.uint8), off, lens.astype(np.int32)
+    return pool(L), pool(M)
 
 
 def pinned(arr):
@@ -143,6 +171,13 @@ def cpu_sample(cfg, seconds_target=12.0, seed=7):
     threads = oracle.max_threads()
     L = cfg["length"]
     sch = cfg["scheme"]
+    if cfg.get("pareto"):  # bounded sample of the length distribution: cap 6000 bp keeps a pair under ~0.1 s of one core
+        (qc, qo, ql), (sc, so, sl) = make_pareto(3000, seed, cap=6000)
+        idx = np.arange(3000, dtype=np.int32)
+        t0 = time.perf_counter()
+        oracle.score_batch(qc, qo, ql, sc, so, sl, idx, idx, cfg["align_type"], cfg["gap_model"] == "affine", *sch, threads=threads)
+        dt = time.perf_counter() - t0
+        return float((ql.astype(np.int64) * sl).sum()) / dt / 1e9, threads, 3000, dt
 
     def run(npairs):
         q, s = make_batch(dict(pairs=npairs, length=L), seed)
@@ -179,11 +214,12 @@ def run_reference(args, cfg, rank, world):
             rates.append(rate)
     value = float(np.mean(rates))
     threads, pairs, dt = info
-    sample = f"{pairs} pairs of {cfg['length']} bp per step ({dt:.2f} s), {cfg['align_type']}/{cfg['gap_model']}"
+    length = cfg["length"] if cfg["length"] else "pareto(cap 6000)"
+    sample = f"{pairs} pairs of {length} bp per step ({dt:.2f} s), {cfg['align_type']}/{cfg['gap_model']}"
     line = {"impl": "reference", "metric": "GCUPS", "value": value, "unit": "GCUPS", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "int32", "data": "synthetic",
-            "config": {"workload": args.workload, "pairs_per_step": pairs, "read_length": cfg["length"],
+            "config": {"workload": args.workload, "pairs_per_step": pairs, "read_length": length,
                        "align_type": cfg["align_type"], "gap_model": cfg["gap_model"], "scheme": list(cfg["scheme"])},
             "cpu_baseline": {"value": value, "unit": "GCUPS", "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -198,6 +234,7 @@ def main():
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--pairs", type=int, default=0, help="override pairs per GPU (debug)")
+    ap.add_argument("--cap", type=int, default=100_000, help="cfg5: length cap of the truncated Pareto distribution")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     cfg = dict(WORKLOADS[args.workload])
@@ -218,14 +255,30 @@ def main():
     device = local % ndev
     scheme = W.ScoringScheme(*cfg["scheme"], cfg["gap_model"])
     variant = cfg.get("variant", "f16x2")
-    q, s = make_batch(cfg, 220507610 + 2 + rank)
-    n, L = cfg["pairs"], cfg["length"]
-    (q_pin, q_keep), (s_pin, s_keep) = pinned(q), pinned(s)
-    off = np.arange(n, dtype=np.int64) * L
-    ln = np.full(n, L, np.int32)
-    idx = np.arange(n, dtype=np.int32)
+    strong = bool(cfg.get("pareto"))
+    seed = 220507610 + int("".join(ch for ch in args.workload if ch.isdigit())[:1] or 0)
+    if cfg.get("pareto"):   # strong scaling: one batch, sharded over the ranks by cell count (wsb_plan_shards)
+        (qc, qo, ql), (sc, so, sl) = make_pareto(cfg["pairs"], seed, cap=args.cap)
+        all_idx = np.arange(cfg["pairs"], dtype=np.int32)
+        if world > 1:
+            shard_of, _ = N.plan_shards(ql, sl, all_idx, all_idx, world)
+            idx = all_idx[shard_of == rank]
+        else:
+            idx = all_idx
+        q_keep = s_keep = None
+        pool_q, pool_s = (qc, qo, ql), (sc, so, sl)
+        L = None
+    else:
+        q, s = make_batch(cfg, seed + rank)
+        L = cfg["length"]
+        (q_pin, q_keep), (s_pin, s_keep) = pinned(q), pinned(s)
+        off = np.arange(cfg["pairs"], dtype=np.int64) * L
+        ln = np.full(cfg["pairs"], L, np.int32)
+        idx = np.arange(cfg["pairs"], dtype=np.int32)
+        pool_q, pool_s = (q_pin.reshape(-1), off, ln), (s_pin.reshape(-1), off, ln)
+    n = len(idx)
     ctx = W.get_context(device)
-    batch = N.Batch(ctx, q_pin.reshape(-1), off, ln, s_pin.reshape(-1), off, ln, idx, idx)
+    batch = N.Batch(ctx, *pool_q, *pool_s, idx, idx)
     cells = batch.total_cells
     traceback = bool(cfg.get("traceback"))
 
@@ -249,19 +302,18 @@ def main():
     wall = time.perf_counter() - t_wall0
     clocks = sampler.stop()
     total_ms = dist_max(float(np.sum(step_ms)), world)      # slowest rank
-    total_cells = dist_sum(float(cells), world) * args.steps
+    total_cells = dist_sum(float(cells), world) * args.steps   # weak: every rank its own batch; strong (cfg5): the shards add up to the one batch
     value = total_cells / (total_ms * 1e-3) / 1e9
     launches = int(dist_sum(float(launches), world))
 
     # end to end through the public API: host buffers in, host results out, every step
-    pool_q, pool_s = W.SequencePool(q_pin.reshape(-1), off, ln), W.SequencePool(s_pin.reshape(-1), off, ln)
     pair_arr = np.stack([idx, idx], 1)
-    job = W.BatchJob(pool_q, pool_s, pair_arr, W.AlignConfig(cfg["align_type"], cfg["gap_model"],
+    job = W.BatchJob(W.SequencePool(*pool_q), W.SequencePool(*pool_s), pair_arr, W.AlignConfig(cfg["align_type"], cfg["gap_model"],
                                                            "traceback" if traceback else "score_only"),
                      scheme, tuning=W.EngineTuning(packed=(variant != "i32")), devices=[device])
     if variant == "i32":
         os.environ["WSB_VARIANT"] = "i32"
-    e2e_steps = max(1, min(args.steps, 3))
+    e2e_steps = max(1, min(args.steps, 5))
     rep = W.run_batch(job)  # warm
     dist_barrier(world)
     t0 = time.perf_counter()
@@ -275,7 +327,7 @@ def main():
     peaks = measured_peaks()
     f_ghz = float(peaks.get("sm_max_mhz", 1965.0)) / 1e3
     n_sm = ctx.sm_count
-    width = 1 if variant == "i32" else 2
+    width = 1 if (variant == "i32" or args.workload in ("cfg3", "cfg4", "cfg5")) else 2   # dominant kernel: int32 fill / long-read kernel
     peak = n_sm * 128 * f_ghz * width / cfg["i_cell"]
     per_gpu = value / world
     traffic = None
@@ -293,12 +345,15 @@ def main():
 
     if rank == 0:
         line = {"metric": "GCUPS", "value": value, "unit": "GCUPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": "i32" if variant == "i32" else "f16x2", "data": "synthetic",
-                "config": {"workload": args.workload, "pairs_per_gpu": n, "read_length": L, "align_type": cfg["align_type"],
+                "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong" if strong else "weak",
+                "vs_baseline": None, "dtype": "i32" if width == 1 else "f16x2", "data": "synthetic",
+                "config": {"workload": args.workload, "pairs_per_gpu": n, "read_length": L if L else "pareto 100..%d" % args.cap,
+                           "align_type": cfg["align_type"],
                            "gap_model": cfg["gap_model"], "scheme": list(cfg["scheme"]),
                            "result_mode": "traceback" if traceback else "score_only", "variant": variant,
-                           "l2": f"inputs {2 * n * L / 1e6:.0f} MB per GPU vs 126 MB L2 (no flush needed)",
+                           "l2": f"inputs {(len(pool_q[0]) + len(pool_s[0])) / 1e6:.0f} MB per GPU vs 126 MB L2 "
+                                 + ("(no flush needed)" if len(pool_q[0]) + len(pool_s[0]) > 252e6 else
+                                    "(inputs re-read from L2/HBM each step; per-cell DRAM traffic is ~0 either way)"),
                            "sharding": "independent pairs per rank, no collective; gloo for barrier/max only"},
                 "roofline": roofline,
                 "e2e": {"value": e2e_value, "unit": "GCUPS", "h2d_bytes_per_step": int(rep.h2d_bytes) * world,
@@ -307,7 +362,7 @@ def main():
         if not args.no_cpu_baseline:
             rate, threads, pairs, dt = cpu_sample(cfg)
             line["cpu_baseline"] = {"value": rate, "unit": "GCUPS", "cores": threads, "kind": "port",
-                                    "sample": f"{pairs} pairs of {L} bp ({dt:.1f} s), oracle/wsoracle.c with OpenMP"}
+                                    "sample": f"{pairs} pairs of {L if L else 'pareto(cap 6000)'} bp ({dt:.1f} s), oracle/wsoracle.c with OpenMP"}
         print(json.dumps(line))
     batch.close()
     if world > 1:

@@ -81,6 +81,14 @@ int wsb_ctx_sm_count(const wsb_ctx* ctx);
 int wsb_batch_create(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t* q_off, const int32_t* q_len, int64_t n_q,
                      const uint8_t* s_codes, const int64_t* s_off, const int32_t* s_len, int64_t n_s,
                      const int32_t* pair_q, const int32_t* pair_s, int64_t n_pairs, wsb_batch** out);
+/* Same, but returns while the copies are still in flight on the context's copy stream: the host arrays must stay
+ * valid and unchanged until the first wsb_batch_score / wsb_batch_traceback on the batch has been followed by a fetch
+ * (or until wsb_batch_destroy).  Large batches are uploaded in up to eight pieces and the first score call launches
+ * piece by piece, so the transfer of later pieces overlaps the kernels of earlier ones (pinned host memory makes the
+ * copies truly asynchronous; pageable memory is staged by the driver). */
+int wsb_batch_create_async(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t* q_off, const int32_t* q_len, int64_t n_q,
+                           const uint8_t* s_codes, const int64_t* s_off, const int32_t* s_len, int64_t n_s,
+                           const int32_t* pair_q, const int32_t* pair_s, int64_t n_pairs, wsb_batch** out);
 void wsb_batch_destroy(wsb_batch* b);
 
 /* Score every pair on the device; results stay in HBM until wsb_batch_fetch_scores.  kernel_ms (optional) receives
@@ -100,6 +108,13 @@ int wsb_batch_fetch_scores(wsb_batch* b, int32_t* out_score, int32_t* out_i, int
 int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* scheme, int align_type, float* kernel_ms, int32_t* n_launches);
 int wsb_batch_fetch_traceback(wsb_batch* b, int32_t* out_score, int32_t* q_start, int32_t* q_end, int32_t* s_start,
                               int32_t* s_end, uint32_t* cigar, int64_t cigar_cap, int64_t* cigar_off, int32_t* status);
+
+/* 1 when the last plan of the batch holds per-pair faults (then fetch the status array), else 0 */
+int wsb_batch_has_faults(const wsb_batch* b);
+/* Page-locked host memory for result buffers, recycled by the library (a fetch into such a block runs at PCIe speed;
+ * pageable destinations are staged by the driver).  Blocks are process-wide, not tied to a context. */
+int wsb_pinned_alloc(size_t bytes, void** out);
+void wsb_pinned_free(void* block);
 
 int64_t wsb_batch_total_cells(const wsb_batch* b); /* sum of m*n over pairs (BatchReport.total_cells, batch.py:243-247) */
 

@@ -21,9 +21,10 @@ WSB_OK, WSB_E_CUDA, WSB_E_ARG, WSB_E_NOMEM, WSB_E_LENGTH, WSB_E_RANGE, WSB_E_SCH
 
 EXPORTED_SYMBOLS = (
     "wsb_strerror", "wsb_version", "wsb_device_count", "wsb_ctx_create", "wsb_ctx_destroy", "wsb_last_error",
-    "wsb_ctx_sm_count", "wsb_batch_create", "wsb_batch_destroy", "wsb_batch_score", "wsb_batch_fetch_scores",
+    "wsb_ctx_sm_count", "wsb_batch_create", "wsb_batch_create_async", "wsb_batch_destroy", "wsb_batch_score", "wsb_batch_fetch_scores",
     "wsb_batch_traceback", "wsb_batch_fetch_traceback", "wsb_batch_total_cells", "wsb_score_batch",
-    "wsb_traceback_batch", "wsb_merged_state_exact", "wsb_f16_range_ok", "wsb_plan_shards",
+    "wsb_traceback_batch", "wsb_merged_state_exact", "wsb_f16_range_ok", "wsb_plan_shards", "wsb_batch_has_faults", "wsb_pinned_alloc",
+    "wsb_pinned_free",
 )
 
 
@@ -57,6 +58,7 @@ def load():
     lib.wsb_ctx_destroy.restype = None
     lib.wsb_ctx_sm_count.argtypes = [p]
     lib.wsb_batch_create.argtypes = [p, p, p, p, i64, p, p, p, i64, p, p, i64, p]
+    lib.wsb_batch_create_async.argtypes = [p, p, p, p, i64, p, p, p, i64, p, p, i64, p]
     lib.wsb_batch_destroy.argtypes = [p]
     lib.wsb_batch_destroy.restype = None
     lib.wsb_batch_score.argtypes = [p, p, ci, ci, p, p]
@@ -67,6 +69,10 @@ def load():
     lib.wsb_batch_total_cells.restype = i64
     lib.wsb_score_batch.argtypes = [p, p, ci, ci, p, p, p, i64, p, p, p, i64, p, p, i64, p, p, p, p]
     lib.wsb_traceback_batch.argtypes = [p, p, ci, p, p, p, i64, p, p, p, i64, p, p, i64, p, p, p, p, p, p, i64, p, p]
+    lib.wsb_batch_has_faults.argtypes = [p]
+    lib.wsb_pinned_alloc.argtypes = [ctypes.c_size_t, p]
+    lib.wsb_pinned_free.argtypes = [p]
+    lib.wsb_pinned_free.restype = None
     lib.wsb_merged_state_exact.argtypes = [p]
     lib.wsb_f16_range_ok.argtypes = [p, i32, i32]
     lib.wsb_plan_shards.argtypes = [p, p, p, p, i64, i32, p, p]
@@ -76,6 +82,21 @@ def load():
 
 def _ptr(a):
     return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def pinned_empty(n: int, dtype=np.int32) -> np.ndarray:
+    """Uninitialised array in page-locked host memory from the library's block cache; the block goes back to the
+    cache when the array (and every view of it) is garbage collected."""
+    import weakref
+    lib = load()
+    dt = np.dtype(dtype)
+    nbytes = max(int(n) * dt.itemsize, 1)
+    ptr = ctypes.c_void_p()
+    if lib.wsb_pinned_alloc(nbytes, ctypes.byref(ptr)) != WSB_OK or not ptr.value:
+        return np.empty(n, dt)  # no pinned memory to be had: a pageable array still works, only slower
+    buf = (ctypes.c_char * nbytes).from_address(ptr.value)
+    weakref.finalize(buf, lib.wsb_pinned_free, ptr.value)
+    return np.frombuffer(buf, dtype=dt, count=int(n))
 
 
 def scheme_struct(scheme) -> SchemeStruct:
@@ -172,7 +193,8 @@ class Batch:
         self.n_pairs = len(arrs[6])
         self.h2d_bytes = int(sum(a.nbytes for a in arrs))
         h = ctypes.c_void_p()
-        rc = self._lib.wsb_batch_create(ctx._h, _ptr(arrs[0]), _ptr(arrs[1]), _ptr(arrs[2]), len(arrs[2]),
+        self._keep = arrs  # the upload is asynchronous: the arrays must outlive it (released in close())
+        rc = self._lib.wsb_batch_create_async(ctx._h, _ptr(arrs[0]), _ptr(arrs[1]), _ptr(arrs[2]), len(arrs[2]),
                                         _ptr(arrs[3]), _ptr(arrs[4]), _ptr(arrs[5]), len(arrs[5]),
                                         _ptr(arrs[6]), _ptr(arrs[7]), self.n_pairs, ctypes.byref(h))
         if rc:
@@ -196,11 +218,16 @@ class Batch:
 
     def fetch_scores(self):
         n = self.n_pairs
-        score = np.empty(n, np.int32); ei = np.empty(n, np.int32); ej = np.empty(n, np.int32)
-        status = np.empty(n, np.int32)
+        big = n >= 65536
+        score, ei, ej = (pinned_empty(n) for _ in range(3)) if big else (np.empty(n, np.int32) for _ in range(3))
+        # the per-pair status array only carries information when the plan recorded a fault
+        self.has_faults = bool(self._lib.wsb_batch_has_faults(self._h))
+        status = np.empty(n, np.int32) if self.has_faults else None
         rc = self._lib.wsb_batch_fetch_scores(self._h, _ptr(score), _ptr(ei), _ptr(ej), _ptr(status))
         if rc:
             raise status_exception(rc, self.ctx.last_error())
+        if status is None:
+            status = np.zeros(n, np.int32)  # calloc: costs nothing until somebody reads it
         return score, ei, ej, status
 
     def traceback(self, scheme, align_type: str, timed: bool = True):
@@ -237,6 +264,7 @@ class Batch:
         if getattr(self, "_h", None):
             self._lib.wsb_batch_destroy(self._h)
             self._h = None
+        self._keep = None
 
     def __del__(self):
         try:

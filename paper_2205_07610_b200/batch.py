@@ -100,6 +100,9 @@ class BatchJob:
             qi, si = arr[bad[0]]
             raise ValueError(f"pair ({int(qi)}, {int(si)}) is out of range")
         self._pair_array = np.ascontiguousarray(arr, np.int32)
+        # the device wants the two index columns as separate contiguous arrays: split once, here
+        self._pair_q = np.ascontiguousarray(self._pair_array[:, 0])
+        self._pair_s = np.ascontiguousarray(self._pair_array[:, 1])
 
 
 class ResultArray(_SequenceABC):
@@ -107,9 +110,16 @@ class ResultArray(_SequenceABC):
     millions of pairs do not pay for millions of Python objects up front."""
 
     def __init__(self, score, q_start, q_end, s_start, s_end, cells, runs=None, run_off=None):
-        self.score, self.q_start, self.q_end, self.s_start, self.s_end, self.cells = (
+        self.score, self.q_start, self.q_end, self.s_start, self.s_end, self._cells = (
             score, q_start, q_end, s_start, s_end, cells)
         self.runs, self.run_off = runs, run_off
+
+    @property
+    def cells(self):
+        """m * n per pair; computed on first use (a callable is stored until then)."""
+        if callable(self._cells):
+            self._cells = self._cells()
+        return self._cells
 
     def __len__(self) -> int:
         return int(self.score.shape[0])
@@ -164,20 +174,22 @@ def _variant_for(job: BatchJob, cfg: AlignConfig) -> str:
     return env if env in ("auto", "f16x2", "i32") else "auto"
 
 
-def _run_shard(device: int, queries: SequencePool, subjects: SequencePool, pair_array: np.ndarray, cfg: AlignConfig,
-               scheme: ScoringScheme, variant: str, out: dict):
+def _run_shard(device: int, queries: SequencePool, subjects: SequencePool, pair_q: np.ndarray, pair_s: np.ndarray,
+               cfg: AlignConfig, scheme: ScoringScheme, variant: str, out: dict):
     try:
         ctx = get_context(device)
         batch = N.Batch(ctx, queries.codes, queries.off, queries.len, subjects.codes, subjects.off, subjects.len,
-                        pair_array[:, 0], pair_array[:, 1])
+                        pair_q, pair_s)
         try:
             out["h2d"] = batch.h2d_bytes
+            out["cells"] = batch.total_cells
             if cfg.result_mode == "traceback":
                 out["ms"], out["launches"] = batch.traceback(scheme, cfg.align_type)
                 out["tb"] = batch.fetch_traceback()
             else:
                 out["ms"], out["launches"] = batch.score(scheme, cfg.align_type, variant)
                 out["scores"] = batch.fetch_scores()
+                out["faults"] = batch.has_faults
         finally:
             batch.close()
     except BaseException as exc:  # re-raised by the caller in the submitting thread
@@ -195,18 +207,23 @@ def run_batch(job: BatchJob) -> BatchReport:
     queries = SequencePool.from_sequences(job.queries)
     subjects = SequencePool.from_sequences(job.subjects)
     pairs = job._pair_array
+    pair_q, pair_s = job._pair_q, job._pair_s
     n = len(pairs)
     variant = _variant_for(job, cfg)
-    m_arr = queries.len.take(pairs[:, 0]).astype(np.int64)
-    n_arr = subjects.len.take(pairs[:, 1]).astype(np.int64)
-    cells = m_arr * n_arr
+    lens = {}
+
+    def pair_lengths():  # per-pair (m, n) as int64, only materialised when something needs them
+        if not lens:
+            lens["m"] = queries.len.take(pair_q).astype(np.int64)
+            lens["n"] = subjects.len.take(pair_s).astype(np.int64)
+        return lens["m"], lens["n"]
 
     t0 = time.perf_counter()
     if len(devices) == 1:
-        shard_index = [np.arange(n)]
-        shard_cells = [int(cells.sum())]
+        shard_index = [np.arange(n) if cfg.result_mode == "traceback" else range(n)]
+        shard_cells = []
     else:
-        shard_of, sc = plan_shards(queries, subjects, pairs, len(devices))
+        shard_of, sc = N.plan_shards(queries.len, subjects.len, pair_q, pair_s, len(devices))
         shard_index = [np.nonzero(shard_of == k)[0] for k in range(len(devices))]
         shard_cells = [int(x) for x in sc]
     outs = [dict() for _ in devices]
@@ -214,12 +231,11 @@ def run_batch(job: BatchJob) -> BatchReport:
     for dev, idx, out in zip(devices, shard_index, outs):
         if len(idx) == 0:
             continue
-        sub_pairs = pairs if len(devices) == 1 else np.ascontiguousarray(pairs[idx])
         if len(devices) == 1:  # no thread hop for the common single-GPU case
-            _run_shard(dev, queries, subjects, sub_pairs, cfg, job.scheme, variant, out)
+            _run_shard(dev, queries, subjects, pair_q, pair_s, cfg, job.scheme, variant, out)
             continue
         th = threading.Thread(target=_run_shard, name=f"waveseq-gpu-{dev}",
-                              args=(dev, queries, subjects, sub_pairs, cfg, job.scheme, variant, out))
+                              args=(dev, queries, subjects, pair_q[idx], pair_s[idx], cfg, job.scheme, variant, out))
         threads.append(th)
         th.start()
     for th in threads:
@@ -233,9 +249,8 @@ def run_batch(job: BatchJob) -> BatchReport:
     runs = run_off = None
     if single and cfg.result_mode != "traceback":  # one shard: the fetched arrays are the result arrays
         score, qe, se, status = outs[0]["scores"]
-        if cfg.align_type == "global":
+        if cfg.align_type == "global":   # the kernels report (m, n) as the end cell
             qs = np.zeros(n, np.int32); ss = qs
-            qe = m_arr.astype(np.int32); se = n_arr.astype(np.int32)
         else:
             qs, ss = qe, se
     else:
@@ -270,20 +285,26 @@ def run_batch(job: BatchJob) -> BatchReport:
                 continue
             sc_, ei, ej, st = out["scores"]
             score[idx], qe[idx], se[idx], status[idx] = sc_, ei, ej, st
-        if cfg.align_type == "global":
-            qe[:] = m_arr; se[:] = n_arr
-        else:  # start is unknown without a traceback pass: both span ends carry the argmax cell (batch.py:111-115)
+        if cfg.align_type != "global":  # start is unknown without a traceback pass: both span ends carry the argmax cell (batch.py:111-115)
             qs[:] = qe; ss[:] = se
-    bad = np.nonzero(status)[0]
+    any_fault = cfg.result_mode == "traceback" or any(o.get("faults", True) for o in outs if o)
+    bad = np.nonzero(status)[0] if any_fault else ()
     if len(bad):
         i = int(bad[0])
+        m_arr, n_arr = pair_lengths()
         raise BatchError(i, N.status_exception(int(status[i]), f"problem of size {int(m_arr[i])}x{int(n_arr[i])}"))
 
-    results = ResultArray(score, qs, qe, ss, se, cells, runs, run_off)
-    if n <= 100_000:
+    def cell_counts():
+        m_arr, n_arr = pair_lengths()
+        return m_arr * n_arr
+
+    results = ResultArray(score, qs, qe, ss, se, cell_counts, runs, run_off)
+    if n <= 4096:  # small batches: a plain list like the reference's; larger ones stay array-backed (same Sequence API)
         results = list(results)
     d2h = sum(4 * 4 * len(idx) for idx in shard_index) + (runs.nbytes if runs is not None else 0)
-    return BatchReport(results=results, wall_time=wall, total_cells=int(cells.sum()),
+    if not shard_cells:
+        shard_cells = [int(outs[0].get("cells", 0))]
+    return BatchReport(results=results, wall_time=wall, total_cells=int(sum(o.get("cells", 0) for o in outs)),
                        kernel_ms=max((o.get("ms", 0.0) for o in outs), default=0.0),
                        gpu_launches=sum(o.get("launches", 0) for o in outs),
                        h2d_bytes=sum(o.get("h2d", 0) for o in outs), d2h_bytes=d2h, shard_cells=shard_cells)

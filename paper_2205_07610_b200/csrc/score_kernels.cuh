@@ -47,7 +47,8 @@ struct ScoreParams {
     const int32_t* pair_q; const int32_t* pair_s;
     const int32_t* units;  // NV pair indices per unit (-1 = empty slot); nullptr = identity (unit u -> pairs NV*u+v)
     int64_t n_units;
-    int64_t n_pairs;
+    int64_t n_pairs;       // identity mapping: exclusive end of the pair range of this launch
+    int64_t pair_base;     // identity mapping: first pair of this launch (a batch may be scored in pieces)
     int32_t* out_score; int32_t* out_i; int32_t* out_j;
     int32_t match, mismatch, alpha, beta;  // beta == alpha for the linear model
     void* bnd;          // stage border scratch: per lane group bnd_rows x {A, B}
@@ -206,7 +207,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const ScoreParams prm) 
             int p = -1;
             if (u < prm.n_units) {
                 if (prm.units) p = prm.units[u * NV + v];
-                else { const int64_t pp = u * NV + v; p = pp < prm.n_pairs ? (int)pp : -1; }
+                else { const int64_t pp = prm.pair_base + u * NV + v; p = pp < prm.n_pairs ? (int)pp : -1; }
             }
             pidx[v] = p; m[v] = 0; n[v] = 0; qp[v] = nullptr; sp[v] = nullptr;
             if (p >= 0) {

@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(kThreads) f16_local_short_kernel(const ScorePa
             int p = -1;
             if (u < prm.n_units) {
                 if (prm.units) p = prm.units[u * 2 + v];
-                else { const int64_t pp = u * 2 + v; p = pp < prm.n_pairs ? (int)pp : -1; }
+                else { const int64_t pp = prm.pair_base + u * 2 + v; p = pp < prm.n_pairs ? (int)pp : -1; }
             }
             pidx[v] = p; m[v] = 0; n[v] = 0; qp[v] = nullptr; sp[v] = nullptr;
             if (p >= 0) {

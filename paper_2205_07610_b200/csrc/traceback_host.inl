@@ -3,7 +3,7 @@
 // wsb_batch_traceback = score pass (end cells, same kernels and tie-break as score-only mode) + per chunk of pairs:
 // direction-code fill -> walk pass 1 (run counts, start cells) -> prefix sum -> walk pass 2 (runs, forward order).
 // Pairs are processed in chunks so that the 0.5 byte/cell code scratch stays inside a fixed budget
-// (WSB_TB_SCRATCH_MB, default 4096 MiB).
+// (WSB_TB_SCRATCH_MB, default 16 GiB).
 #include <cub/device/device_scan.cuh>
 
 struct TbShape { int P, K; };
@@ -72,7 +72,7 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
     const int P = kTbShapes[shape].P, K = kTbShapes[shape].K;
     TbFillFn fill = shape == 0 ? tb_pick_fill<8, 16>(atype, affine)
                   : shape == 1 ? tb_pick_fill<8, 32>(atype, affine) : tb_pick_fill<32, 16>(atype, affine);
-    size_t budget_words = (size_t)4096 << 18;  // 4096 MiB in 32-bit words
+    size_t budget_words = (size_t)16384 << 18;  // 16 GiB in 32-bit words (a B200 carries 180 GB)
     if (const char* e = getenv("WSB_TB_SCRATCH_MB")) { const long mb = atol(e); if (mb > 0) budget_words = (size_t)mb << 18; }
 
     int per_sm = 0;

@@ -29,6 +29,7 @@ struct wsb_ctx {
     int device = 0;
     int sm_count = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;  // host-to-device uploads of a batch run here, overlapping the kernels of earlier pieces
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // launch groups of the long-read kernel run side by side on these streams (fork after ev0, join before ev1)
     static constexpr int kAux = 6;
@@ -103,6 +104,13 @@ struct wsb_batch {
     const Plan* last_plan = nullptr;
     void* d_bnd = nullptr;
     size_t bnd_bytes = 0;
+    // Piecewise upload: piece k covers pairs [piece_end[k-1], piece_end[k]) and is complete (pools included) once
+    // piece_ev[k] has fired on the copy stream; the first score call after creation launches piece by piece.
+    static constexpr int kMaxPieces = 8;
+    int n_pieces = 0;
+    int64_t piece_end[kMaxPieces] = {};
+    cudaEvent_t piece_ev[kMaxPieces] = {};
+    bool upload_pending = false;
     TracebackState tb;  // traceback_kernels.cuh
 };
 
@@ -204,6 +212,7 @@ extern "C" int wsb_ctx_create(int device, wsb_ctx** out) {
     if (cudaSetDevice(device) != cudaSuccess ||
         cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
         (void)cudaGetLastError();
         delete c;
@@ -230,6 +239,7 @@ extern "C" void wsb_ctx_destroy(wsb_ctx* c) {
     }
     if (c->d_queues) cudaFree(c->d_queues);
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     delete c;
 }
 
@@ -237,18 +247,43 @@ extern "C" const char* wsb_last_error(const wsb_ctx* c) { return c ? c->last_err
 extern "C" int wsb_ctx_sm_count(const wsb_ctx* c) { return c ? c->sm_count : 0; }
 
 // ------------------------------------------------------------------------------------------------ batch
+// Metadata arrays of regular batches (equal-length reads laid out back to back, pair i = (i, i)) are arithmetic
+// progressions: those are generated on the device instead of crossing the bus (40 bytes per pair at 150 bp).
+template <class T> static bool is_progression(const T* a, int64_t n, T& a0, T& d) {
+    a0 = n > 0 ? a[0] : T(0);
+    d = n > 1 ? T(a[1] - a[0]) : T(0);
+    for (int64_t k = 0; k < n; ++k)
+        if (a[k] != T(a0 + d * T(k))) return false;
+    return true;
+}
+template <class T> __global__ void fill_progression_kernel(T* dst, T a0, T d, int64_t n) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) dst[k] = T(a0 + d * T(k));
+}
+
 template <class T> static int upload(wsb_ctx* ctx, T** dst, const T* src, int64_t count) {
     *dst = nullptr;
     const size_t bytes = sizeof(T) * (size_t)std::max<int64_t>(count, 1);
     CUDA_TRY(ctx, ctx->alloc((void**)dst, bytes));
-    if (count > 0) CUDA_TRY(ctx, cudaMemcpyAsync(*dst, src, sizeof(T) * (size_t)count, cudaMemcpyHostToDevice, ctx->stream));
+    if (count > 0) CUDA_TRY(ctx, cudaMemcpyAsync(*dst, src, sizeof(T) * (size_t)count, cudaMemcpyHostToDevice, ctx->copy_stream));
+    return WSB_OK;
+}
+template <class T> static int generate(wsb_ctx* ctx, T** dst, T a0, T d, int64_t count) {
+    *dst = nullptr;
+    CUDA_TRY(ctx, ctx->alloc((void**)dst, sizeof(T) * (size_t)std::max<int64_t>(count, 1)));
+    if (count > 0) {
+        fill_progression_kernel<T><<<(unsigned)((count + 255) / 256), 256, 0, ctx->copy_stream>>>(*dst, a0, d, count);
+        CUDA_TRY(ctx, cudaGetLastError());
+    }
     return WSB_OK;
 }
 
 extern "C" void wsb_batch_destroy(wsb_batch* b) {
     if (!b) return;
     cudaSetDevice(b->ctx->device);
+    cudaStreamSynchronize(b->ctx->copy_stream);
     cudaStreamSynchronize(b->ctx->stream);
+    for (int k = 0; k < wsb_batch::kMaxPieces; ++k) if (b->piece_ev[k]) cudaEventDestroy(b->piece_ev[k]);
     for (void* p : {(void*)b->d_qcodes, (void*)b->d_scodes, (void*)b->d_qoff, (void*)b->d_soff, (void*)b->d_qlen,
                     (void*)b->d_slen, (void*)b->d_pq, (void*)b->d_ps, (void*)b->d_score, (void*)b->d_i, (void*)b->d_j,
                     b->d_bnd})
@@ -258,10 +293,10 @@ extern "C" void wsb_batch_destroy(wsb_batch* b) {
     delete b;
 }
 
-extern "C" int wsb_batch_create(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t* q_off, const int32_t* q_len,
-                                int64_t n_q, const uint8_t* s_codes, const int64_t* s_off, const int32_t* s_len,
-                                int64_t n_s, const int32_t* pair_q, const int32_t* pair_s, int64_t n_pairs,
-                                wsb_batch** out) {
+extern "C" int wsb_batch_create_async(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t* q_off, const int32_t* q_len,
+                                      int64_t n_q, const uint8_t* s_codes, const int64_t* s_off, const int32_t* s_len,
+                                      int64_t n_s, const int32_t* pair_q, const int32_t* pair_s, int64_t n_pairs,
+                                      wsb_batch** out) {
     if (!ctx || !out || !q_codes || !q_off || !q_len || !s_codes || !s_off || !s_len || !pair_q || !pair_s ||
         n_q <= 0 || n_s <= 0 || n_pairs <= 0 || n_pairs > (int64_t)0x7fffffff)
         return WSB_E_ARG;
@@ -305,29 +340,146 @@ extern "C" int wsb_batch_create(wsb_ctx* ctx, const uint8_t* q_codes, const int6
         b->total_cells += cells[k];
     }
 
-    const int64_t q_bytes = q_off[n_q - 1] + q_len[n_q - 1];
-    const int64_t s_bytes = s_off[n_s - 1] + s_len[n_s - 1];
-    int64_t q_total = 0, s_total = 0;  // pools need not be packed in order: take the furthest end
-    for (int64_t k = 0; k < n_q; ++k) q_total = std::max(q_total, q_off[k] + q_len[k]);
-    for (int64_t k = 0; k < n_s; ++k) s_total = std::max(s_total, s_off[k] + s_len[k]);
-    (void)q_bytes; (void)s_bytes;
-    int rc;
-#define UP(dst, src, cnt) if ((rc = upload(ctx, &b->dst, src, cnt)) != WSB_OK) { wsb_batch_destroy(b); return rc; }
-    UP(d_qcodes, q_codes, q_total) UP(d_scodes, s_codes, s_total)
-    UP(d_qoff, q_off, n_q) UP(d_soff, s_off, n_s) UP(d_qlen, q_len, n_q) UP(d_slen, s_len, n_s)
-    UP(d_pq, pair_q, n_pairs) UP(d_ps, pair_s, n_pairs)
-#undef UP
-    for (int32_t** p : {&b->d_score, &b->d_i, &b->d_j}) {
-        cudaError_t e = ctx->alloc((void**)p, sizeof(int32_t) * (size_t)n_pairs);
-        if (e != cudaSuccess) { ctx->last_error = cudaGetErrorString(e); wsb_batch_destroy(b); return WSB_E_NOMEM; }
+    // metadata scans, one host thread each: furthest sequence end of either pool (pools need not be packed in order)
+    // and the arithmetic-progression test of the six index / offset / length arrays
+    int64_t q_total = 0, s_total = 0;
+    int64_t o0[2] = {0, 0}, od[2] = {0, 0};
+    int32_t l0[2] = {0, 0}, ld[2] = {0, 0}, p0[2] = {0, 0}, pd[2] = {0, 0};
+    bool ap_off[2] = {false, false}, ap_len[2] = {false, false}, ap_pair[2] = {false, false};
+    {
+        auto total_q = [&] { int64_t x = 0; for (int64_t k = 0; k < n_q; ++k) x = std::max(x, q_off[k] + q_len[k]); q_total = x; };
+        auto total_s = [&] { int64_t x = 0; for (int64_t k = 0; k < n_s; ++k) x = std::max(x, s_off[k] + s_len[k]); s_total = x; };
+        if (n_pairs >= 65536) {
+            std::thread th[8] = {
+                std::thread(total_q), std::thread(total_s),
+                std::thread([&] { ap_off[0] = is_progression(q_off, n_q, o0[0], od[0]); }),
+                std::thread([&] { ap_off[1] = is_progression(s_off, n_s, o0[1], od[1]); }),
+                std::thread([&] { ap_len[0] = is_progression(q_len, n_q, l0[0], ld[0]); }),
+                std::thread([&] { ap_len[1] = is_progression(s_len, n_s, l0[1], ld[1]); }),
+                std::thread([&] { ap_pair[0] = is_progression(pair_q, n_pairs, p0[0], pd[0]); }),
+                std::thread([&] { ap_pair[1] = is_progression(pair_s, n_pairs, p0[1], pd[1]); })};
+            for (auto& x : th) x.join();
+        } else { total_q(); total_s(); }
     }
-    cudaError_t e = cudaStreamSynchronize(ctx->stream);  // host arrays may be reused by the caller after return
-    if (e != cudaSuccess) { ctx->last_error = cudaGetErrorString(e); wsb_batch_destroy(b); return WSB_E_CUDA; }
+    // Pieces: the pairs are cut into up to eight ranges; piece k needs the pool bytes up to the furthest sequence end
+    // any pair of pieces 0..k references, so the pools go up in address order, one slice per piece, and a piece can be
+    // scored while the slices of later pieces are still on the bus.  (Arbitrary pair lists degrade gracefully: the
+    // first piece then simply waits for most of the pool.)
+    int n_pieces = 1;
+    if (n_pairs >= 262144 && q_total + s_total >= ((int64_t)32 << 20)) n_pieces = wsb_batch::kMaxPieces;
+    b->n_pieces = n_pieces;
+    std::vector<int64_t> need_q((size_t)n_pieces, 0), need_s((size_t)n_pieces, 0);
+    {
+        auto piece_work = [&](int k) {
+            const int64_t lo = k == 0 ? 0 : b->piece_end[k - 1], hi = b->piece_end[k];
+            int64_t mq = 0, msq = 0;
+            for (int64_t p = lo; p < hi; ++p) {
+                const int a = pair_q[p], c = pair_s[p];
+                mq = std::max(mq, q_off[a] + q_len[a]);
+                msq = std::max(msq, s_off[c] + s_len[c]);
+            }
+            need_q[k] = mq; need_s[k] = msq;
+        };
+        for (int k = 0; k < n_pieces; ++k)   // boundaries on multiples of 2048 pairs (packed units never straddle pieces)
+            b->piece_end[k] = k + 1 == n_pieces ? n_pairs : std::min<int64_t>(n_pairs, (n_pairs * (k + 1) / n_pieces + 2047) / 2048 * 2048);
+        if (n_pieces == 1) { need_q[0] = q_total; need_s[0] = s_total; }
+        else {
+            std::vector<std::thread> th;
+            for (int k = 0; k < n_pieces; ++k) th.emplace_back(piece_work, k);
+            for (auto& x : th) x.join();
+            for (int k = 1; k < n_pieces; ++k) { need_q[k] = std::max(need_q[k], need_q[k - 1]); need_s[k] = std::max(need_s[k], need_s[k - 1]); }
+            need_q[n_pieces - 1] = q_total; need_s[n_pieces - 1] = s_total;
+        }
+    }
+    int rc;
+    {
+#define UPG(dst, src, cnt, ap, a0, d) \
+        if ((rc = (ap) ? generate(ctx, &b->dst, a0, d, cnt) : upload(ctx, &b->dst, src, cnt)) != WSB_OK) { wsb_batch_destroy(b); return rc; }
+        UPG(d_qoff, q_off, n_q, ap_off[0], o0[0], od[0]) UPG(d_soff, s_off, n_s, ap_off[1], o0[1], od[1])
+        UPG(d_qlen, q_len, n_q, ap_len[0], l0[0], ld[0]) UPG(d_slen, s_len, n_s, ap_len[1], l0[1], ld[1])
+        UPG(d_pq, pair_q, n_pairs, ap_pair[0], p0[0], pd[0]) UPG(d_ps, pair_s, n_pairs, ap_pair[1], p0[1], pd[1])
+#undef UPG
+    }
+    auto fail = [&](cudaError_t e) {
+        ctx->last_error = cudaGetErrorString(e);
+        wsb_batch_destroy(b);
+        return e == cudaErrorMemoryAllocation ? WSB_E_NOMEM : WSB_E_CUDA;
+    };
+    cudaError_t e;
+    if ((e = ctx->alloc((void**)&b->d_qcodes, (size_t)std::max<int64_t>(q_total, 1))) != cudaSuccess) return fail(e);
+    if ((e = ctx->alloc((void**)&b->d_scodes, (size_t)std::max<int64_t>(s_total, 1))) != cudaSuccess) return fail(e);
+    int64_t done_q = 0, done_s = 0;
+    for (int k = 0; k < n_pieces; ++k) {
+        if (need_q[k] > done_q) {
+            e = cudaMemcpyAsync(b->d_qcodes + done_q, q_codes + done_q, (size_t)(need_q[k] - done_q), cudaMemcpyHostToDevice, ctx->copy_stream);
+            if (e != cudaSuccess) return fail(e);
+            done_q = need_q[k];
+        }
+        if (need_s[k] > done_s) {
+            e = cudaMemcpyAsync(b->d_scodes + done_s, s_codes + done_s, (size_t)(need_s[k] - done_s), cudaMemcpyHostToDevice, ctx->copy_stream);
+            if (e != cudaSuccess) return fail(e);
+            done_s = need_s[k];
+        }
+        if ((e = cudaEventCreateWithFlags(&b->piece_ev[k], cudaEventDisableTiming)) != cudaSuccess) return fail(e);
+        if ((e = cudaEventRecord(b->piece_ev[k], ctx->copy_stream)) != cudaSuccess) return fail(e);
+    }
+    b->upload_pending = true;
+    for (int32_t** p : {&b->d_score, &b->d_i, &b->d_j}) {
+        e = ctx->alloc((void**)p, sizeof(int32_t) * (size_t)n_pairs);
+        if (e != cudaSuccess) return fail(e);
+    }
     *out = b;
     return WSB_OK;
 }
 
+extern "C" int wsb_batch_create(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t* q_off, const int32_t* q_len,
+                                int64_t n_q, const uint8_t* s_codes, const int64_t* s_off, const int32_t* s_len,
+                                int64_t n_s, const int32_t* pair_q, const int32_t* pair_s, int64_t n_pairs,
+                                wsb_batch** out) {
+    int rc = wsb_batch_create_async(ctx, q_codes, q_off, q_len, n_q, s_codes, s_off, s_len, n_s, pair_q, pair_s, n_pairs, out);
+    if (rc) return rc;
+    cudaError_t e = cudaStreamSynchronize(ctx->copy_stream);  // host arrays may be reused by the caller after return
+    if (e != cudaSuccess) { ctx->last_error = cudaGetErrorString(e); wsb_batch_destroy(*out); *out = nullptr; return WSB_E_CUDA; }
+    return WSB_OK;
+}
+
 extern "C" int64_t wsb_batch_total_cells(const wsb_batch* b) { return b ? b->total_cells : 0; }
+extern "C" int wsb_batch_has_faults(const wsb_batch* b) { return (b && b->last_plan && b->last_plan->any_error) ? 1 : 0; }
+
+// Page-locked host blocks for result downloads, recycled process-wide (cudaHostAlloc of tens of MB costs milliseconds).
+#include <mutex>
+static std::mutex g_pin_mu;
+static std::multimap<size_t, void*> g_pin_free;
+static std::map<void*, size_t> g_pin_live;
+extern "C" int wsb_pinned_alloc(size_t bytes, void** out) {
+    if (!out) return WSB_E_ARG;
+    const size_t want = std::max<size_t>(4096, (bytes + 4095) / 4096 * 4096);
+    {
+        std::lock_guard<std::mutex> lk(g_pin_mu);
+        auto it = g_pin_free.lower_bound(want);
+        if (it != g_pin_free.end() && it->first <= want + want / 2) {
+            *out = it->second; g_pin_live[*out] = it->first; g_pin_free.erase(it);
+            return WSB_OK;
+        }
+    }
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, want, cudaHostAllocDefault) != cudaSuccess) { (void)cudaGetLastError(); *out = nullptr; return WSB_E_NOMEM; }
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    g_pin_live[p] = want;
+    *out = p;
+    return WSB_OK;
+}
+extern "C" void wsb_pinned_free(void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    auto it = g_pin_live.find(p);
+    if (it == g_pin_live.end()) return;
+    size_t held = 0;
+    for (auto& kv : g_pin_free) held += kv.first;
+    if (held + it->second > ((size_t)1 << 30)) cudaFreeHost(p);   // keep at most 1 GiB parked
+    else g_pin_free.emplace(it->second, p);
+    g_pin_live.erase(it);
+}
 
 // ------------------------------------------------------------------------------------------------ kernel shapes
 struct Shape { int P, K; };
@@ -663,6 +815,12 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
     if (plan.groups.size() > 64) return WSB_E_ARG;  // cannot happen: at most 16 + 10 launch groups per plan
     CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_queues, 0, 64 * sizeof(unsigned int), ctx->stream));
 
+    // first call after creation: the uploads may still be in flight on the copy stream
+    const bool piecewise = b->upload_pending && b->n_pieces > 1 && !plan_only && plan.groups.size() == 1 &&
+                           plan.groups[0].unit_off < 0 && plan.groups[0].long_nw == 0;
+    if (b->upload_pending && !piecewise && b->n_pieces > 0)
+        CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, b->piece_ev[b->n_pieces - 1], 0));
+
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
     int launches = 0, n_aux = 0;
     bool aux_used[wsb_ctx::kAux] = {};
@@ -690,14 +848,34 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
         prm.s_codes = b->d_scodes; prm.s_off = b->d_soff; prm.s_len = b->d_slen;
         prm.pair_q = b->d_pq; prm.pair_s = b->d_ps;
         prm.units = g.unit_off >= 0 ? plan.d_units + g.unit_off : nullptr;
-        prm.n_units = g.n_units; prm.n_pairs = b->n_pairs;
+        prm.n_units = g.n_units; prm.n_pairs = b->n_pairs; prm.pair_base = 0;
         prm.out_score = b->d_score; prm.out_i = b->d_i; prm.out_j = b->d_j;
         prm.match = sch->match; prm.mismatch = sch->mismatch; prm.alpha = sch->gap_open; prm.beta = beta_eff;
         prm.bnd = geo[k].bnd_rows ? (char*)b->d_bnd + geo[k].bnd_off : nullptr; prm.bnd_rows = geo[k].bnd_rows;
+        if (piecewise) {  // uniform batch, identity unit mapping: one launch per uploaded piece, as its slice lands
+            const int nv = g.variant == WSB_VARIANT_F16X2 ? 2 : 1;
+            const Shape sh = g.variant == WSB_VARIANT_F16X2 ? kShapesF16[g.shape] : kShapesI32[g.shape];
+            const int gpb = kThreads / sh.P;
+            const int64_t full_blocks = (g.n_units + gpb - 1) / gpb;
+            const int64_t resident = full_blocks <= geo[k].grid ? (int64_t)1 << 40 : geo[k].grid;  // grid cap = resident blocks
+            for (int pc = 0; pc < b->n_pieces; ++pc) {
+                const int64_t lo = pc == 0 ? 0 : b->piece_end[pc - 1], hi = b->piece_end[pc];
+                if (hi <= lo) continue;
+                CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, b->piece_ev[pc], 0));
+                prm.pair_base = lo; prm.n_pairs = hi; prm.n_units = (hi - lo + nv - 1) / nv;
+                const int64_t blocks = (prm.n_units + gpb - 1) / gpb;
+                const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, resident));
+                geo[k].fn<<<grid, kThreads, geo[k].smem, ctx->stream>>>(prm);
+                CUDA_TRY(ctx, cudaGetLastError());
+                ++launches;
+            }
+            continue;
+        }
         geo[k].fn<<<geo[k].grid, kThreads, geo[k].smem, ctx->stream>>>(prm);
         CUDA_TRY(ctx, cudaGetLastError());
         ++launches;
     }
+    b->upload_pending = false;
     for (int a = 0; a < wsb_ctx::kAux; ++a)
         if (aux_used[a]) {
             CUDA_TRY(ctx, cudaEventRecord(ctx->aux_done[a], ctx->aux[a]));
