@@ -56,6 +56,10 @@ struct ScoreParams {
 };
 
 // ---------------------------------------------------------------- arithmetic policies
+// int32 with the substitution score looked up by one IDP.4A: the subject symbol is kept as a profile word (delta =
+// match - mismatch in the byte of its code, 0 elsewhere or everywhere for flagged / pad symbols), the query symbol as a
+// one-hot byte word (0 for flagged / pad), so H_diag + mismatch + delta * [q == s] is dp4a(profile, onehot, HM_diag).
+// Needs |match - mismatch| <= 127; ArI32W below is the unrestricted fallback.
 struct ArI32 {
     using V = int32_t;
     static constexpr int NV = 1;
@@ -65,10 +69,7 @@ struct ArI32 {
     static __device__ __forceinline__ int get(V a, int) { return a; }
     static __device__ __forceinline__ V add(V a, V b) { return a + b; }
     static __device__ __forceinline__ V vmax(V a, V b) { return max(a, b); }
-    // d = hmd + (q == s ? delta : 0)
-    template <bool RELU> static __device__ __forceinline__ V diag(V hmd, V q, V s, V delta) {
-        return hmd + ((q == s) ? delta : 0);
-    }
+    template <bool RELU> static __device__ __forceinline__ V diag(V hmd, V q, V s, V) { return __dp4a(s, q, hmd); }
     // max(g + c, d [, 0]); d may or may not already be clamped
     template <bool RELU> static __device__ __forceinline__ V addmax(V g, V c, V d) {
         return RELU ? __viaddmax_s32_relu(g, c, d) : __viaddmax_s32(g, c, d);
@@ -78,11 +79,21 @@ struct ArI32 {
     }
     static __device__ __forceinline__ bool any_gt(V a, V b) { return a > b; }
     static __device__ __forceinline__ bool any_ge(V a, V b) { return a >= b; }
-    static __device__ __forceinline__ V codes(int a, int) { return a; }
+    static __device__ __forceinline__ V subj(int a, int, int delta) { return a < 4 ? (V)((unsigned)(delta & 0xff) << (8 * a)) : 0; }
+    static __device__ __forceinline__ V query(int a, int) { return a < 4 ? (V)(1u << (8 * a)) : 0; }
     static __device__ __forceinline__ unsigned gt_mask(V a, V b) { return a > b ? 0xffffu : 0u; }
     static __device__ __forceinline__ unsigned ge_mask(V a, V b) { return a >= b ? 0xffffu : 0u; }
     static __device__ __forceinline__ unsigned bits(V a) { return (unsigned)a; }
     static __device__ __forceinline__ int get_bits(unsigned w, int) { return (int)w; }
+};
+
+// int32 for any scheme: symbol codes compared directly (compare + select + add per cell)
+struct ArI32W : ArI32 {
+    template <bool RELU> static __device__ __forceinline__ V diag(V hmd, V q, V s, V delta) {
+        return hmd + ((q == s) ? delta : 0);
+    }
+    static __device__ __forceinline__ V subj(int a, int, int) { return a; }
+    static __device__ __forceinline__ V query(int a, int) { return a; }
 };
 
 struct ArF16 {
@@ -105,6 +116,8 @@ struct ArF16 {
     static __device__ __forceinline__ bool any_ge(V a, V b) { return __hge2_mask(a, b) != 0u; }
     // symbol codes 0..7 as fp16 integers, both halves in ONE register (the barrier stops the compiler from keeping
     // the halves apart and re-packing them with a PRMT per cell)
+    static __device__ __forceinline__ V subj(int a, int b, int) { return codes(a, b); }
+    static __device__ __forceinline__ V query(int a, int b) { return codes(a, b); }
     static __device__ __forceinline__ V codes(int a, int b) {
         const unsigned lut_lo = 0x42403C00u, lut_hi = 0x47464544u;  // high bytes of fp16(0..3), fp16(4..7)
         const unsigned ha = __byte_perm(lut_lo, lut_hi, a) & 0xffu, hb = __byte_perm(lut_lo, lut_hi, b) & 0xffu;
@@ -246,7 +259,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const ScoreParams prm) 
 #pragma unroll
                     for (int v = 0; v < NV; ++v)
                         if (x < m[v]) { const int code = qp[v][x]; c[v] = code < 4 ? code : kFlagQuery; }
-                    qring[gib][x] = AR::codes(c[0], c[1]);
+                    qring[gib][x] = AR::query(c[0], c[1]);
                 }
                 __syncwarp();
             }
@@ -259,7 +272,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const ScoreParams prm) 
 #pragma unroll
                 for (int v = 0; v < NV; ++v)
                     if (col0 + c < n[v]) { const int x = sp[v][col0 + c]; code[v] = x < 4 ? x : kFlagSubject; }
-                sc[c] = AR::codes(code[0], code[1]);
+                sc[c] = AR::subj(code[0], code[1], prm.match - prm.mismatch);
                 const int h0 = edge_h(GLOBAL_EDGES, col0 + c + 1, alpha, beta);
                 T[c] = AR::splat(GAP == GAP_EXACT ? kNeg32 : h0);  // exact model: T[] unused, EP holds E - beta
                 HM[c] = AR::splat(h0 + mism);
@@ -298,7 +311,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const ScoreParams prm) 
 #pragma unroll
                             for (int v = 0; v < NV; ++v)
                                 if (row < m[v]) { const int code = qp[v][row]; c[v] = code < 4 ? code : kFlagQuery; }
-                            qring[gib][row & (kQRing - 1)] = AR::codes(c[0], c[1]);
+                            qring[gib][row & (kQRing - 1)] = AR::query(c[0], c[1]);
                         }
                         __syncwarp();
                     }

@@ -488,8 +488,8 @@ struct Shape { int P, K; };
 // (2 instead of 4 resident blocks per SM), so it is only reachable through WSB_FORCE_SHAPE=3.
 static const Shape kShapesF16[] = {{4, 16}, {8, 19}, {8, 32}, {4, 38}, {16, 16}};
 // int32 shapes: narrow groups for short reads, full warps with wide stages for long reads
-static const Shape kShapesI32[] = {{8, 16}, {16, 16}, {32, 16}};
-constexpr int kNumShapesF16 = 3, kNumShapesI32 = 3;  // shapes the planner may choose
+static const Shape kShapesI32[] = {{8, 16}, {16, 16}, {32, 16}, {8, 19}};
+constexpr int kNumShapesF16 = 3, kNumShapesI32 = 4;  // shapes the planner may choose
 constexpr int kNumShapes = 5;  // bucket array bound
 
 static double padded_cost(const Shape& s, int m, int n) {
@@ -517,7 +517,7 @@ template <class AR, int P, int K, int GAP> static KernelSel pick_atype(int atype
     switch (atype) {
         case AT_GLOBAL: return {score_kernel<AR, P, K, AT_GLOBAL, GAP>, score_smem_bytes<AR, P, K, AT_GLOBAL>()};
         case AT_LOCAL:
-            if constexpr (std::is_same<AR, ArI32>::value) {
+            if constexpr (!std::is_same<AR, ArF16>::value) {
                 if (masked) return {score_kernel<AR, P, K, AT_LOCAL, GAP, true>, score_smem_bytes<AR, P, K, AT_LOCAL>()};
             }
             return {score_kernel<AR, P, K, AT_LOCAL, GAP>, score_smem_bytes<AR, P, K, AT_LOCAL>()};
@@ -528,7 +528,7 @@ template <class AR, int P, int K, int GAP> static KernelSel pick_atype(int atype
 template <class AR, int P, int K> static KernelSel pick_gap(int atype, int gap, bool masked) {
     if (gap == GAP_LINEAR) return pick_atype<AR, P, K, GAP_LINEAR>(atype, masked);
     if (gap == GAP_MERGED) return pick_atype<AR, P, K, GAP_MERGED>(atype, masked);
-    if constexpr (std::is_same<AR, ArI32>::value) return pick_atype<ArI32, P, K, GAP_EXACT>(atype, masked);
+    if constexpr (!std::is_same<AR, ArF16>::value) return pick_atype<AR, P, K, GAP_EXACT>(atype, masked);
     return {nullptr, 0};  // the packed kernels have no exact three-state model
 }
 
@@ -552,7 +552,7 @@ static LongFn pick_long(int atype, int gap) {
 }
 
 // short_ok: every unit of the launch fits one stage and the short kernel's query buffer
-static KernelSel pick_kernel(int variant, int shape, int atype, int gap, bool masked, bool short_ok) {
+static KernelSel pick_kernel(int variant, int shape, int atype, int gap, bool masked, bool short_ok, bool wide) {
     static const char* no_short = getenv("WSB_NO_SHORT");  // tuning aid: force the general kernel
     if (variant == WSB_VARIANT_F16X2 && atype == AT_LOCAL && short_ok && !(no_short && no_short[0])) {
         switch (shape) {
@@ -572,10 +572,12 @@ static KernelSel pick_kernel(int variant, int shape, int atype, int gap, bool ma
             default: return pick_gap<ArF16, 16, 16>(atype, gap, masked);
         }
     }
+    if (wide) return pick_gap<ArI32W, 8, 16>(atype, gap, masked);  // |match - mismatch| > 127: compare/select kernel
     switch (shape) {
         case 0: return pick_gap<ArI32, 8, 16>(atype, gap, masked);
         case 1: return pick_gap<ArI32, 16, 16>(atype, gap, masked);
-        default: return pick_gap<ArI32, 32, 16>(atype, gap, masked);
+        case 2: return pick_gap<ArI32, 32, 16>(atype, gap, masked);
+        default: return pick_gap<ArI32, 8, 19>(atype, gap, masked);
     }
 }
 
@@ -593,6 +595,7 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
     const int gap_i32 = !affine ? GAP_LINEAR : (wsb_merged_state_exact(sch) ? GAP_MERGED : GAP_EXACT);
     const int gap_f16 = !affine ? GAP_LINEAR : GAP_MERGED;
     const int ms = max_step(sch);
+    const bool wide_scheme = std::abs(sch->match - sch->mismatch) > 127;
     plan.status.assign((size_t)np, 0);
 
     if (variant == WSB_VARIANT_F16X2 && !merged_ok) return WSB_E_SCHEME;
@@ -604,7 +607,7 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
         const bool fits = f16_scheme_ok && wsb_f16_range_ok(sch, m, n);
         if (variant == WSB_VARIANT_F16X2 && !fits) { status = WSB_E_RANGE; return; }
         if (variant != WSB_VARIANT_I32 && fits) { var = WSB_VARIANT_F16X2; shape = best_shape(kShapesF16, kNumShapesF16, 5, m, n); }
-        else { var = WSB_VARIANT_I32; shape = best_shape(kShapesI32, kNumShapesI32, 3, m, n); }
+        else { var = WSB_VARIANT_I32; shape = wide_scheme ? 0 : best_shape(kShapesI32, kNumShapesI32, 4, m, n); }
     };
     // The long-read kernel (score_long.cuh) takes the int32 pairs that would otherwise run full-warp stages: it needs
     // byte-sized substitution scores, the merged (or linear) gap state and, for local alignment, non-improving pads.
@@ -613,9 +616,13 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
                                 std::abs(sch->mismatch) <= 127 && (atype != AT_LOCAL || (sch->mismatch <= 0 && sch->match >= 0));
     auto long_ok = [&](int var, int shape, int m, int n) {
         (void)shape;
-        static const char* thr = getenv("WSB_LONG_MIN_N");  // tuning aid
-        const int min_n = thr && thr[0] ? atoi(thr) : 512;
-        return long_scheme_ok && var == WSB_VARIANT_I32 && m >= 64 && n > min_n;
+        if (!long_scheme_ok || var != WSB_VARIANT_I32 || m < 64) return false;
+        static const char* thr = getenv("WSB_LONG_MIN_N");  // tuning aid: take everything wider than this
+        if (thr && thr[0]) return n > atoi(thr);
+        // 512-column stages: below ~2 kbp the narrow lane groups of score_kernel win unless the width fits well
+        // (measured crossover, tools/len_sweep.py)
+        const int64_t padded = (int64_t)((n + kLongW - 1) / kLongW) * kLongW;
+        return n > 2048 || (n > 512 && padded * 100 <= (int64_t)n * 115);
     };
 
     if (b->uniform) {
@@ -792,7 +799,8 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
         }
         const Shape sh = g.variant == WSB_VARIANT_F16X2 ? kShapesF16[g.shape] : kShapesI32[g.shape];
         const bool short_ok = g.max_n <= sh.P * sh.K && g.max_m <= kShortQRows - 4 * sh.P - 2;
-        const KernelSel sel = pick_kernel(g.variant, g.shape, atype, g.gap, sch->mismatch > 0 || sch->match < 0, short_ok);
+        const KernelSel sel = pick_kernel(g.variant, g.shape, atype, g.gap, sch->mismatch > 0 || sch->match < 0, short_ok,
+                                          std::abs(sch->match - sch->mismatch) > 127);
         KernelFn fn = sel.fn;
         if (!fn) return WSB_E_SCHEME;
         CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel.smem));

@@ -167,3 +167,16 @@ def test_long_reads_with_non_merged_scheme_use_exact_model(ctx):
     pairs = [(i, i) for i in range(len(qs))]
     for at in ("global", "local", "semiglobal"):
         assert_scores_equal(gpu_scores(ctx, qs, ss, pairs, scheme, at), oracle_scores(qs, ss, pairs, scheme, at), at)
+
+
+@pytest.mark.parametrize("align_type", ["global", "local", "semiglobal"])
+def test_wide_substitution_scores_use_compare_select_kernel(ctx, align_type):
+    """|match - mismatch| > 127 does not fit the byte profile of the dp4a kernels: the planner falls back to ArI32W."""
+    rng = np.random.default_rng(79)
+    scheme = scheme_of((100, -90, 120, 10), "affine")
+    qs, ss, pairs = _random_batch(rng, 60, 1, 700, flagged=0.2)
+    assert_scores_equal(gpu_scores(ctx, qs, ss, pairs, scheme, align_type), oracle_scores(qs, ss, pairs, scheme, align_type),
+                        f"wide {align_type}")
+    lin = scheme_of((90, -80, 100, 100), "linear")
+    assert_scores_equal(gpu_scores(ctx, qs, ss, pairs, lin, align_type), oracle_scores(qs, ss, pairs, lin, align_type),
+                        f"wide linear {align_type}")
