@@ -7,11 +7,13 @@
 #include <cub/device/device_scan.cuh>
 
 struct TbShape { int P, K; };
-static const TbShape kTbShapes[] = {{8, 16}, {8, 32}, {32, 16}};
+static const TbShape kTbShapes[] = {{8, 16}, {8, 32}, {32, 16}, {16, 16}};
 
 static int tb_pick_shape(int max_n) {
+    static const char* force = getenv("WSB_TB_SHAPE");  // tuning aid
+    if (force && force[0]) return std::min(3, std::max(0, atoi(force)));
     if (max_n <= 128) return 0;
-    if (max_n <= 256) return 1;
+    if (max_n <= 256) return 1;   // (8,32); (16,16) = index 3 doubles the resident warps but measured 2 % slower at 250 bp
     return 2;
 }
 
@@ -71,7 +73,8 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
     const int shape = tb_pick_shape(max_n);
     const int P = kTbShapes[shape].P, K = kTbShapes[shape].K;
     TbFillFn fill = shape == 0 ? tb_pick_fill<8, 16>(atype, affine)
-                  : shape == 1 ? tb_pick_fill<8, 32>(atype, affine) : tb_pick_fill<32, 16>(atype, affine);
+                  : shape == 1 ? tb_pick_fill<8, 32>(atype, affine)
+                  : shape == 2 ? tb_pick_fill<32, 16>(atype, affine) : tb_pick_fill<16, 16>(atype, affine);
     size_t budget_words = (size_t)16384 << 18;  // 16 GiB in 32-bit words (a B200 carries 180 GB)
     if (const char* e = getenv("WSB_TB_SCRATCH_MB")) { const long mb = atol(e); if (mb > 0) budget_words = (size_t)mb << 18; }
 
@@ -170,7 +173,7 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
         prm.end_i = b->d_i; prm.end_j = b->d_j; prm.start_i = tb.d_qs; prm.start_j = tb.d_ss;
         prm.w_score = b->d_score; prm.w_i = b->d_i; prm.w_j = b->d_j;
         prm.n_runs = d_cnt; prm.run_off = d_chunk_off; prm.runs = nullptr;
-        prm.tb_p = P; prm.tb_k = K;
+        prm.tb_p = P; prm.tb_k = K; prm.one = 1;
 
         TB_TRY(cudaEventRecord(e0, ctx->stream));
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((count + gpb - 1) / gpb, max_grid));

@@ -44,6 +44,7 @@ struct TbParams {
     const int64_t* run_off;                       // exclusive prefix of n_runs, relative to the launch
     uint32_t* runs;                               // out (pass 2): runs of the launch, forward order
     int32_t tb_p, tb_k;                           // lane-group shape the codes were written with
+    int32_t one;                                  // 1, opaque to the compiler (keeps plane-bit adds on the FMA pipe)
 };
 
 // code block geometry shared by fill and walk
@@ -54,13 +55,15 @@ __host__ __device__ inline int64_t tb_code_words(int m, int n, int P, int K) {
 }
 
 // max(a, b) with "a wins ties", and the plane bit added to w when a wins: compare, select, predicated add
-__device__ __forceinline__ int max_mark(int a, int b, uint32_t& w, uint32_t bit) {
+// (the add is written as bit * one + w with one == 1 at run time, so that it issues on the FMA pipe as IMAD: compare
+// and select already fill the ALU pipe)
+__device__ __forceinline__ int max_mark(int a, int b, uint32_t& w, uint32_t bit, int one) {
     int r;
     asm("{\n\t.reg .pred p;\n\t"
         "setp.ge.s32 p, %2, %3;\n\t"
         "selp.s32 %0, %2, %3, p;\n\t"
-        "@p add.u32 %1, %1, %4;\n\t"
-        "}" : "=r"(r), "+r"(w) : "r"(a), "r"(b), "r"(bit));
+        "@p mad.lo.u32 %1, %5, %4, %1;\n\t"
+        "}" : "=r"(r), "+r"(w) : "r"(a), "r"(b), "r"(bit), "r"(one));
     return r;
 }
 
@@ -79,7 +82,7 @@ __global__ void __launch_bounds__(kThreads) tb_fill_kernel(const TbParams prm) {
     const int64_t group_global = (int64_t)blockIdx.x * GPB + gib;
     const int64_t n_groups = (int64_t)gridDim.x * GPB;
     int2* bnd = prm.bnd ? prm.bnd + group_global * prm.bnd_rows : nullptr;
-    const int alpha = prm.alpha, beta = prm.beta, mism = prm.mismatch;
+    const int alpha = prm.alpha, beta = prm.beta, mism = prm.mismatch, one = prm.one;
     // profile bytes hold sigma + alpha, so that the diagonal candidate comes straight from the stored H - alpha
     const unsigned miss4 = (unsigned)((mism + alpha) & 0xff) * 0x01010101u;
     const unsigned hit = (unsigned)((prm.match + alpha) & 0xff);
@@ -186,14 +189,14 @@ __global__ void __launch_bounds__(kThreads) tb_fill_kernel(const TbParams prm) {
                                 } else {
                                     int e, f;
                                     if (AFFINE) {
-                                        e = max_mark(EP[c], AL[c], we, 1u << (16 + c8));
-                                        f = max_mark(fl, al, wf, 1u << (24 + c8));
+                                        e = max_mark(EP[c], AL[c], we, 1u << (16 + c8), one);
+                                        f = max_mark(fl, al, wf, 1u << (24 + c8), one);
                                         EP[c] = e - beta; fl = f - beta;
                                     } else {
                                         e = AL[c]; f = al;
                                     }
-                                    const int m1 = max_mark(d, e, wd, 1u << c8);
-                                    h = max_mark(m1, f, wm, 1u << (8 + c8));
+                                    const int m1 = max_mark(d, e, wd, 1u << c8, one);
+                                    h = max_mark(m1, f, wm, 1u << (8 + c8), one);
                                 }
                                 al = h - alpha;
                                 AL[c] = al;
