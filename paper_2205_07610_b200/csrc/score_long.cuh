@@ -24,6 +24,7 @@
 #pragma once
 #include "score_kernels.cuh"
 
+#include <cooperative_groups.h>
 #include <type_traits>
 
 namespace wsb {
@@ -43,6 +44,7 @@ struct LongParams {
     int2* bnd;             // per block: (NW + 1) border columns of bnd_rows entries {T - gamma, H}
     int64_t bnd_rows;
     unsigned int* queue;   // work queue head, zeroed before the launch
+    int32_t* cflags;       // cluster launches: per cluster 160 ints (progress counters of its warps, unit slot, reduction slots)
     int32_t one;           // 1, opaque to the compiler: keeps selected adds on the FMA pipe as IMAD
 };
 
@@ -58,7 +60,7 @@ __device__ __forceinline__ int fma_add(int a, int one, int b) {
     return d;
 }
 
-template <int ATYPE, int GAP>
+template <int ATYPE, int GAP, bool CLUSTER = false>
 __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long_kernel(const LongParams prm) {
     constexpr int K = kLongK, W = kLongW;
     constexpr bool LOCAL = ATYPE == AT_LOCAL;
@@ -67,26 +69,50 @@ __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long_kernel(const Lo
     constexpr bool MERGED = GAP == GAP_MERGED;
     static_assert(GAP == GAP_LINEAR || GAP == GAP_MERGED, "the exact three-state model stays in score_kernel");
 
-    __shared__ int s_prog[kLongMaxWarps];           // border rows published by each warp, summed over its stages
+    __shared__ int s_prog[kLongMaxWarps + 1];       // border rows published per stage slot: generation * (m + 1) + rows
+    __shared__ int s_next;                          // next stage of the current pair to hand out
     __shared__ int s_unit;
     __shared__ int s_red[kLongMaxWarps][3];
     __shared__ int4 s_in[kLongMaxWarps][64];        // two chunks of 32 rows of lane-0 inputs per warp: {T - gamma, H, selector}
 
+    // A pair is spread over the GW = CS * NW warps of a thread-block cluster (CS = 1 for ordinary launches).  With
+    // CS > 1 the progress counters and the stage counter live in global memory (release / acquire at gpu scope); the
+    // border columns are global anyway.
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int CS = CLUSTER ? (int)cluster.num_blocks() : 1;      // CLUSTER = false: compile-time 1, no cluster code at all
+    const int crank = CLUSTER ? (int)cluster.block_rank() : 0;
     const int NW = blockDim.x >> 5;
+    const int GW = CS * NW;
     const int w = threadIdx.x >> 5;
     const int t = threadIdx.x & 31;
     const int alpha = prm.alpha, beta = prm.beta, mism = prm.mismatch, one = prm.one;
     const int gamma = MERGED ? min(alpha, beta) : alpha;
     const int nalpha = -alpha, ngamma = -gamma;
     const unsigned mism4 = (unsigned)(mism & 0xff) * 0x01010101u;
-    int2* const bnd_block = prm.bnd + (int64_t)blockIdx.x * (NW + 1) * prm.bnd_rows;
-    volatile int* prog = s_prog;
+    const int64_t cluster_id = blockIdx.x / CS;
+    int2* const bnd_block = prm.bnd + cluster_id * (GW + 1) * prm.bnd_rows;
+    int32_t* const cf = CS > 1 ? prm.cflags + cluster_id * 160 : nullptr;   // [0..128] progress, [129] next stage, [130] unit, [132..155] reduction
+    volatile int* prog = CS > 1 ? cf : s_prog;
+    int* const next_stage = CS > 1 ? cf + 129 : &s_next;
 
     for (;;) {
-        __syncthreads();  // previous pair fully retired (progress counters, reduction slots)
-        if (threadIdx.x == 0) s_unit = (int)atomicAdd(prm.queue, 1u);
-        if (threadIdx.x < kLongMaxWarps) s_prog[threadIdx.x] = 0;
-        __syncthreads();
+        // previous pair fully retired (progress counters, reduction slots), next unit fetched by one thread
+        if (CS > 1) {
+            cluster.sync();
+            if (crank == 0 && threadIdx.x == 0) cf[130] = (int)atomicAdd(prm.queue, 1u);
+            if (crank == 0 && threadIdx.x < 130) cf[threadIdx.x] = 0;
+            __threadfence();
+            cluster.sync();
+            if (threadIdx.x == 0) s_unit = *(volatile int*)(cf + 130);
+            __syncthreads();
+        } else {
+            __syncthreads();
+            if (threadIdx.x == 0) s_unit = (int)atomicAdd(prm.queue, 1u);
+            if (threadIdx.x <= kLongMaxWarps) s_prog[threadIdx.x] = 0;
+            if (threadIdx.x == 0) s_next = 0;
+            __syncthreads();
+        }
         const int64_t u = s_unit;
         if (u >= prm.n_units) break;
         const int p = prm.units[u];
@@ -98,8 +124,18 @@ __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long_kernel(const Lo
 
         int best_v = GLOBAL_EDGES ? kNeg32 : 0, best_i = 0, best_j = SEMI ? n : 0;
 
-        int k_local = 0;
-        for (int st = w; st < nstages; st += NW, ++k_local) {
+        // Stages are handed out in order to whichever warp is free (atomic counter): the GW warps stay busy until the
+        // pair runs out of stages, whatever the stage count.  Stage st writes border column st mod (GW + 1); when it is
+        // handed out, stages <= st - GW have finished, so that column's previous reader is done.
+#ifdef WSB_LONG_STATIC
+        for (int st = crank * NW + w; st < nstages; st += GW) {
+#else
+        for (;;) {
+            int st = 0;
+            if (t == 0) st = atomicAdd(next_stage, 1);
+            st = __shfl_sync(0xffffffffu, st, 0);
+            if (st >= nstages) break;
+#endif
             const bool first = st == 0, last = st + 1 == nstages;
             const int col0 = st * W + t * K;  // this strip holds matrix columns col0+1 .. col0+K
             unsigned prof[K];
@@ -122,10 +158,12 @@ __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long_kernel(const Lo
             unsigned sel = 0u;                      // that row's query symbol, one-hot in bytes (0 = flagged)
             int edge = edge_h(GLOBAL_EDGES, 1, alpha, beta);   // stage 0: H(r, 0) of lane 0's current row
             // incoming border column (stage st - 1) and its producer
-            const int2* in_col = bnd_block + (int64_t)((st + NW) % (NW + 1)) * prm.bnd_rows;   // (st - 1) mod (NW + 1)
-            int2* out_ptr = bnd_block + (int64_t)(st % (NW + 1)) * prm.bnd_rows - 31;  // lane 31 at iteration it: row it - 31 -> slot it - 32 (it starts at 1)
-            const int pw_id = (w + NW - 1) % NW;
-            const int p_base = (w == 0 ? k_local - 1 : k_local) * m;  // producer's published rows before its stage
+            const int2* in_col = bnd_block + (int64_t)((st + GW) % (GW + 1)) * prm.bnd_rows;   // (st - 1) mod (GW + 1)
+            int2* out_ptr = bnd_block + (int64_t)(st % (GW + 1)) * prm.bnd_rows - 31;  // lane 31 at iteration it: row it - 31 -> slot it - 32 (it starts at 1)
+            const int pw_id = (st + GW) % (GW + 1);                    // progress slot of stage st - 1
+            const int p_base = st > 0 ? (st - 1) / (GW + 1) * (m + 1) : 0;   // its generation offset
+            const int out_slot = st % (GW + 1);
+            const int out_base = st / (GW + 1) * (m + 1);
             const bool do_out = t == 31 && !last;
             const int cap_rel = n - 1 - col0;  // register index of matrix column n, if inside this strip
             const bool has_cap = last && cap_rel >= 0 && cap_rel < K;
@@ -142,7 +180,7 @@ __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long_kernel(const Lo
                 if (!first) {
                     const int need = p_base + min(m, row0 + 32);
                     while (prog[pw_id] < need) __nanosleep(40);
-                    __threadfence_block();
+                    if (CS > 1) __threadfence(); else __threadfence_block();
                     pre = __ldcg(in_col + row0 + t);
                 }
             };
@@ -229,8 +267,8 @@ __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long_kernel(const Lo
                     for (int it = it0; it <= it1; ++it) iteration(it, std::true_type{});
                 }
                 if (do_out) {  // publish the border rows lane 31 has completed
-                    __threadfence_block();
-                    prog[w] = k_local * m + min(max(it1 - 31, 0), m);
+                    if (CS > 1) __threadfence(); else __threadfence_block();
+                    prog[out_slot] = out_base + min(max(it1 - 31, 0), m);
                 }
             }
             // rows are complete: every lane's registers hold row m of its strip
@@ -261,8 +299,22 @@ __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long_kernel(const Lo
                 if (better_cell(s_red[x][0], s_red[x][1], s_red[x][2], bv, bi, bj)) {
                     bv = s_red[x][0]; bi = s_red[x][1]; bj = s_red[x][2];
                 }
-            if (LOCAL && bv <= 0) { bv = 0; bi = 0; bj = 0; }
-            prm.out_score[p] = bv; prm.out_i[p] = bi; prm.out_j[p] = bj;
+            if (CS > 1) { cf[132 + 3 * crank] = bv; cf[133 + 3 * crank] = bi; cf[134 + 3 * crank] = bj; __threadfence(); }
+            else {
+                if (LOCAL && bv <= 0) { bv = 0; bi = 0; bj = 0; }
+                prm.out_score[p] = bv; prm.out_i[p] = bi; prm.out_j[p] = bj;
+            }
+        }
+        if (CS > 1) {
+            cluster.sync();
+            if (crank == 0 && threadIdx.x == 0) {
+                volatile int* r = cf + 132;
+                int bv = r[0], bi = r[1], bj = r[2];
+                for (int x = 1; x < CS; ++x)
+                    if (better_cell(r[3 * x], r[3 * x + 1], r[3 * x + 2], bv, bi, bj)) { bv = r[3 * x]; bi = r[3 * x + 1]; bj = r[3 * x + 2]; }
+                if (LOCAL && bv <= 0) { bv = 0; bi = 0; bj = 0; }
+                prm.out_score[p] = bv; prm.out_i[p] = bi; prm.out_j[p] = bj;
+            }
         }
     }
 }

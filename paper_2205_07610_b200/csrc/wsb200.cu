@@ -36,6 +36,7 @@ struct wsb_ctx {
     cudaStream_t aux[kAux] = {};
     cudaEvent_t aux_done[kAux] = {};
     unsigned int* d_queues = nullptr;  // work-queue heads of the long-read launches
+    int32_t* d_cflags = nullptr;       // cluster launches of the long-read kernel: 160 ints per cluster
     std::string last_error;
     // Device-memory cache: batches come and go with every run_batch call, and cudaMalloc/cudaFree of GB-sized pools
     // cost tens of milliseconds each, so freed blocks are kept (size-bucketed, 2 MiB granularity) and reused.
@@ -80,7 +81,8 @@ struct LaunchGroup {  // pairs that run in one kernel launch
     int64_t n_units = 0;
     int64_t unit_off = 0;  // offset (in int32) into the plan's unit array; -1 = identity mapping
     int max_m = 0, max_n = 0;
-    int long_nw = 0;       // > 0: long-read kernel with this many warps per pair (score_long.cuh)
+    int long_nw = 0;       // > 0: long-read kernel with this many warps per block (score_long.cuh)
+    int cluster = 1;       // long-read kernel: thread blocks per pair (a cluster of 2, 4 or 8 for the giants of a batch)
 };
 
 struct Plan {
@@ -218,7 +220,9 @@ extern "C" int wsb_ctx_create(int device, wsb_ctx** out) {
         delete c;
         return WSB_E_CUDA;
     }
-    bool ok = cudaMalloc((void**)&c->d_queues, 64 * sizeof(unsigned int)) == cudaSuccess;
+    bool ok = cudaMalloc((void**)&c->d_queues, 64 * sizeof(unsigned int)) == cudaSuccess &&
+              cudaMalloc((void**)&c->d_cflags, 1024 * 160 * sizeof(int32_t)) == cudaSuccess &&
+              cudaMemset(c->d_cflags, 0, 1024 * 160 * sizeof(int32_t)) == cudaSuccess;
     for (int k = 0; k < wsb_ctx::kAux && ok; ++k)
         ok = cudaStreamCreateWithFlags(&c->aux[k], cudaStreamNonBlocking) == cudaSuccess &&
              cudaEventCreateWithFlags(&c->aux_done[k], cudaEventDisableTiming) == cudaSuccess;
@@ -238,6 +242,7 @@ extern "C" void wsb_ctx_destroy(wsb_ctx* c) {
         if (c->aux_done[k]) cudaEventDestroy(c->aux_done[k]);
     }
     if (c->d_queues) cudaFree(c->d_queues);
+    if (c->d_cflags) cudaFree(c->d_cflags);
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     delete c;
@@ -538,16 +543,16 @@ template <int P, int K> static KernelSel pick_short(int gap) {
 }
 
 using LongFn = void (*)(const LongParams);
-template <int GAP> static LongFn pick_long_atype(int atype) {
+template <int GAP, bool CLUSTER> static LongFn pick_long_atype(int atype) {
     switch (atype) {
-        case AT_GLOBAL: return score_long_kernel<AT_GLOBAL, GAP>;
-        case AT_LOCAL: return score_long_kernel<AT_LOCAL, GAP>;
-        default: return score_long_kernel<AT_SEMI, GAP>;
+        case AT_GLOBAL: return score_long_kernel<AT_GLOBAL, GAP, CLUSTER>;
+        case AT_LOCAL: return score_long_kernel<AT_LOCAL, GAP, CLUSTER>;
+        default: return score_long_kernel<AT_SEMI, GAP, CLUSTER>;
     }
 }
-static LongFn pick_long(int atype, int gap) {
-    if (gap == GAP_LINEAR) return pick_long_atype<GAP_LINEAR>(atype);
-    if (gap == GAP_MERGED) return pick_long_atype<GAP_MERGED>(atype);
+static LongFn pick_long(int atype, int gap, bool cluster) {
+    if (gap == GAP_LINEAR) return cluster ? pick_long_atype<GAP_LINEAR, true>(atype) : pick_long_atype<GAP_LINEAR, false>(atype);
+    if (gap == GAP_MERGED) return cluster ? pick_long_atype<GAP_MERGED, true>(atype) : pick_long_atype<GAP_MERGED, false>(atype);
     return nullptr;
 }
 
@@ -666,30 +671,42 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
     // giants of a skewed batch get up to 16 warps), beyond that the cheapest count in warp-iterations wins (pipeline
     // fill of ~80 rows per extra warp, idle warps when the stage count is not a multiple).
     if (!long_pairs.empty()) {
-        std::vector<int64_t> by_nw[kLongMaxWarps + 1];
+        // class index = log2(warps per pair): 0..4 -> 1..16 warps in one block, 5..7 -> clusters of 2, 4, 8 blocks x 16 warps
+        std::vector<int64_t> by_class[8];
         const double machine_warps = (double)ctx->sm_count * 20.0;
         const double makespan = std::max(long_iters / machine_warps, 1.0);
+        static const char* no_cluster = getenv("WSB_NO_CLUSTER");  // tuning aid
+        const int max_class = (no_cluster && no_cluster[0]) ? 4 : 7;
         for (int64_t p : long_pairs) {
             const int stages = (b->n[p] + kLongW - 1) / kLongW;
             const double t1 = (double)stages * (b->m[p] + 31);
-            // warps per pair come from {1, 2, 4, 8, 16}: blocks then spread evenly over the four schedulers of an SM
-            int lo = 1;
-            while (lo < kLongMaxWarps && lo < stages && t1 / lo > 0.25 * makespan) lo *= 2;
-            int best_nw = lo;
+            // warps per pair come from powers of two: blocks then spread evenly over the four schedulers of an SM
+            // ... but a cluster only up to about twice the pair's proportional share of the machine, or a few giants that
+            // dominate the batch would queue behind each other in half-idle clusters
+            const double share_cap = std::max(1.0, 2.0 * t1 / std::max(long_iters, 1.0) * machine_warps);
+            int lo = 0;
+            while (lo < max_class && (2 << lo) <= stages && (lo < 4 || (double)(2 << lo) <= share_cap) &&
+                   t1 / (1 << lo) > 0.25 * makespan) ++lo;
+            int best = lo;
             double best_cost = 1e300;
-            for (int nw = lo; nw <= std::min(kLongMaxWarps, 2 * lo); nw *= 2) {
+            for (int c = lo; c <= std::min(lo + 1, std::min(max_class, 4)); ++c) {   // one block: also weigh the next size up
+                const int nw = 1 << c;
+                if (nw > stages) break;
                 const double rounds = (double)((stages + nw - 1) / nw);
                 const double cost = nw * (rounds * (b->m[p] + 31) + (nw - 1) * 100.0);
-                if (cost < best_cost * 0.999) { best_cost = cost; best_nw = nw; }
+                if (cost < best_cost * 0.999) { best_cost = cost; best = c; }
             }
-            by_nw[best_nw].push_back(p);
+            if (lo > 4) best = lo;
+            by_class[best].push_back(p);
         }
-        for (int nw = kLongMaxWarps; nw >= 1; --nw) {
-            auto& v = by_nw[nw];
+        for (int c = 7; c >= 0; --c) {
+            auto& v = by_class[c];
             if (v.empty()) continue;
             std::stable_sort(v.begin(), v.end(), by_work);
             LaunchGroup g;
-            g.variant = WSB_VARIANT_I32; g.shape = 2; g.gap = gap_i32; g.long_nw = nw;
+            g.variant = WSB_VARIANT_I32; g.shape = 2; g.gap = gap_i32;
+            g.long_nw = c <= 4 ? 1 << c : kLongMaxWarps;
+            g.cluster = c <= 4 ? 1 : 1 << (c - 4);
             g.unit_off = (int64_t)units.size();
             g.n_units = (int64_t)v.size();
             for (int64_t p : v) {
@@ -786,15 +803,30 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
     size_t bnd_need = 0;
     for (const LaunchGroup& g : plan.groups) {
         if (g.long_nw > 0) {
-            LongFn lfn = pick_long(atype, g.gap);
+            LongFn lfn = pick_long(atype, g.gap, g.cluster > 1);
             if (!lfn) return WSB_E_SCHEME;
-            int per_sm = 0;
-            CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lfn, g.long_nw * 32, 0));
-            per_sm = std::max(per_sm, 1);
-            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(g.n_units, (int64_t)ctx->sm_count * per_sm));
+            int grid = 1;
+            if (g.cluster > 1) {  // one pair per cluster: as many clusters as the device can co-schedule
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3((unsigned)(g.cluster * std::min<int64_t>(g.n_units, 1024)));
+                cfg.blockDim = dim3((unsigned)(g.long_nw * 32));
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeClusterDimension;
+                at[0].val.clusterDim.x = (unsigned)g.cluster; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+                cfg.attrs = at; cfg.numAttrs = 1;
+                int max_clusters = 0;
+                CUDA_TRY(ctx, cudaOccupancyMaxActiveClusters(&max_clusters, lfn, &cfg));
+                max_clusters = std::max(1, std::min(max_clusters, 256));   // three cluster classes share 1024 flag blocks
+                grid = g.cluster * (int)std::min<int64_t>(g.n_units, max_clusters);
+            } else {
+                int per_sm = 0;
+                CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lfn, g.long_nw * 32, 0));
+                per_sm = std::max(per_sm, 1);
+                grid = (int)std::max<int64_t>(1, std::min<int64_t>(g.n_units, (int64_t)ctx->sm_count * per_sm));
+            }
             const int64_t rows = ((int64_t)g.max_m + 31) / 32 * 32 + 64;
             geo.push_back({nullptr, lfn, 0, grid, rows, bnd_need});
-            bnd_need += (size_t)rows * sizeof(int2) * (size_t)(g.long_nw + 1) * (size_t)grid;
+            bnd_need += (size_t)rows * sizeof(int2) * (size_t)(g.long_nw * g.cluster + 1) * (size_t)(grid / g.cluster);
             continue;
         }
         const Shape sh = g.variant == WSB_VARIANT_F16X2 ? kShapesF16[g.shape] : kShapesI32[g.shape];
@@ -846,7 +878,19 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
             lp.match = sch->match; lp.mismatch = sch->mismatch; lp.alpha = sch->gap_open; lp.beta = beta_eff;
             lp.bnd = reinterpret_cast<int2*>((char*)b->d_bnd + geo[k].bnd_off); lp.bnd_rows = geo[k].bnd_rows;
             lp.queue = ctx->d_queues + k; lp.one = 1;
-            geo[k].lfn<<<geo[k].grid, g.long_nw * 32, 0, ctx->aux[a]>>>(lp);
+            lp.cflags = ctx->d_cflags + (size_t)256 * 160 * (size_t)(g.cluster == 2 ? 0 : g.cluster == 4 ? 1 : 2);
+            if (g.cluster > 1) {
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3((unsigned)geo[k].grid); cfg.blockDim = dim3((unsigned)(g.long_nw * 32));
+                cfg.dynamicSmemBytes = 0; cfg.stream = ctx->aux[a];
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeClusterDimension;
+                at[0].val.clusterDim.x = (unsigned)g.cluster; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+                cfg.attrs = at; cfg.numAttrs = 1;
+                CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, geo[k].lfn, lp));
+            } else {
+                geo[k].lfn<<<geo[k].grid, g.long_nw * 32, 0, ctx->aux[a]>>>(lp);
+            }
             CUDA_TRY(ctx, cudaGetLastError());
             ++launches;
             continue;

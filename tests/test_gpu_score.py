@@ -180,3 +180,24 @@ def test_wide_substitution_scores_use_compare_select_kernel(ctx, align_type):
     lin = scheme_of((90, -80, 100, 100), "linear")
     assert_scores_equal(gpu_scores(ctx, qs, ss, pairs, lin, align_type), oracle_scores(qs, ss, pairs, lin, align_type),
                         f"wide linear {align_type}")
+
+
+@pytest.mark.parametrize("align_type", ["global", "local", "semiglobal"])
+def test_long_read_kernel_cluster_classes(ctx, align_type):
+    """A batch whose largest pairs dwarf the rest: the planner gives them whole thread-block clusters (2, 4, 8 blocks of
+    16 warps), with progress counters in global memory."""
+    rng = np.random.default_rng(4242)
+    scheme = scheme_of((2, -1, 2, 1), "affine")
+    shapes = [(1500, 70000), (2500, 40000), (3000, 20000), (1200, 9000), (900, 5000), (700, 2500)]
+    shapes += [(300, 600)] * 6
+    qs, ss = [], []
+    for m, n in shapes:
+        q = random_codes(rng, m)
+        s = random_codes(rng, n)
+        at = int(rng.integers(0, n - m))
+        s[at:at + m] = mutate_codes(rng, q, 0.05, 0.0, 0.0)[:m]   # a diagonal band worth finding
+        qs.append(q); ss.append(s)
+    pairs = [(i, i) for i in range(len(qs))]
+    want = oracle_scores(qs, ss, pairs, scheme, align_type)
+    got = gpu_scores(ctx, qs, ss, pairs, scheme, align_type, "auto")
+    assert_scores_equal(got, want, f"cluster {align_type}")
