@@ -191,3 +191,23 @@ def test_two_rank_sharding_over_gloo(tmp_path):
     mp.spawn(_rank_main, args=(2, port, str(tmp_path)), nprocs=2, join=True)
     imbalance = float(open(tmp_path / "ok").read())
     assert 1.0 <= imbalance < 1.6   # the skewed law has a few 10^10-cell pairs; LPT keeps the max shard near the mean
+
+
+def test_pinned_result_buffers_fall_back_to_pageable_memory_without_a_device():
+    from paper_2205_07610_b200 import _native as N
+    a = N.pinned_empty(1000)
+    assert a.shape == (1000,) and a.dtype == np.int32
+    a[:] = 7                      # writable either way
+    assert int(a.sum()) == 7000
+
+
+def test_bench_workload_generators_are_seeded_and_shaped():
+    import bench
+    (qc, qo, ql), (sc, so, sl) = bench.make_pareto(5000, 1)
+    assert ql.min() >= 100 and ql.max() <= 100_000 and sl.min() >= 100 and sl.max() <= 100_000
+    assert len(qc) == int(ql.sum()) and qo[-1] + ql[-1] == len(qc) and qc.max() <= 3
+    (qc2, _, ql2), _ = bench.make_pareto(5000, 1)
+    assert (ql == ql2).all() and (qc == qc2).all()
+    q, s = bench.make_batch(dict(pairs=64, length=250, related=0.5), 3)
+    assert q.shape == s.shape == (64, 250)
+    assert (q[::2] == s[::2]).mean() > 0.5 and (q[1::2] == s[1::2]).mean() < 0.4
