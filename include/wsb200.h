@@ -51,7 +51,12 @@ enum wsb_gap_model { WSB_GAP_LINEAR = 0, WSB_GAP_AFFINE = 1 };
  * exactly representable fp16 integer (|v| <= 2048) and the scheme allows the merged gap state
  * (engine.merged_state_exact, engine.py:71-94), else the int32 kernel.  Forcing F16X2 makes out-of-range pairs fail
  * with WSB_E_RANGE in their status slot (the reference's PackedRangeOverflow, engine.py:530-534). */
-enum wsb_variant { WSB_VARIANT_AUTO = 0, WSB_VARIANT_F16X2 = 1, WSB_VARIANT_I32 = 2 };
+enum wsb_variant { WSB_VARIANT_AUTO = 0, WSB_VARIANT_F16X2 = 1, WSB_VARIANT_I32 = 2, WSB_VARIANT_S16X2 = 3 };
+/* S16X2 (opt-in, experimental): routed like AUTO, but short local alignments (reads that fit one 152-column stage,
+ * scheme within one byte) take the packed int16 DPX kernel of score_short16.cuh instead of the half2 kernel -- two
+ * alignments per thread, exact in 16-bit integers; pairs with a flagged subject symbol are re-scored by the half2
+ * kernel inside the same call.  Results are identical; AUTO does not pick it yet because it is currently slower
+ * (DESIGN.md 4.6). */
 
 enum wsb_status {
     WSB_OK = 0,

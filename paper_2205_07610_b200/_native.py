@@ -14,7 +14,7 @@ _lib = None
 
 ALIGN_TYPE_ID = {"global": 0, "local": 1, "semiglobal": 2}
 GAP_MODEL_ID = {"linear": 0, "affine": 1}
-VARIANT_ID = {"auto": 0, "f16x2": 1, "i32": 2}
+VARIANT_ID = {"auto": 0, "f16x2": 1, "i32": 2, "s16x2": 3}
 
 WSB_OK, WSB_E_CUDA, WSB_E_ARG, WSB_E_NOMEM, WSB_E_LENGTH, WSB_E_RANGE, WSB_E_SCHEME, WSB_E_CAPACITY, WSB_E_NODEVICE = (
     0, -1, -2, -3, -4, -5, -6, -7, -8)

@@ -261,7 +261,10 @@ __global__ void __launch_bounds__(kThreads) f16_local_short_kernel(const ScorePa
     (void)edge_ta; (void)edge_tg; (void)edge_hm;
     const int col0 = t * K;
 
-    const int64_t rounds = (prm.n_units + n_groups - 1) / n_groups;
+    // re-score launch behind the packed int16 kernel: the unit list and its length live on the device
+    const int64_t listed = prm.n_pairs_dev ? (int64_t)*prm.n_pairs_dev : 0;
+    const int64_t n_units = prm.n_pairs_dev ? (listed + 1) / 2 : prm.n_units;
+    const int64_t rounds = (n_units + n_groups - 1) / n_groups;
     for (int64_t rd = 0; rd < rounds; ++rd) {
         const int64_t u = rd * n_groups + group_global;
         int pidx[2], m[2], n[2];
@@ -271,8 +274,9 @@ __global__ void __launch_bounds__(kThreads) f16_local_short_kernel(const ScorePa
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
             int p = -1;
-            if (u < prm.n_units) {
-                if (prm.units) p = prm.units[u * 2 + v];
+            if (u < n_units) {
+                if (prm.n_pairs_dev) p = u * 2 + v < listed ? prm.units[u * 2 + v] : -1;
+                else if (prm.units) p = prm.units[u * 2 + v];
                 else { const int64_t pp = prm.pair_base + u * 2 + v; p = pp < prm.n_pairs ? (int)pp : -1; }
             }
             pidx[v] = p; m[v] = 0; n[v] = 0; qp[v] = nullptr; sp[v] = nullptr;

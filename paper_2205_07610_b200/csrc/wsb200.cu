@@ -4,6 +4,7 @@
 #include "../../include/wsb200.h"
 #include "score_kernels.cuh"
 #include "score_short.cuh"
+#include "score_short16.cuh"
 #include "score_long.cuh"
 #include "traceback_kernels.cuh"
 
@@ -106,6 +107,7 @@ struct wsb_batch {
     const Plan* last_plan = nullptr;
     void* d_bnd = nullptr;
     size_t bnd_bytes = 0;
+    int32_t* d_redo = nullptr;   // packed int16 kernel: list of pairs to re-score (slot 0 = count, list from slot 4)
     // Piecewise upload: piece k covers pairs [piece_end[k-1], piece_end[k]) and is complete (pools included) once
     // piece_ev[k] has fired on the copy stream; the first score call after creation launches piece by piece.
     static constexpr int kMaxPieces = 8;
@@ -291,7 +293,7 @@ extern "C" void wsb_batch_destroy(wsb_batch* b) {
     for (int k = 0; k < wsb_batch::kMaxPieces; ++k) if (b->piece_ev[k]) cudaEventDestroy(b->piece_ev[k]);
     for (void* p : {(void*)b->d_qcodes, (void*)b->d_scodes, (void*)b->d_qoff, (void*)b->d_soff, (void*)b->d_qlen,
                     (void*)b->d_slen, (void*)b->d_pq, (void*)b->d_ps, (void*)b->d_score, (void*)b->d_i, (void*)b->d_j,
-                    b->d_bnd})
+                    b->d_bnd, (void*)b->d_redo})
         if (p) b->ctx->release(p);
     for (auto& kv : b->plans) if (kv.second.d_units) cudaFree(kv.second.d_units);
     b->tb.release();
@@ -494,8 +496,14 @@ struct Shape { int P, K; };
 static const Shape kShapesF16[] = {{4, 16}, {8, 19}, {8, 32}, {4, 38}, {16, 16}};
 // int32 shapes: narrow groups for short reads, full warps with wide stages for long reads
 static const Shape kShapesI32[] = {{8, 16}, {16, 16}, {32, 16}, {8, 19}};
+static const Shape kShapesS16[] = {{8, 16}, {8, 19}};   // packed int16 short-read kernel (local only)
+static Shape shape_of(int variant, int shape);
 constexpr int kNumShapesF16 = 3, kNumShapesI32 = 4;  // shapes the planner may choose
 constexpr int kNumShapes = 5;  // bucket array bound
+
+static Shape shape_of(int variant, int shape) {
+    return variant == WSB_VARIANT_F16X2 ? kShapesF16[shape] : variant == WSB_VARIANT_S16X2 ? kShapesS16[shape] : kShapesI32[shape];
+}
 
 static double padded_cost(const Shape& s, int m, int n) {
     const int w = s.P * s.K;
@@ -556,9 +564,15 @@ static LongFn pick_long(int atype, int gap, bool cluster) {
     return nullptr;
 }
 
+template <int P, int K> static KernelSel pick_short16(int gap) {
+    if (gap == GAP_LINEAR) return {s16_local_short_kernel<P, K, GAP_LINEAR>, short16_smem_bytes<P, K>()};
+    return {s16_local_short_kernel<P, K, GAP_MERGED>, short16_smem_bytes<P, K>()};
+}
+
 // short_ok: every unit of the launch fits one stage and the short kernel's query buffer
 static KernelSel pick_kernel(int variant, int shape, int atype, int gap, bool masked, bool short_ok, bool wide) {
     static const char* no_short = getenv("WSB_NO_SHORT");  // tuning aid: force the general kernel
+    if (variant == WSB_VARIANT_S16X2) return shape == 0 ? pick_short16<8, 16>(gap) : pick_short16<8, 19>(gap);
     if (variant == WSB_VARIANT_F16X2 && atype == AT_LOCAL && short_ok && !(no_short && no_short[0])) {
         switch (shape) {
             case 0: return pick_short<4, 16>(gap);
@@ -590,7 +604,7 @@ static KernelSel pick_kernel(int variant, int shape, int atype, int gap, bool ma
 // Length-bucketing partitioner: classify every pair (variant by value range, kernel shape by padded work), sort each
 // class by work so neighbouring lane groups (and the two halves of a packed unit) carry near-equal loads, and emit one
 // launch group per (variant, shape).  Replaces batch._plan_units / _chunk_units (batch.py:118-164).
-static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int variant, Plan& plan) {
+static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int variant, Plan& plan, bool want_s16) {
     wsb_ctx* ctx = b->ctx;
     const int64_t np = b->n_pairs;
     const bool affine = sch->gap_model == WSB_GAP_AFFINE;
@@ -601,6 +615,8 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
     const int gap_f16 = !affine ? GAP_LINEAR : GAP_MERGED;
     const int ms = max_step(sch);
     const bool wide_scheme = std::abs(sch->match - sch->mismatch) > 127;
+    const bool s16_ok = want_s16 && atype == AT_LOCAL && f16_scheme_ok && std::abs(sch->match) <= 127 &&
+                        std::abs(sch->mismatch) <= 127;
     plan.status.assign((size_t)np, 0);
 
     if (variant == WSB_VARIANT_F16X2 && !merged_ok) return WSB_E_SCHEME;
@@ -611,7 +627,9 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
         if ((int64_t)ms * ((int64_t)m + n) >= (1ll << 29)) { status = WSB_E_LENGTH; return; }
         const bool fits = f16_scheme_ok && wsb_f16_range_ok(sch, m, n);
         if (variant == WSB_VARIANT_F16X2 && !fits) { status = WSB_E_RANGE; return; }
-        if (variant != WSB_VARIANT_I32 && fits) { var = WSB_VARIANT_F16X2; shape = best_shape(kShapesF16, kNumShapesF16, 5, m, n); }
+        if (variant == WSB_VARIANT_AUTO && fits && s16_ok && n <= 152 && m <= kShort16QRows - 4 * 8 - 2) {
+            var = WSB_VARIANT_S16X2; shape = n <= 128 ? 0 : 1;   // packed int16 DPX kernel: same pairs as the half2 short kernel
+        } else if (variant != WSB_VARIANT_I32 && fits) { var = WSB_VARIANT_F16X2; shape = best_shape(kShapesF16, kNumShapesF16, 5, m, n); }
         else { var = WSB_VARIANT_I32; shape = wide_scheme ? 0 : best_shape(kShapesI32, kNumShapesI32, 4, m, n); }
     };
     // The long-read kernel (score_long.cuh) takes the int32 pairs that would otherwise run full-warp stages: it needs
@@ -637,8 +655,8 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
         if (var < 0) return WSB_OK;
         if (!long_ok(var, shape, b->m[0], b->n[0])) {
             LaunchGroup g;
-            g.variant = var; g.shape = shape; g.gap = var == WSB_VARIANT_F16X2 ? gap_f16 : gap_i32;
-            g.n_units = var == WSB_VARIANT_F16X2 ? (np + 1) / 2 : np;
+            g.variant = var; g.shape = shape; g.gap = var == WSB_VARIANT_I32 ? gap_i32 : gap_f16;
+            g.n_units = var == WSB_VARIANT_I32 ? np : (np + 1) / 2;
             g.unit_off = -1; g.max_m = b->m[0]; g.max_n = b->n[0];
             plan.groups.push_back(g);
             return WSB_OK;
@@ -646,7 +664,7 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
     }
 
     // general path: bucket, sort by work (descending), pair neighbours
-    std::vector<int64_t> bucket[2][kNumShapes];
+    std::vector<int64_t> bucket[3][kNumShapes];   // class 0 = half2, 1 = int32, 2 = packed int16
     std::vector<int64_t> long_pairs;
     double long_iters = 0.0;  // single-warp iterations of all long-class pairs
     for (int64_t p = 0; p < np; ++p) {
@@ -658,7 +676,7 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
             long_pairs.push_back(p);
             long_iters += (double)((b->n[p] + kLongW - 1) / kLongW) * (b->m[p] + 31);
         } else {
-            bucket[var == WSB_VARIANT_F16X2 ? 0 : 1][shape].push_back(p);
+            bucket[var == WSB_VARIANT_F16X2 ? 0 : var == WSB_VARIANT_S16X2 ? 2 : 1][shape].push_back(p);
         }
     }
     std::vector<int32_t> units;
@@ -716,17 +734,17 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
             plan.groups.push_back(g);
         }
     }
-    for (int cls = 0; cls < 2; ++cls)
+    for (int cls = 0; cls < 3; ++cls)
         for (int s = 0; s < kNumShapes; ++s) {
             auto& v = bucket[cls][s];
             if (v.empty()) continue;
             std::stable_sort(v.begin(), v.end(), by_work);
             LaunchGroup g;
-            g.variant = cls == 0 ? WSB_VARIANT_F16X2 : WSB_VARIANT_I32;
-            g.shape = s; g.gap = cls == 0 ? gap_f16 : gap_i32;
+            g.variant = cls == 0 ? WSB_VARIANT_F16X2 : cls == 2 ? WSB_VARIANT_S16X2 : WSB_VARIANT_I32;
+            g.shape = s; g.gap = cls == 1 ? gap_i32 : gap_f16;
             g.unit_off = (int64_t)units.size();
             for (int64_t p : v) { g.max_m = std::max(g.max_m, b->m[p]); g.max_n = std::max(g.max_n, b->n[p]); }
-            if (cls == 0) {
+            if (cls != 1) {
                 g.n_units = ((int64_t)v.size() + 1) / 2;
                 for (size_t k = 0; k < v.size(); k += 2) {
                     units.push_back((int32_t)v[k]);
@@ -780,17 +798,20 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
     if (!b) return WSB_E_ARG;
     int rc = check_scheme(sch, atype);
     if (rc) return rc;
-    if (variant < WSB_VARIANT_AUTO || variant > WSB_VARIANT_I32) return WSB_E_ARG;
+    if (variant < WSB_VARIANT_AUTO || variant > WSB_VARIANT_S16X2) return WSB_E_ARG;
+    const bool want_s16 = variant == WSB_VARIANT_S16X2;   // opt-in: routed like AUTO, short local pairs take the packed int16 kernel
+    if (want_s16) variant = WSB_VARIANT_AUTO;
     wsb_ctx* ctx = b->ctx;
     CUDA_TRY(ctx, cudaSetDevice(ctx->device));
     const bool affine = sch->gap_model == WSB_GAP_AFFINE;
     const int beta_eff = affine ? sch->gap_extend : sch->gap_open;
 
-    auto key = std::make_tuple(sch->match, sch->mismatch, sch->gap_open, sch->gap_extend, sch->gap_model, atype, variant);
+    auto key = std::make_tuple(sch->match, sch->mismatch, sch->gap_open, sch->gap_extend, sch->gap_model, atype,
+                               want_s16 ? (int)WSB_VARIANT_S16X2 : variant);
     auto it = b->plans.find(key);
     if (it == b->plans.end()) {
         Plan plan;
-        rc = build_plan(b, sch, atype, variant, plan);
+        rc = build_plan(b, sch, atype, variant, plan, want_s16);
         if (rc) { if (plan.d_units) cudaFree(plan.d_units); return rc; }
         it = b->plans.emplace(key, std::move(plan)).first;
     }
@@ -829,7 +850,7 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
             bnd_need += (size_t)rows * sizeof(int2) * (size_t)(g.long_nw * g.cluster + 1) * (size_t)(grid / g.cluster);
             continue;
         }
-        const Shape sh = g.variant == WSB_VARIANT_F16X2 ? kShapesF16[g.shape] : kShapesI32[g.shape];
+        const Shape sh = shape_of(g.variant, g.shape);
         const bool short_ok = g.max_n <= sh.P * sh.K && g.max_m <= kShortQRows - 4 * sh.P - 2;
         const KernelSel sel = pick_kernel(g.variant, g.shape, atype, g.gap, sch->mismatch > 0 || sch->match < 0, short_ok,
                                           std::abs(sch->match - sch->mismatch) > 127);
@@ -860,6 +881,15 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
                            plan.groups[0].unit_off < 0 && plan.groups[0].long_nw == 0;
     if (b->upload_pending && !piecewise && b->n_pieces > 0)
         CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, b->piece_ev[b->n_pieces - 1], 0));
+
+    bool any_s16 = false;
+    int s16_gap = GAP_MERGED;
+    for (const LaunchGroup& g : plan.groups) any_s16 = any_s16 || g.variant == WSB_VARIANT_S16X2;
+    if (any_s16 && !plan_only) {   // list of pairs the packed int16 kernel hands back (flagged subject symbols)
+        if (!b->d_redo) CUDA_TRY(ctx, ctx->alloc((void**)&b->d_redo, sizeof(int32_t) * (size_t)(b->n_pairs + 8)));
+        CUDA_TRY(ctx, cudaMemsetAsync(b->d_redo, 0, 16, ctx->stream));
+    }
+    any_s16 = false;
 
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
     int launches = 0, n_aux = 0;
@@ -901,12 +931,14 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
         prm.pair_q = b->d_pq; prm.pair_s = b->d_ps;
         prm.units = g.unit_off >= 0 ? plan.d_units + g.unit_off : nullptr;
         prm.n_units = g.n_units; prm.n_pairs = b->n_pairs; prm.pair_base = 0;
+        prm.redo = b->d_redo ? b->d_redo + 4 : nullptr; prm.redo_count = b->d_redo; prm.n_pairs_dev = nullptr;
+        if (g.variant == WSB_VARIANT_S16X2) { any_s16 = true; s16_gap = g.gap; }
         prm.out_score = b->d_score; prm.out_i = b->d_i; prm.out_j = b->d_j;
         prm.match = sch->match; prm.mismatch = sch->mismatch; prm.alpha = sch->gap_open; prm.beta = beta_eff;
         prm.bnd = geo[k].bnd_rows ? (char*)b->d_bnd + geo[k].bnd_off : nullptr; prm.bnd_rows = geo[k].bnd_rows;
         if (piecewise) {  // uniform batch, identity unit mapping: one launch per uploaded piece, as its slice lands
-            const int nv = g.variant == WSB_VARIANT_F16X2 ? 2 : 1;
-            const Shape sh = g.variant == WSB_VARIANT_F16X2 ? kShapesF16[g.shape] : kShapesI32[g.shape];
+            const int nv = g.variant == WSB_VARIANT_I32 ? 1 : 2;
+            const Shape sh = shape_of(g.variant, g.shape);
             const int gpb = kThreads / sh.P;
             const int64_t full_blocks = (g.n_units + gpb - 1) / gpb;
             const int64_t resident = full_blocks <= geo[k].grid ? (int64_t)1 << 40 : geo[k].grid;  // grid cap = resident blocks
@@ -924,6 +956,21 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
             continue;
         }
         geo[k].fn<<<geo[k].grid, kThreads, geo[k].smem, ctx->stream>>>(prm);
+        CUDA_TRY(ctx, cudaGetLastError());
+        ++launches;
+    }
+    if (any_s16) {   // re-score what the packed int16 kernel could not encode, with the half2 short kernel
+        const KernelSel sel = pick_short<8, 19>(s16_gap);
+        CUDA_TRY(ctx, cudaFuncSetAttribute(sel.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel.smem));
+        ScoreParams prm = {};
+        prm.q_codes = b->d_qcodes; prm.q_off = b->d_qoff; prm.q_len = b->d_qlen;
+        prm.s_codes = b->d_scodes; prm.s_off = b->d_soff; prm.s_len = b->d_slen;
+        prm.pair_q = b->d_pq; prm.pair_s = b->d_ps;
+        prm.units = b->d_redo + 4; prm.n_pairs_dev = b->d_redo; prm.n_units = 0; prm.n_pairs = b->n_pairs;
+        prm.out_score = b->d_score; prm.out_i = b->d_i; prm.out_j = b->d_j;
+        prm.match = sch->match; prm.mismatch = sch->mismatch; prm.alpha = sch->gap_open; prm.beta = beta_eff;
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((b->n_pairs / 2 + 15) / 16, (int64_t)ctx->sm_count * 2));
+        sel.fn<<<grid, kThreads, sel.smem, ctx->stream>>>(prm);
         CUDA_TRY(ctx, cudaGetLastError());
         ++launches;
     }

@@ -201,3 +201,27 @@ def test_long_read_kernel_cluster_classes(ctx, align_type):
     want = oracle_scores(qs, ss, pairs, scheme, align_type)
     got = gpu_scores(ctx, qs, ss, pairs, scheme, align_type, "auto")
     assert_scores_equal(got, want, f"cluster {align_type}")
+
+
+@pytest.mark.parametrize("gap_model", ["linear", "affine"])
+def test_packed_int16_variant_equals_oracle_including_flagged_subjects(ctx, gap_model):
+    """Opt-in S16X2 variant (score_short16.cuh): short local pairs run in packed int16; a pair whose subject holds a
+    flagged symbol cannot be encoded there and is re-scored by the half2 kernel inside the same call."""
+    rng = np.random.default_rng(16)
+    scheme = scheme_of((2, -1, 2, 1) if gap_model == "affine" else (2, -1, 1, 1), gap_model)
+    n = 3001
+    qs = [random_codes(rng, int(rng.integers(30, 161))) for _ in range(n)]
+    ss = [mutate_codes(rng, q)[:150] if i % 2 else random_codes(rng, int(rng.integers(30, 151))) for i, q in enumerate(qs)]
+    for i in range(0, n, 7):      # flagged symbols on either side, sometimes both
+        if i % 3 != 1:
+            s = ss[i].copy(); s[rng.integers(0, len(s))] = 4; ss[i] = s
+        if i % 3 != 0:
+            q = qs[i].copy(); q[rng.integers(0, len(q))] = 4; qs[i] = q
+    qs.append(random_codes(rng, 600)); ss.append(random_codes(rng, 700))    # too long for the kernel: routed as in AUTO
+    pairs = [(i, i) for i in range(len(qs))]
+    want = oracle_scores(qs, ss, pairs, scheme, "local")
+    got = gpu_scores(ctx, qs, ss, pairs, scheme, "local", "s16x2")
+    assert_scores_equal(got, want, f"s16x2 {gap_model}")
+    # other alignment types: S16X2 is simply AUTO
+    assert_scores_equal(gpu_scores(ctx, qs[:200], ss[:200], pairs[:200], scheme, "global", "s16x2"),
+                        oracle_scores(qs[:200], ss[:200], pairs[:200], scheme, "global"), "s16x2 global")

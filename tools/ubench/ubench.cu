@@ -23,7 +23,7 @@ enum Op { OP_IADD3, OP_IMAD, OP_LOP3, OP_PRMT, OP_IMNMX, OP_VIMNMX3, OP_VIADDMNM
           MIX_PRMT_VIMNMX16, MIX_PRMT_HFMA2, MIX_IMNMX_IMAD, MIX_HMNMX2_HADD2_SHFL, MIX_VIMNMX16_IMAD,
           MIX_HSET2_HFMA2, MIX_HSET2_HMNMX2, MIX_CELL_DPX, MIX_CELL_H2, MIX_VIADD16_IMAD, MIX_LDS_VIMNMX16,
           MIX_SHFL_VIMNMX16, MIX_IADD3_IMAD, MIX_LOP3_IMAD,
-          OP_IDP4A, OP_VIADD32, MIX_IDP_VIMNMX3, MIX_CELL_I32_IDP, MIX_CELL_I32_PRMT, MIX_CELL_S16_PRMT, MIX_CELL_H2V, MIX_CELL_H2V_ALT, MIX_VHMNMX_HADD2, MIX_VHMNMX_HFMA2, MIX_2VHMNMX_3HADD2, MIX_HMNMX2x2_HADD2, OP_COUNT };
+          OP_IDP4A, OP_VIADD32, MIX_IDP_VIMNMX3, MIX_CELL_I32_IDP, MIX_CELL_I32_PRMT, MIX_CELL_S16_PRMT, MIX_CELL_H2V, MIX_CELL_H2V_ALT, MIX_VHMNMX_HADD2, MIX_VHMNMX_HFMA2, MIX_2VHMNMX_3HADD2, MIX_HMNMX2x2_HADD2, MIX_CELL_S16V, MIX_CELL_S16V_RM, OP_COUNT };
 
 static const char* names[] = {"IADD3","IMAD","LOP3","PRMT","IMNMX(VIMNMX.S32)","VIMNMX3","VIADDMNMX","VIADDMNMX.RELU",
   "VIMNMX.S16x2","VIMNMX3.S16x2","VIADDMNMX.S16x2","VIADDMNMX.S16x2.RELU","VIADD.16x2",
@@ -35,10 +35,11 @@ static const char* names[] = {"IADD3","IMAD","LOP3","PRMT","IMNMX(VIMNMX.S32)","
   "mix VIADD16+IMAD","mix LDS+3xVIMNMX16","mix SHFL+7xVIMNMX16","mix IADD3+IMAD","mix LOP3+IMAD",
   "IDP.4A.S8.S8","VIADD(s32 +imm)","mix IDP4A+VIMNMX3","mix i32 cell(IDP4A,2VIMNMX3,2IMAD)","mix i32 cell(PRMT,IMAD,2VIMNMX3,2IMAD)","mix s16x2 cell(2PRMT,LOP3,VIADD16,2VIMNMX3.16,2VIADD16)",
   "mix short-kernel cell(HSET2,HFMA2.RELU,2VHMNMX,3HADD2)","mix short-kernel cell, strictly alternating order",
-  "mix VHMNMX+HADD2","mix VHMNMX+HFMA2","mix 2VHMNMX+3HADD2","mix 2xHMNMX2(unfused)+HADD2"};
+  "mix VHMNMX+HADD2","mix VHMNMX+HFMA2","mix 2VHMNMX+3HADD2","mix 2xHMNMX2(unfused)+HADD2",
+  "mix s16x2 short cell(PRMT,VIADD16,2VIMNMX3.16.RELU,2VIADD16)","same + row max (1 VIMNMX3.16 per 2 cells)"};
 // instructions counted per chain step
 static const int per_step[] = {1,1,1,1,1,1,1,1, 1,1,1,1,1, 1,1,1,1,1,1,1,1,1,1, 1,1,1,2,
-  2,2,2,2,2, 2,2,2,9,2, 2,2,6,9, 2,4,8,2,2, 1,1,2,5,6,8, 7,7, 2,2,5,3};
+  2,2,2,2,2, 2,2,2,9,2, 2,2,6,9, 2,4,8,2,2, 1,1,2,5,6,8, 7,7, 2,2,5,3, 6,13};
 
 __device__ __forceinline__ uint32_t h2max(uint32_t a, uint32_t b){ uint32_t d; asm volatile("max.f16x2 %0,%1,%2;" : "=r"(d) : "r"(a),"r"(b)); return d; }
 __device__ __forceinline__ uint32_t h2add(uint32_t a, uint32_t b){ uint32_t d; asm volatile("add.f16x2 %0,%1,%2;" : "=r"(d) : "r"(a),"r"(b)); return d; }
@@ -182,6 +183,31 @@ __global__ void __launch_bounds__(1024, 1) bench(uint32_t* out, const uint32_t* 
         else if (OP == MIX_VHMNMX_HFMA2) { v = h2max(h2max(v, y), z); v = h2fma(v, y, w); }
         else if (OP == MIX_2VHMNMX_3HADD2) { uint32_t a = h2max(h2max(v, y), z); uint32_t b = h2max(h2max(v, w), y); uint32_t c = h2add(a, w); uint32_t d = h2add(b, z); v = h2add(c, d); }
         else if (OP == MIX_HMNMX2x2_HADD2) { uint32_t a = h2max(v, y); BAR(a); a = h2max(a, z); v = h2add(a, w); }
+        else if (OP == MIX_CELL_S16V) {
+          uint32_t sg; asm volatile("prmt.b32 %0,%1,%2,%3;" : "=r"(sg) : "r"(y),"r"(z),"r"(w));
+          uint32_t d = __vadd2(sg, v); BAR(d);
+          uint32_t h = __vimax3_s16x2_relu(w, v, d); BAR(h);
+          uint32_t tn = __vimax3_s16x2_relu(z, v, d); BAR(tn);
+          uint32_t la = __vadd2(tn, y); BAR(la);
+          uint32_t lg = __vadd2(tn, z); BAR(lg);
+          v = la ^ lg ^ h;   // LOP3, not counted
+        }
+        else if (OP == MIX_CELL_S16V_RM) {   // two cells + one 3-input row max
+          uint32_t sg; asm volatile("prmt.b32 %0,%1,%2,%3;" : "=r"(sg) : "r"(y),"r"(z),"r"(w));
+          uint32_t d = __vadd2(sg, v); BAR(d);
+          uint32_t h = __vimax3_s16x2_relu(w, v, d); BAR(h);
+          uint32_t tn = __vimax3_s16x2_relu(z, v, d); BAR(tn);
+          uint32_t la = __vadd2(tn, y); BAR(la);
+          uint32_t lg = __vadd2(tn, z); BAR(lg);
+          uint32_t sg2; asm volatile("prmt.b32 %0,%1,%2,%3;" : "=r"(sg2) : "r"(y),"r"(z),"r"(la));
+          uint32_t d2 = __vadd2(sg2, h); BAR(d2);
+          uint32_t h2 = __vimax3_s16x2_relu(la, v, d2); BAR(h2);
+          uint32_t tn2 = __vimax3_s16x2_relu(lg, v, d2); BAR(tn2);
+          uint32_t la2 = __vadd2(tn2, y); BAR(la2);
+          uint32_t lg2 = __vadd2(tn2, z); BAR(lg2);
+          uint32_t rm = __vimax3_s16x2(w, h, h2); BAR(rm);
+          v = la2 ^ lg2 ^ rm;
+        }
         x[j] = v;
       }
     }
