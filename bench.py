@@ -235,6 +235,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--pairs", type=int, default=0, help="override pairs per GPU (debug)")
     ap.add_argument("--cap", type=int, default=100_000, help="cfg5: length cap of the truncated Pareto distribution")
+    ap.add_argument("--host-format", default="bytes", choices=["bytes", "packed2"],
+                    help="e2e leg: host pools as one byte per symbol, or in the reference's 2-bit Sequence.data layout")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     cfg = dict(WORKLOADS[args.workload])
@@ -308,7 +310,12 @@ def main():
 
     # end to end through the public API: host buffers in, host results out, every step
     pair_arr = np.stack([idx, idx], 1)
-    job = W.BatchJob(W.SequencePool(*pool_q), W.SequencePool(*pool_s), pair_arr, W.AlignConfig(cfg["align_type"], cfg["gap_model"],
+    host_q, host_s = W.SequencePool(*pool_q), W.SequencePool(*pool_s)
+    if args.host_format == "packed2":   # packed once, outside the timed region: the host format of the input, not a step
+        host_q, host_s = host_q.to_packed(), host_s.to_packed()
+        keep_packed = [pinned(hp.packed) for hp in (host_q, host_s)]
+        host_q.packed, host_s.packed = keep_packed[0][0], keep_packed[1][0]
+    job = W.BatchJob(host_q, host_s, pair_arr, W.AlignConfig(cfg["align_type"], cfg["gap_model"],
                                                            "traceback" if traceback else "score_only"),
                      scheme, tuning=W.EngineTuning(packed=(variant != "i32")), devices=[device])
     if variant == "i32":
@@ -351,6 +358,7 @@ def main():
                            "align_type": cfg["align_type"],
                            "gap_model": cfg["gap_model"], "scheme": list(cfg["scheme"]),
                            "result_mode": "traceback" if traceback else "score_only", "variant": variant,
+                           "e2e_host_format": args.host_format,
                            "l2": f"inputs {(len(pool_q[0]) + len(pool_s[0])) / 1e6:.0f} MB per GPU vs 126 MB L2 "
                                  + ("(no flush needed)" if len(pool_q[0]) + len(pool_s[0]) > 252e6 else
                                     "(inputs re-read from L2/HBM each step; per-cell DRAM traffic is ~0 either way)"),

@@ -94,6 +94,15 @@ int wsb_batch_create(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t* q_off,
 int wsb_batch_create_async(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t* q_off, const int32_t* q_len, int64_t n_q,
                            const uint8_t* s_codes, const int64_t* s_off, const int32_t* s_len, int64_t n_s,
                            const int32_t* pair_q, const int32_t* pair_s, int64_t n_pairs, wsb_batch** out);
+/* Same as wsb_batch_create_async for pools kept in the reference's 2-bit layout (Sequence.data, core.py:78-87: four
+ * symbols per byte, low bits first), here over the concatenated pool: symbol k of the pool sits in bits 2*(k%4) of byte
+ * k/4.  Flagged (non-ACGT) symbols, stored as code 0 in the packed data like the reference does (core.py:101-114), are
+ * listed by pool position in q_flag_pos / s_flag_pos.  A quarter of the bytes cross the bus; the pools are expanded to
+ * one byte per symbol on the device, slice by slice. */
+int wsb_batch_create_packed_async(wsb_ctx* ctx, const uint8_t* q_packed, const int64_t* q_flag_pos, int64_t n_q_flags,
+                                  const int64_t* q_off, const int32_t* q_len, int64_t n_q, const uint8_t* s_packed,
+                                  const int64_t* s_flag_pos, int64_t n_s_flags, const int64_t* s_off, const int32_t* s_len,
+                                  int64_t n_s, const int32_t* pair_q, const int32_t* pair_s, int64_t n_pairs, wsb_batch** out);
 void wsb_batch_destroy(wsb_batch* b);
 
 /* Score every pair on the device; results stay in HBM until wsb_batch_fetch_scores.  kernel_ms (optional) receives

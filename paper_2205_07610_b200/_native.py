@@ -21,7 +21,7 @@ WSB_OK, WSB_E_CUDA, WSB_E_ARG, WSB_E_NOMEM, WSB_E_LENGTH, WSB_E_RANGE, WSB_E_SCH
 
 EXPORTED_SYMBOLS = (
     "wsb_strerror", "wsb_version", "wsb_device_count", "wsb_ctx_create", "wsb_ctx_destroy", "wsb_last_error",
-    "wsb_ctx_sm_count", "wsb_batch_create", "wsb_batch_create_async", "wsb_batch_destroy", "wsb_batch_score", "wsb_batch_fetch_scores",
+    "wsb_ctx_sm_count", "wsb_batch_create", "wsb_batch_create_async", "wsb_batch_create_packed_async", "wsb_batch_destroy", "wsb_batch_score", "wsb_batch_fetch_scores",
     "wsb_batch_traceback", "wsb_batch_fetch_traceback", "wsb_batch_total_cells", "wsb_score_batch",
     "wsb_traceback_batch", "wsb_merged_state_exact", "wsb_f16_range_ok", "wsb_plan_shards", "wsb_batch_has_faults", "wsb_pinned_alloc",
     "wsb_pinned_free",
@@ -59,6 +59,7 @@ def load():
     lib.wsb_ctx_sm_count.argtypes = [p]
     lib.wsb_batch_create.argtypes = [p, p, p, p, i64, p, p, p, i64, p, p, i64, p]
     lib.wsb_batch_create_async.argtypes = [p, p, p, p, i64, p, p, p, i64, p, p, i64, p]
+    lib.wsb_batch_create_packed_async.argtypes = [p, p, p, i64, p, p, i64, p, p, i64, p, p, i64, p, p, i64, p]
     lib.wsb_batch_destroy.argtypes = [p]
     lib.wsb_batch_destroy.restype = None
     lib.wsb_batch_score.argtypes = [p, p, ci, ci, p, p]
@@ -183,21 +184,36 @@ class Context:
 class Batch:
     """Device-resident pools + pair list (wsb_batch)."""
 
-    def __init__(self, ctx: Context, q_codes, q_off, q_len, s_codes, s_off, s_len, pair_q, pair_s):
+    def __init__(self, ctx: Context, q_codes, q_off, q_len, s_codes, s_off, s_len, pair_q, pair_s, packed=None):
+        """packed = ((q_packed, q_flag_pos), (s_packed, s_flag_pos)): both pools in the 2-bit layout (four symbols per
+        byte, low bits first over the concatenated pool) plus the positions of flagged symbols; q_codes / s_codes are
+        then ignored (may be None)."""
         self._lib = load()
         self.ctx = ctx
-        arrs = [np.ascontiguousarray(q_codes, np.uint8), np.ascontiguousarray(q_off, np.int64),
-                np.ascontiguousarray(q_len, np.int32), np.ascontiguousarray(s_codes, np.uint8),
+        meta = [np.ascontiguousarray(q_off, np.int64), np.ascontiguousarray(q_len, np.int32),
                 np.ascontiguousarray(s_off, np.int64), np.ascontiguousarray(s_len, np.int32),
                 np.ascontiguousarray(pair_q, np.int32), np.ascontiguousarray(pair_s, np.int32)]
-        self.n_pairs = len(arrs[6])
-        self.h2d_bytes = int(sum(a.nbytes for a in arrs))
+        self.n_pairs = len(meta[4])
         h = ctypes.c_void_p()
-        self._keep = arrs  # the upload is asynchronous: the arrays must outlive it (released in close())
-        rc = self._lib.wsb_batch_create_async(ctx._h, _ptr(arrs[0]), _ptr(arrs[1]), _ptr(arrs[2]), len(arrs[2]),
-                                        _ptr(arrs[3]), _ptr(arrs[4]), _ptr(arrs[5]), len(arrs[5]),
-                                        _ptr(arrs[6]), _ptr(arrs[7]), self.n_pairs, ctypes.byref(h))
+        if packed is None:
+            pools = [np.ascontiguousarray(q_codes, np.uint8), np.ascontiguousarray(s_codes, np.uint8)]
+            self._keep = pools + meta  # the upload is asynchronous: the arrays must outlive it (released in close())
+            rc = self._lib.wsb_batch_create_async(ctx._h, _ptr(pools[0]), _ptr(meta[0]), _ptr(meta[1]), len(meta[1]),
+                                                  _ptr(pools[1]), _ptr(meta[2]), _ptr(meta[3]), len(meta[3]),
+                                                  _ptr(meta[4]), _ptr(meta[5]), self.n_pairs, ctypes.byref(h))
+        else:
+            (qp, qf), (sp, sf) = packed
+            pools = [np.ascontiguousarray(qp, np.uint8), np.ascontiguousarray(sp, np.uint8),
+                     np.ascontiguousarray(qf if qf is not None else [], np.int64),
+                     np.ascontiguousarray(sf if sf is not None else [], np.int64)]
+            self._keep = pools + meta
+            rc = self._lib.wsb_batch_create_packed_async(
+                ctx._h, _ptr(pools[0]), _ptr(pools[2]) if len(pools[2]) else None, len(pools[2]), _ptr(meta[0]), _ptr(meta[1]),
+                len(meta[1]), _ptr(pools[1]), _ptr(pools[3]) if len(pools[3]) else None, len(pools[3]), _ptr(meta[2]),
+                _ptr(meta[3]), len(meta[3]), _ptr(meta[4]), _ptr(meta[5]), self.n_pairs, ctypes.byref(h))
+        self.h2d_bytes = int(sum(a.nbytes for a in self._keep))
         if rc:
+            self._keep = None
             raise status_exception(rc, ctx.last_error())
         self._h = h
 

@@ -178,8 +178,12 @@ def _run_shard(device: int, queries: SequencePool, subjects: SequencePool, pair_
                cfg: AlignConfig, scheme: ScoringScheme, variant: str, out: dict):
     try:
         ctx = get_context(device)
-        batch = N.Batch(ctx, queries.codes, queries.off, queries.len, subjects.codes, subjects.off, subjects.len,
-                        pair_q, pair_s)
+        if queries.packed is not None and subjects.packed is not None:   # 2-bit pools: a quarter of the bytes to upload
+            batch = N.Batch(ctx, None, queries.off, queries.len, None, subjects.off, subjects.len, pair_q, pair_s,
+                            packed=((queries.packed, queries.flag_pos), (subjects.packed, subjects.flag_pos)))
+        else:
+            batch = N.Batch(ctx, queries.codes, queries.off, queries.len, subjects.codes, subjects.off, subjects.len,
+                            pair_q, pair_s)
         try:
             out["h2d"] = batch.h2d_bytes
             out["cells"] = batch.total_cells

@@ -112,6 +112,8 @@ struct wsb_batch {
     // piece_ev[k] has fired on the copy stream; the first score call after creation launches piece by piece.
     static constexpr int kMaxPieces = 8;
     int n_pieces = 0;
+    int n_pieces_usable = 0;             // 1: score only after the whole upload (packed pools with flagged positions)
+    void* stage_blocks[4] = {};          // packed-pool staging areas, released with the batch
     int64_t piece_end[kMaxPieces] = {};
     cudaEvent_t piece_ev[kMaxPieces] = {};
     bool upload_pending = false;
@@ -293,18 +295,46 @@ extern "C" void wsb_batch_destroy(wsb_batch* b) {
     for (int k = 0; k < wsb_batch::kMaxPieces; ++k) if (b->piece_ev[k]) cudaEventDestroy(b->piece_ev[k]);
     for (void* p : {(void*)b->d_qcodes, (void*)b->d_scodes, (void*)b->d_qoff, (void*)b->d_soff, (void*)b->d_qlen,
                     (void*)b->d_slen, (void*)b->d_pq, (void*)b->d_ps, (void*)b->d_score, (void*)b->d_i, (void*)b->d_j,
-                    b->d_bnd, (void*)b->d_redo})
+                    b->d_bnd, (void*)b->d_redo, b->stage_blocks[0], b->stage_blocks[1], b->stage_blocks[2], b->stage_blocks[3]})
         if (p) b->ctx->release(p);
     for (auto& kv : b->plans) if (kv.second.d_units) cudaFree(kv.second.d_units);
     b->tb.release();
     delete b;
 }
 
-extern "C" int wsb_batch_create_async(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t* q_off, const int32_t* q_len,
-                                      int64_t n_q, const uint8_t* s_codes, const int64_t* s_off, const int32_t* s_len,
-                                      int64_t n_s, const int32_t* pair_q, const int32_t* pair_s, int64_t n_pairs,
-                                      wsb_batch** out) {
-    if (!ctx || !out || !q_codes || !q_off || !q_len || !s_codes || !s_off || !s_len || !pair_q || !pair_s ||
+// 2-bit packed pools (the reference's Sequence.data layout, core.py:78-87: four symbols per byte, low bits first, here
+// over the concatenated pool) are expanded on the device: a quarter of the bytes cross the bus.
+__global__ void unpack2_kernel(const uint8_t* packed_slice, int64_t first_byte, int64_t sym_lo, int64_t sym_hi, uint8_t* codes) {
+    // one thread per packed byte of the slice; symbols outside [sym_lo, sym_hi) belong to a neighbouring slice
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t byte = first_byte + k;
+    const int64_t s0 = byte * 4;
+    if (s0 >= sym_hi) return;
+    const unsigned v = packed_slice[k];
+    if (s0 >= sym_lo && s0 + 3 < sym_hi && (reinterpret_cast<uintptr_t>(codes + s0) & 3) == 0) {
+        *reinterpret_cast<uchar4*>(codes + s0) = make_uchar4(v & 3, (v >> 2) & 3, (v >> 4) & 3, (v >> 6) & 3);
+        return;
+    }
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+        if (s0 + x >= sym_lo && s0 + x < sym_hi) codes[s0 + x] = (v >> (2 * x)) & 3;
+}
+__global__ void set_flags_kernel(const int64_t* idx, int64_t n, int64_t limit, uint8_t* codes) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n && idx[k] >= 0 && idx[k] < limit) codes[idx[k]] = 4;
+}
+
+struct PackedPools {   // optional: pools given in the 2-bit layout (+ sorted-or-not lists of flagged symbol positions)
+    const uint8_t* q_packed = nullptr; const int64_t* q_flags = nullptr; int64_t n_q_flags = 0;
+    const uint8_t* s_packed = nullptr; const int64_t* s_flags = nullptr; int64_t n_s_flags = 0;
+};
+
+static int batch_create_impl(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t* q_off, const int32_t* q_len,
+                             int64_t n_q, const uint8_t* s_codes, const int64_t* s_off, const int32_t* s_len,
+                             int64_t n_s, const int32_t* pair_q, const int32_t* pair_s, int64_t n_pairs,
+                             const PackedPools& pk, wsb_batch** out) {
+    if (!ctx || !out || (!q_codes && !pk.q_packed) || !q_off || !q_len || (!s_codes && !pk.s_packed) || !s_off || !s_len ||
+        !pair_q || !pair_s ||
         n_q <= 0 || n_s <= 0 || n_pairs <= 0 || n_pairs > (int64_t)0x7fffffff)
         return WSB_E_ARG;
     *out = nullptr;
@@ -415,28 +445,73 @@ extern "C" int wsb_batch_create_async(wsb_ctx* ctx, const uint8_t* q_codes, cons
     cudaError_t e;
     if ((e = ctx->alloc((void**)&b->d_qcodes, (size_t)std::max<int64_t>(q_total, 1))) != cudaSuccess) return fail(e);
     if ((e = ctx->alloc((void**)&b->d_scodes, (size_t)std::max<int64_t>(s_total, 1))) != cudaSuccess) return fail(e);
+    // pool slices, address-ordered; a packed pool goes up as packed bytes into a staging area and is expanded per slice
+    uint8_t *stage_q = nullptr, *stage_s = nullptr;
+    int64_t *dflags_q = nullptr, *dflags_s = nullptr;
+    if (pk.q_packed && (e = ctx->alloc((void**)&stage_q, (size_t)(q_total / 4 + 2))) != cudaSuccess) return fail(e);
+    if (pk.s_packed && (e = ctx->alloc((void**)&stage_s, (size_t)(s_total / 4 + 2))) != cudaSuccess) return fail(e);
+    auto send = [&](const uint8_t* codes, const uint8_t* packed, uint8_t* stage, uint8_t* dst, int64_t lo, int64_t hi) -> cudaError_t {
+        if (hi <= lo) return cudaSuccess;
+        if (!packed) return cudaMemcpyAsync(dst + lo, codes + lo, (size_t)(hi - lo), cudaMemcpyHostToDevice, ctx->copy_stream);
+        const int64_t b0 = lo / 4, b1 = (hi + 3) / 4;   // packed bytes covering symbols [lo, hi)
+        cudaError_t r = cudaMemcpyAsync(stage + b0, packed + b0, (size_t)(b1 - b0), cudaMemcpyHostToDevice, ctx->copy_stream);
+        if (r != cudaSuccess) return r;
+        unpack2_kernel<<<(unsigned)((b1 - b0 + 255) / 256), 256, 0, ctx->copy_stream>>>(stage + b0, b0, lo, hi, dst);
+        return cudaGetLastError();
+    };
     int64_t done_q = 0, done_s = 0;
     for (int k = 0; k < n_pieces; ++k) {
-        if (need_q[k] > done_q) {
-            e = cudaMemcpyAsync(b->d_qcodes + done_q, q_codes + done_q, (size_t)(need_q[k] - done_q), cudaMemcpyHostToDevice, ctx->copy_stream);
-            if (e != cudaSuccess) return fail(e);
-            done_q = need_q[k];
-        }
-        if (need_s[k] > done_s) {
-            e = cudaMemcpyAsync(b->d_scodes + done_s, s_codes + done_s, (size_t)(need_s[k] - done_s), cudaMemcpyHostToDevice, ctx->copy_stream);
-            if (e != cudaSuccess) return fail(e);
-            done_s = need_s[k];
+        if ((e = send(q_codes, pk.q_packed, stage_q, b->d_qcodes, done_q, need_q[k])) != cudaSuccess) return fail(e);
+        done_q = std::max(done_q, need_q[k]);
+        if ((e = send(s_codes, pk.s_packed, stage_s, b->d_scodes, done_s, need_s[k])) != cudaSuccess) return fail(e);
+        done_s = std::max(done_s, need_s[k]);
+        if (k + 1 == n_pieces) {   // flagged positions (rare) are stamped once everything is expanded
+            if (pk.q_packed && pk.n_q_flags > 0) {
+                if ((e = ctx->alloc((void**)&dflags_q, sizeof(int64_t) * (size_t)pk.n_q_flags)) != cudaSuccess) return fail(e);
+                if ((e = cudaMemcpyAsync(dflags_q, pk.q_flags, sizeof(int64_t) * (size_t)pk.n_q_flags, cudaMemcpyHostToDevice, ctx->copy_stream)) != cudaSuccess) return fail(e);
+                set_flags_kernel<<<(unsigned)((pk.n_q_flags + 255) / 256), 256, 0, ctx->copy_stream>>>(dflags_q, pk.n_q_flags, q_total, b->d_qcodes);
+            }
+            if (pk.s_packed && pk.n_s_flags > 0) {
+                if ((e = ctx->alloc((void**)&dflags_s, sizeof(int64_t) * (size_t)pk.n_s_flags)) != cudaSuccess) return fail(e);
+                if ((e = cudaMemcpyAsync(dflags_s, pk.s_flags, sizeof(int64_t) * (size_t)pk.n_s_flags, cudaMemcpyHostToDevice, ctx->copy_stream)) != cudaSuccess) return fail(e);
+                set_flags_kernel<<<(unsigned)((pk.n_s_flags + 255) / 256), 256, 0, ctx->copy_stream>>>(dflags_s, pk.n_s_flags, s_total, b->d_scodes);
+            }
         }
         if ((e = cudaEventCreateWithFlags(&b->piece_ev[k], cudaEventDisableTiming)) != cudaSuccess) return fail(e);
         if ((e = cudaEventRecord(b->piece_ev[k], ctx->copy_stream)) != cudaSuccess) return fail(e);
     }
+    // staging areas are only touched by work already queued on the copy stream: hand them back to the cache now, the
+    // next user of those blocks is ordered behind this batch on the same streams
+    b->stage_blocks[0] = stage_q; b->stage_blocks[1] = stage_s; b->stage_blocks[2] = dflags_q; b->stage_blocks[3] = dflags_s;
     b->upload_pending = true;
+    if ((pk.q_packed && pk.n_q_flags > 0) || (pk.s_packed && pk.n_s_flags > 0)) b->n_pieces_usable = 1;  // flags land last
     for (int32_t** p : {&b->d_score, &b->d_i, &b->d_j}) {
         e = ctx->alloc((void**)p, sizeof(int32_t) * (size_t)n_pairs);
         if (e != cudaSuccess) return fail(e);
     }
     *out = b;
     return WSB_OK;
+}
+
+extern "C" int wsb_batch_create_async(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t* q_off, const int32_t* q_len,
+                                      int64_t n_q, const uint8_t* s_codes, const int64_t* s_off, const int32_t* s_len,
+                                      int64_t n_s, const int32_t* pair_q, const int32_t* pair_s, int64_t n_pairs,
+                                      wsb_batch** out) {
+    if (!q_codes || !s_codes) return WSB_E_ARG;
+    return batch_create_impl(ctx, q_codes, q_off, q_len, n_q, s_codes, s_off, s_len, n_s, pair_q, pair_s, n_pairs, PackedPools(), out);
+}
+
+extern "C" int wsb_batch_create_packed_async(wsb_ctx* ctx, const uint8_t* q_packed, const int64_t* q_flag_pos, int64_t n_q_flags,
+                                             const int64_t* q_off, const int32_t* q_len, int64_t n_q,
+                                             const uint8_t* s_packed, const int64_t* s_flag_pos, int64_t n_s_flags,
+                                             const int64_t* s_off, const int32_t* s_len, int64_t n_s,
+                                             const int32_t* pair_q, const int32_t* pair_s, int64_t n_pairs, wsb_batch** out) {
+    if (!q_packed || !s_packed || n_q_flags < 0 || n_s_flags < 0 || (n_q_flags > 0 && !q_flag_pos) || (n_s_flags > 0 && !s_flag_pos))
+        return WSB_E_ARG;
+    PackedPools pk;
+    pk.q_packed = q_packed; pk.q_flags = q_flag_pos; pk.n_q_flags = n_q_flags;
+    pk.s_packed = s_packed; pk.s_flags = s_flag_pos; pk.n_s_flags = n_s_flags;
+    return batch_create_impl(ctx, nullptr, q_off, q_len, n_q, nullptr, s_off, s_len, n_s, pair_q, pair_s, n_pairs, pk, out);
 }
 
 extern "C" int wsb_batch_create(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t* q_off, const int32_t* q_len,
@@ -877,7 +952,7 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
     CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_queues, 0, 64 * sizeof(unsigned int), ctx->stream));
 
     // first call after creation: the uploads may still be in flight on the copy stream
-    const bool piecewise = b->upload_pending && b->n_pieces > 1 && !plan_only && plan.groups.size() == 1 &&
+    const bool piecewise = b->upload_pending && b->n_pieces > 1 && b->n_pieces_usable != 1 && !plan_only && plan.groups.size() == 1 &&
                            plan.groups[0].unit_off < 0 && plan.groups[0].long_nw == 0;
     if (b->upload_pending && !piecewise && b->n_pieces > 0)
         CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, b->piece_ev[b->n_pieces - 1], 0));

@@ -15,7 +15,9 @@ class SequencePool:
     """codes[off[k] : off[k] + len[k]] are the symbols of sequence k: 0..3 = ACGT, 4 = flagged."""
 
     def __init__(self, codes: np.ndarray, off: np.ndarray, lengths: np.ndarray, ids=None):
-        self.codes = np.ascontiguousarray(codes, np.uint8)
+        self.packed = None       # optional 2-bit form of the pool (from_packed): what run_batch uploads when present
+        self.flag_pos = None
+        self._codes = np.ascontiguousarray(codes, np.uint8) if codes is not None else None
         self.off = np.ascontiguousarray(off, np.int64)
         self.len = np.ascontiguousarray(lengths, np.int32)
         self.ids = ids
@@ -24,6 +26,40 @@ class SequencePool:
 
     def __len__(self) -> int:
         return int(self.len.shape[0])
+
+    @property
+    def codes(self) -> np.ndarray:
+        """One byte per symbol (expanded on first use when the pool was built from packed data)."""
+        if self._codes is None:
+            total = int((self.off + self.len).max()) if len(self.len) else 0
+            sym = np.arange(total, dtype=np.int64)
+            c = (self.packed[sym >> 2] >> ((sym & 3) << 1).astype(np.uint8)) & 3
+            if self.flag_pos is not None and len(self.flag_pos):
+                c[self.flag_pos] = FLAGGED_CODE
+            self._codes = c.astype(np.uint8)
+        return self._codes
+
+    @classmethod
+    def from_packed(cls, packed: np.ndarray, off: np.ndarray, lengths: np.ndarray, flag_pos=None, ids=None) -> "SequencePool":
+        """Pool in the reference's 2-bit layout (Sequence.data, core.py:78-87: four symbols per byte, low bits first)
+        over the concatenated pool: symbol k sits in bits 2*(k%4) of byte k//4.  flag_pos lists the pool positions of
+        flagged (non-ACGT) symbols, which the packed data stores as 0 like the reference does."""
+        pool = cls(None, off, lengths, ids)
+        pool.packed = np.ascontiguousarray(packed, np.uint8)
+        pool.flag_pos = None if flag_pos is None else np.ascontiguousarray(flag_pos, np.int64)
+        return pool
+
+    def to_packed(self) -> "SequencePool":
+        """The same pool in 2-bit form (host-side packing; meant for pools that are reused across batches)."""
+        c = self.codes
+        flags = np.nonzero(c >= FLAGGED_CODE)[0].astype(np.int64)
+        v = np.where(c >= FLAGGED_CODE, 0, c).astype(np.uint8)
+        pad = (-len(v)) % 4
+        if pad:
+            v = np.concatenate([v, np.zeros(pad, np.uint8)])
+        v = v.reshape(-1, 4)
+        packed = (v[:, 0] | (v[:, 1] << 2) | (v[:, 2] << 4) | (v[:, 3] << 6)).astype(np.uint8)
+        return SequencePool.from_packed(packed, self.off, self.len, flags, self.ids)
 
     def __getitem__(self, k: int) -> Sequence:
         """Materialise one Sequence (reference type) on demand."""

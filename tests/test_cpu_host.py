@@ -211,3 +211,20 @@ def test_bench_workload_generators_are_seeded_and_shaped():
     q, s = bench.make_batch(dict(pairs=64, length=250, related=0.5), 3)
     assert q.shape == s.shape == (64, 250)
     assert (q[::2] == s[::2]).mean() > 0.5 and (q[1::2] == s[1::2]).mean() < 0.4
+
+
+def test_packed_pool_round_trip_matches_reference_layout():
+    """2-bit pool layout = the reference's Sequence.data (core.py:78-87): low bits first, flagged symbols stored as 0."""
+    from paper_2205_07610_b200.pool import SequencePool
+    rng = np.random.default_rng(9)
+    lens = rng.integers(1, 40, 50).astype(np.int32)
+    off = np.zeros(50, np.int64); off[1:] = np.cumsum(lens[:-1])
+    codes = rng.integers(0, 4, int(lens.sum())).astype(np.uint8)
+    codes[[3, 17, 100]] = 4
+    pool = SequencePool(codes, off, lens)
+    packed = pool.to_packed()
+    assert packed.packed.nbytes == (len(codes) + 3) // 4 and list(packed.flag_pos) == [3, 17, 100]
+    assert packed.packed[0] == (codes[0] | (codes[1] << 2) | (codes[2] << 4) | (0 << 6))   # symbol 3 is flagged -> 0
+    assert (packed.codes == codes).all()
+    seq = packed[5]
+    assert len(seq) == lens[5]

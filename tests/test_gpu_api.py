@@ -113,3 +113,32 @@ def test_pool_inputs_and_lazy_results():
         score, end = oracle.ref_score(q[k], s[k], "local", True, 2, -1, 2, 1)
         assert (rep.results[k].score, rep.results[k].q_end, rep.results[k].s_end) == (score, end[0], end[1])
     assert rep.gpu_launches >= 1 and rep.h2d_bytes > 2 * n * 40 and rep.kernel_ms > 0
+
+
+def test_packed_pools_give_identical_results():
+    """Pools in the reference's 2-bit layout are expanded on the device (wsb_batch_create_packed_async)."""
+    rng = np.random.default_rng(21)
+    n = 70_000   # large enough for the piecewise upload path when unflagged
+    L = 150
+    q = rng.integers(0, 4, (n, L), dtype=np.uint8)
+    s = rng.integers(0, 4, (n, L), dtype=np.uint8)
+    idx = np.arange(n, dtype=np.int32)
+    pairs = np.stack([idx, idx], 1)
+    for flagged in (False, True):
+        if flagged:
+            q[5, 7] = 4; s[11, 3] = 4; s[n - 1, L - 1] = 4
+        pq, ps = W.SequencePool.from_uniform(q), W.SequencePool.from_uniform(s)
+        for cfg in (W.AlignConfig("local", "affine"), W.AlignConfig("global", "affine"),
+                    W.AlignConfig("semiglobal", "affine", "traceback")):
+            count = n if cfg.result_mode == "score_only" else 3000
+            a = W.run_batch(W.BatchJob(pq, ps, pairs[:count], cfg, W.ScoringScheme()))
+            b = W.run_batch(W.BatchJob(pq.to_packed(), ps.to_packed(), pairs[:count], cfg, W.ScoringScheme()))
+            assert b.h2d_bytes < a.h2d_bytes
+            ra, rb = a.results, b.results
+            if isinstance(ra, list):
+                assert ra == rb
+            else:
+                for f in ("score", "q_start", "q_end", "s_start", "s_end"):
+                    assert (getattr(ra, f) == getattr(rb, f)).all(), (flagged, cfg.align_type, f)
+                if ra.runs is not None:
+                    assert (ra.runs == rb.runs).all() and (ra.run_off == rb.run_off).all()
