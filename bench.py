@@ -334,7 +334,9 @@ def main():
     peaks = measured_peaks()
     f_ghz = float(peaks.get("sm_max_mhz", 1965.0)) / 1e3
     n_sm = ctx.sm_count
-    width = 1 if (variant == "i32" or args.workload in ("cfg3", "cfg4", "cfg5")) else 2   # dominant kernel: int32 fill / long-read kernel
+    # dominant kernel: cfg3 int32 fill, cfg5 int32 long-read kernel; cfg4's equal-shape pairs run two per block in packed int16
+    width = 1 if (variant == "i32" or args.workload in ("cfg3", "cfg5")) else 2
+    dtype = "i32" if width == 1 else ("s16x2" if args.workload == "cfg4" else "f16x2")
     peak = n_sm * 128 * f_ghz * width / cfg["i_cell"]
     per_gpu = value / world
     traffic = None
@@ -353,7 +355,7 @@ def main():
     if rank == 0:
         line = {"metric": "GCUPS", "value": value, "unit": "GCUPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong" if strong else "weak",
-                "vs_baseline": None, "dtype": "i32" if width == 1 else "f16x2", "data": "synthetic",
+                "vs_baseline": None, "dtype": dtype, "data": "synthetic",
                 "config": {"workload": args.workload, "pairs_per_gpu": n, "read_length": L if L else "pareto 100..%d" % args.cap,
                            "align_type": cfg["align_type"],
                            "gap_model": cfg["gap_model"], "scheme": list(cfg["scheme"]),

@@ -44,6 +44,8 @@ struct LongParams {
     int2* bnd;             // per block: (NW + 1) border columns of bnd_rows entries {T - gamma, H}
     int64_t bnd_rows;
     unsigned int* queue;   // work queue head, zeroed before the launch
+    int32_t* redo; int32_t* redo_count;   // packed int16 kernel (score_long16.cuh): pairs handed back to this kernel
+    const int32_t* n_units_dev;           // re-score launch: number of units is read from the device
     int32_t* cflags;       // cluster launches: per cluster 160 ints (progress counters of its warps, unit slot, reduction slots)
     int32_t one;           // 1, opaque to the compiler: keeps selected adds on the FMA pipe as IMAD
 };
@@ -114,7 +116,7 @@ __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long_kernel(const Lo
             __syncthreads();
         }
         const int64_t u = s_unit;
-        if (u >= prm.n_units) break;
+        if (u >= (prm.n_units_dev ? (int64_t)*prm.n_units_dev : prm.n_units)) break;
         const int p = prm.units[u];
         const int qa = prm.pair_q[p], sb = prm.pair_s[p];
         const int m = prm.q_len[qa], n = prm.s_len[sb];

@@ -6,6 +6,7 @@
 #include "score_short.cuh"
 #include "score_short16.cuh"
 #include "score_long.cuh"
+#include "score_long16.cuh"
 #include "traceback_kernels.cuh"
 
 #include <cuda_runtime.h>
@@ -83,6 +84,7 @@ struct LaunchGroup {  // pairs that run in one kernel launch
     int64_t unit_off = 0;  // offset (in int32) into the plan's unit array; -1 = identity mapping
     int max_m = 0, max_n = 0;
     int long_nw = 0;       // > 0: long-read kernel with this many warps per block (score_long.cuh)
+    bool long16 = false;   // long-read kernel, packed int16: units are two pairs of identical shape (score_long16.cuh)
     int cluster = 1;       // long-read kernel: thread blocks per pair (a cluster of 2, 4 or 8 for the giants of a batch)
 };
 
@@ -107,6 +109,7 @@ struct wsb_batch {
     const Plan* last_plan = nullptr;
     void* d_bnd = nullptr;
     size_t bnd_bytes = 0;
+    int32_t* d_redo_long = nullptr;   // packed int16 long-read kernel: same, re-scored by the int32 long-read kernel
     int32_t* d_redo = nullptr;   // packed int16 kernel: list of pairs to re-score (slot 0 = count, list from slot 4)
     // Piecewise upload: piece k covers pairs [piece_end[k-1], piece_end[k]) and is complete (pools included) once
     // piece_ev[k] has fired on the copy stream; the first score call after creation launches piece by piece.
@@ -295,7 +298,7 @@ extern "C" void wsb_batch_destroy(wsb_batch* b) {
     for (int k = 0; k < wsb_batch::kMaxPieces; ++k) if (b->piece_ev[k]) cudaEventDestroy(b->piece_ev[k]);
     for (void* p : {(void*)b->d_qcodes, (void*)b->d_scodes, (void*)b->d_qoff, (void*)b->d_soff, (void*)b->d_qlen,
                     (void*)b->d_slen, (void*)b->d_pq, (void*)b->d_ps, (void*)b->d_score, (void*)b->d_i, (void*)b->d_j,
-                    b->d_bnd, (void*)b->d_redo, b->stage_blocks[0], b->stage_blocks[1], b->stage_blocks[2], b->stage_blocks[3]})
+                    b->d_bnd, (void*)b->d_redo, (void*)b->d_redo_long, b->stage_blocks[0], b->stage_blocks[1], b->stage_blocks[2], b->stage_blocks[3]})
         if (p) b->ctx->release(p);
     for (auto& kv : b->plans) if (kv.second.d_units) cudaFree(kv.second.d_units);
     b->tb.release();
@@ -644,6 +647,19 @@ template <int P, int K> static KernelSel pick_short16(int gap) {
     return {s16_local_short_kernel<P, K, GAP_MERGED>, short16_smem_bytes<P, K>()};
 }
 
+template <int GAP> static LongFn pick_long16_atype(int atype) {
+    switch (atype) {
+        case AT_GLOBAL: return score_long16_kernel<AT_GLOBAL, GAP>;
+        case AT_LOCAL: return score_long16_kernel<AT_LOCAL, GAP>;
+        default: return score_long16_kernel<AT_SEMI, GAP>;
+    }
+}
+static LongFn pick_long16(int atype, int gap) {
+    if (gap == GAP_LINEAR) return pick_long16_atype<GAP_LINEAR>(atype);
+    if (gap == GAP_MERGED) return pick_long16_atype<GAP_MERGED>(atype);
+    return nullptr;
+}
+
 // short_ok: every unit of the launch fits one stage and the short kernel's query buffer
 static KernelSel pick_kernel(int variant, int shape, int atype, int gap, bool masked, bool short_ok, bool wide) {
     static const char* no_short = getenv("WSB_NO_SHORT");  // tuning aid: force the general kernel
@@ -689,6 +705,7 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
     const int gap_i32 = !affine ? GAP_LINEAR : (wsb_merged_state_exact(sch) ? GAP_MERGED : GAP_EXACT);
     const int gap_f16 = !affine ? GAP_LINEAR : GAP_MERGED;
     const int ms = max_step(sch);
+    const int beta_eff_plan = affine ? sch->gap_extend : sch->gap_open;
     const bool wide_scheme = std::abs(sch->match - sch->mismatch) > 127;
     const bool s16_ok = want_s16 && atype == AT_LOCAL && f16_scheme_ok && std::abs(sch->match) <= 127 &&
                         std::abs(sch->mismatch) <= 127;
@@ -764,13 +781,39 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
     // giants of a skewed batch get up to 16 warps), beyond that the cheapest count in warp-iterations wins (pipeline
     // fill of ~80 rows per extra warp, idle warps when the stage count is not a multiple).
     if (!long_pairs.empty()) {
+        // Packed int16 units: two long pairs of identical shape whose values fit 16 bits run in the halves of one
+        // register set (score_long16.cuh); everything else runs one pair per block / cluster in int32.
+        static const char* no_l16 = getenv("WSB_NO_LONG16");  // tuning aid
+        const bool l16_scheme = variant == WSB_VARIANT_AUTO && !(no_l16 && no_l16[0]);
+        std::vector<int64_t> cand, singles;
+        for (int64_t p : long_pairs) {
+            // 16-bit value range: scores rise by at most match per diagonal step, and no value falls below the all-gap
+            // path (2 alpha + beta (m + n)) by more than one open / mismatch (local: nothing falls below -alpha)
+            const int64_t mm = b->m[p], nn = b->n[p];
+            const int64_t hi = (int64_t)std::max(sch->match, 0) * std::min(mm, nn) + sch->gap_open + beta_eff_plan;
+            const int64_t lo = atype == AT_LOCAL ? sch->gap_open
+                                                 : 3ll * sch->gap_open + (int64_t)beta_eff_plan * (mm + nn) + std::abs(sch->mismatch);
+            const bool fits16 = l16_scheme && hi <= 32000 && lo <= 32000;
+            (fits16 ? cand : singles).push_back(p);
+        }
+        std::stable_sort(cand.begin(), cand.end(), [&](int64_t x, int64_t y) {
+            if (b->n[x] != b->n[y]) return b->n[x] > b->n[y];
+            return b->m[x] > b->m[y];
+        });
+        std::vector<std::pair<int64_t, int64_t>> twins;   // units of the packed kernel
+        for (size_t k = 0; k < cand.size();) {
+            if (k + 1 < cand.size() && b->n[cand[k]] == b->n[cand[k + 1]] && b->m[cand[k]] == b->m[cand[k + 1]]) {
+                twins.emplace_back(cand[k], cand[k + 1]); k += 2;
+            } else { singles.push_back(cand[k]); ++k; }
+        }
         // class index = log2(warps per pair): 0..4 -> 1..16 warps in one block, 5..7 -> clusters of 2, 4, 8 blocks x 16 warps
         std::vector<int64_t> by_class[8];
+        std::vector<std::pair<int64_t, int64_t>> twins_by_class[5];
         const double machine_warps = (double)ctx->sm_count * 20.0;
         const double makespan = std::max(long_iters / machine_warps, 1.0);
         static const char* no_cluster = getenv("WSB_NO_CLUSTER");  // tuning aid
         const int max_class = (no_cluster && no_cluster[0]) ? 4 : 7;
-        for (int64_t p : long_pairs) {
+        auto pick_class = [&](int64_t p, int top) {
             const int stages = (b->n[p] + kLongW - 1) / kLongW;
             const double t1 = (double)stages * (b->m[p] + 31);
             // warps per pair come from powers of two: blocks then spread evenly over the four schedulers of an SM
@@ -778,11 +821,11 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
             // dominate the batch would queue behind each other in half-idle clusters
             const double share_cap = std::max(1.0, 2.0 * t1 / std::max(long_iters, 1.0) * machine_warps);
             int lo = 0;
-            while (lo < max_class && (2 << lo) <= stages && (lo < 4 || (double)(2 << lo) <= share_cap) &&
+            while (lo < top && (2 << lo) <= stages && (lo < 4 || (double)(2 << lo) <= share_cap) &&
                    t1 / (1 << lo) > 0.25 * makespan) ++lo;
             int best = lo;
             double best_cost = 1e300;
-            for (int c = lo; c <= std::min(lo + 1, std::min(max_class, 4)); ++c) {   // one block: also weigh the next size up
+            for (int c = lo; c <= std::min(lo + 1, std::min(top, 4)); ++c) {   // one block: also weigh the next size up
                 const int nw = 1 << c;
                 if (nw > stages) break;
                 const double rounds = (double)((stages + nw - 1) / nw);
@@ -790,7 +833,25 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
                 if (cost < best_cost * 0.999) { best_cost = cost; best = c; }
             }
             if (lo > 4) best = lo;
-            by_class[best].push_back(p);
+            return best;
+        };
+        for (int64_t p : singles) by_class[pick_class(p, max_class)].push_back(p);
+        for (auto& tw : twins) twins_by_class[pick_class(tw.first, 4)].push_back(tw);
+        for (int c = 4; c >= 0; --c) {
+            auto& v = twins_by_class[c];
+            if (v.empty()) continue;
+            std::stable_sort(v.begin(), v.end(), [&](const std::pair<int64_t, int64_t>& x, const std::pair<int64_t, int64_t>& y) {
+                return by_work(x.first, y.first);
+            });
+            LaunchGroup g;
+            g.variant = WSB_VARIANT_I32; g.shape = 2; g.gap = gap_i32; g.long_nw = 1 << c; g.long16 = true;
+            g.unit_off = (int64_t)units.size();
+            g.n_units = (int64_t)v.size();
+            for (auto& tw : v) {
+                g.max_m = std::max(g.max_m, b->m[tw.first]); g.max_n = std::max(g.max_n, b->n[tw.first]);
+                units.push_back((int32_t)tw.first); units.push_back((int32_t)tw.second);
+            }
+            plan.groups.push_back(g);
         }
         for (int c = 7; c >= 0; --c) {
             auto& v = by_class[c];
@@ -893,13 +954,18 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
     const Plan& plan = it->second;
     b->last_plan = &plan;
 
+    bool any_l16 = false;
+    int l16_gap = GAP_MERGED;
+    int64_t l16_rows = 0;
+    size_t l16_bnd_off = 0;
+    const int l16_redo_nw = 4, l16_redo_grid = ctx->sm_count * 2;
     // launch geometry + border scratch (every launch group owns a slice: long-read groups run concurrently)
     struct Geo { KernelFn fn; LongFn lfn; size_t smem; int grid; int64_t bnd_rows; size_t bnd_off; };
     std::vector<Geo> geo;
     size_t bnd_need = 0;
     for (const LaunchGroup& g : plan.groups) {
         if (g.long_nw > 0) {
-            LongFn lfn = pick_long(atype, g.gap, g.cluster > 1);
+            LongFn lfn = g.long16 ? pick_long16(atype, g.gap) : pick_long(atype, g.gap, g.cluster > 1);
             if (!lfn) return WSB_E_SCHEME;
             int grid = 1;
             if (g.cluster > 1) {  // one pair per cluster: as many clusters as the device can co-schedule
@@ -943,12 +1009,22 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
         geo.push_back({fn, nullptr, sel.smem, grid, rows, bnd_need});
         bnd_need += ((size_t)rows * 8u * (size_t)grid * gpb + 255) / 256 * 256;
     }
+    {   // the packed int16 long-read kernel may hand pairs back: scratch for their int32 re-score launch
+        int64_t rows16 = 0;
+        for (size_t k = 0; k < plan.groups.size(); ++k) if (plan.groups[k].long16) rows16 = std::max(rows16, geo[k].bnd_rows);
+        if (rows16 > 0 && !plan_only) {
+            l16_bnd_off = bnd_need;
+            bnd_need += (size_t)rows16 * sizeof(int2) * (size_t)(l16_redo_nw + 1) * (size_t)l16_redo_grid;
+            if (!b->d_redo_long) CUDA_TRY(ctx, ctx->alloc((void**)&b->d_redo_long, sizeof(int32_t) * (size_t)(b->n_pairs + 8)));
+            CUDA_TRY(ctx, cudaMemsetAsync(b->d_redo_long, 0, 16, ctx->stream));
+        }
+    }
     if (bnd_need > b->bnd_bytes) {
         if (b->d_bnd) { ctx->release(b->d_bnd); b->d_bnd = nullptr; b->bnd_bytes = 0; }
         CUDA_TRY(ctx, ctx->alloc(&b->d_bnd, bnd_need));
         b->bnd_bytes = bnd_need;
     }
-    if (plan.groups.size() > 64) return WSB_E_ARG;  // cannot happen: at most 16 + 10 launch groups per plan
+    if (plan.groups.size() > 63) return WSB_E_ARG;  // cannot happen: at most 16 + 10 launch groups per plan
     CUDA_TRY(ctx, cudaMemsetAsync(ctx->d_queues, 0, 64 * sizeof(unsigned int), ctx->stream));
 
     // first call after creation: the uploads may still be in flight on the copy stream
@@ -983,6 +1059,8 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
             lp.match = sch->match; lp.mismatch = sch->mismatch; lp.alpha = sch->gap_open; lp.beta = beta_eff;
             lp.bnd = reinterpret_cast<int2*>((char*)b->d_bnd + geo[k].bnd_off); lp.bnd_rows = geo[k].bnd_rows;
             lp.queue = ctx->d_queues + k; lp.one = 1;
+            lp.redo = b->d_redo_long ? b->d_redo_long + 4 : nullptr; lp.redo_count = b->d_redo_long; lp.n_units_dev = nullptr;
+            if (g.long16) { any_l16 = true; l16_gap = g.gap; l16_rows = std::max(l16_rows, geo[k].bnd_rows); }
             lp.cflags = ctx->d_cflags + (size_t)256 * 160 * (size_t)(g.cluster == 2 ? 0 : g.cluster == 4 ? 1 : 2);
             if (g.cluster > 1) {
                 cudaLaunchConfig_t cfg = {};
@@ -1055,6 +1133,22 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
             CUDA_TRY(ctx, cudaEventRecord(ctx->aux_done[a], ctx->aux[a]));
             CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, ctx->aux_done[a], 0));
         }
+    if (any_l16) {   // pairs the packed int16 long-read kernel handed back (flagged subject symbols): int32 long-read kernel
+        LongFn lfn = pick_long(atype, l16_gap, false);
+        if (!lfn) return WSB_E_SCHEME;
+        LongParams lp = {};
+        lp.q_codes = b->d_qcodes; lp.q_off = b->d_qoff; lp.q_len = b->d_qlen;
+        lp.s_codes = b->d_scodes; lp.s_off = b->d_soff; lp.s_len = b->d_slen;
+        lp.pair_q = b->d_pq; lp.pair_s = b->d_ps;
+        lp.units = b->d_redo_long + 4; lp.n_units = 0; lp.n_units_dev = b->d_redo_long;
+        lp.out_score = b->d_score; lp.out_i = b->d_i; lp.out_j = b->d_j;
+        lp.match = sch->match; lp.mismatch = sch->mismatch; lp.alpha = sch->gap_open; lp.beta = beta_eff;
+        lp.bnd = reinterpret_cast<int2*>((char*)b->d_bnd + l16_bnd_off); lp.bnd_rows = l16_rows;
+        lp.queue = ctx->d_queues + 63; lp.one = 1; lp.cflags = ctx->d_cflags;
+        lfn<<<l16_redo_grid, l16_redo_nw * 32, 0, ctx->stream>>>(lp);
+        CUDA_TRY(ctx, cudaGetLastError());
+        ++launches;
+    }
     {  // empty-side pairs (only possible for non-uniform batches or a uniform batch of empties)
         bool any_empty = false;
         if (b->uniform) any_empty = b->m[0] == 0 || b->n[0] == 0;

@@ -225,3 +225,30 @@ def test_packed_int16_variant_equals_oracle_including_flagged_subjects(ctx, gap_
     # other alignment types: S16X2 is simply AUTO
     assert_scores_equal(gpu_scores(ctx, qs[:200], ss[:200], pairs[:200], scheme, "global", "s16x2"),
                         oracle_scores(qs[:200], ss[:200], pairs[:200], scheme, "global"), "s16x2 global")
+
+
+@pytest.mark.parametrize("align_type,gap_model", COMBOS)
+def test_packed_int16_long_read_kernel_twins_and_hand_backs(ctx, align_type, gap_model):
+    """Long pairs of identical shape run two per block in packed int16 (score_long16.cuh); pairs whose subject holds a
+    flagged symbol are handed back to the int32 kernel inside the same call; odd counts leave a single."""
+    rng = np.random.default_rng(1616)
+    scheme = scheme_of((2, -1, 2, 1) if gap_model == "affine" else (2, -1, 2, 2), gap_model)
+    qs, ss = [], []
+    for (m, n, count) in ((1100, 1300, 5), (2600, 2600, 4), (700, 3100, 3), (4000, 1024, 2)):
+        for k in range(count):
+            q = random_codes(rng, m)
+            s = random_codes(rng, n)
+            if k % 2 == 0:
+                at = int(rng.integers(0, max(1, n - m))) if n > m else 0
+                piece = mutate_codes(rng, q, 0.05, 0.0, 0.0)[:min(m, n - at)]
+                s[at:at + len(piece)] = piece
+            qs.append(q); ss.append(s)
+    ss[1] = ss[1].copy(); ss[1][700] = 4          # flagged subject symbol: hand-back
+    qs[6] = qs[6].copy(); qs[6][1234] = 4         # flagged query symbol: exact in the packed kernel
+    ss[10] = ss[10].copy(); ss[10][3000] = 4; qs[10] = qs[10].copy(); qs[10][5] = 4
+    pairs = [(i, i) for i in range(len(qs))]
+    want = oracle_scores(qs, ss, pairs, scheme, align_type)
+    got = gpu_scores(ctx, qs, ss, pairs, scheme, align_type, "auto")
+    assert_scores_equal(got, want, f"long16 {align_type}/{gap_model}")
+    i32 = gpu_scores(ctx, qs, ss, pairs, scheme, align_type, "i32")
+    assert_scores_equal(i32, want, f"long int32 {align_type}/{gap_model}")
