@@ -221,7 +221,9 @@ template <int K> __device__ __forceinline__ void record_rows(const __half2 (&hm)
     }
 }
 
-template <int P, int K, int GAP>
+// LISTED = true: re-score launch behind the packed int16 kernel (unit list and its length live on the device); kept
+// out of the main instantiation so that the headline kernel's code is untouched by it
+template <int P, int K, int GAP, bool LISTED = false>
 #ifdef WSB_SHORT_MINB
 __global__ void __launch_bounds__(kThreads, (K <= 20 ? WSB_SHORT_MINB : 1)) f16_local_short_kernel(const ScoreParams prm) {
 #else
@@ -262,8 +264,8 @@ __global__ void __launch_bounds__(kThreads) f16_local_short_kernel(const ScorePa
     const int col0 = t * K;
 
     // re-score launch behind the packed int16 kernel: the unit list and its length live on the device
-    const int64_t listed = prm.n_pairs_dev ? (int64_t)*prm.n_pairs_dev : 0;
-    const int64_t n_units = prm.n_pairs_dev ? (listed + 1) / 2 : prm.n_units;
+    const int64_t listed = LISTED ? (int64_t)*prm.n_pairs_dev : 0;
+    const int64_t n_units = LISTED ? (listed + 1) / 2 : prm.n_units;
     const int64_t rounds = (n_units + n_groups - 1) / n_groups;
     for (int64_t rd = 0; rd < rounds; ++rd) {
         const int64_t u = rd * n_groups + group_global;
@@ -275,7 +277,7 @@ __global__ void __launch_bounds__(kThreads) f16_local_short_kernel(const ScorePa
         for (int v = 0; v < 2; ++v) {
             int p = -1;
             if (u < n_units) {
-                if (prm.n_pairs_dev) p = u * 2 + v < listed ? prm.units[u * 2 + v] : -1;
+                if (LISTED) p = u * 2 + v < listed ? prm.units[u * 2 + v] : -1;
                 else if (prm.units) p = prm.units[u * 2 + v];
                 else { const int64_t pp = prm.pair_base + u * 2 + v; p = pp < prm.n_pairs ? (int)pp : -1; }
             }

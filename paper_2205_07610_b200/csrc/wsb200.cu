@@ -1113,7 +1113,9 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
         ++launches;
     }
     if (any_s16) {   // re-score what the packed int16 kernel could not encode, with the half2 short kernel
-        const KernelSel sel = pick_short<8, 19>(s16_gap);
+        const KernelSel sel = s16_gap == GAP_LINEAR
+            ? KernelSel{f16_local_short_kernel<8, 19, GAP_LINEAR, true>, short_smem_bytes<8, 19>()}
+            : KernelSel{f16_local_short_kernel<8, 19, GAP_MERGED, true>, short_smem_bytes<8, 19>()};
         CUDA_TRY(ctx, cudaFuncSetAttribute(sel.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel.smem));
         ScoreParams prm = {};
         prm.q_codes = b->d_qcodes; prm.q_off = b->d_qoff; prm.q_len = b->d_qlen;
