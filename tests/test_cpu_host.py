@@ -228,3 +228,23 @@ def test_packed_pool_round_trip_matches_reference_layout():
     assert (packed.codes == codes).all()
     seq = packed[5]
     assert len(seq) == lens[5]
+
+
+def test_wire_formats_and_bench_conventions(tmp_path):
+    """cigar_string / write_results_tsv (io.py:80-110) and median_rate / theoretical_peak (bench.py:30-43) conventions."""
+    import paper_2205_07610_b200 as W
+    r = W.AlignmentResult(score=5, q_start=0, q_end=4, s_start=0, s_end=3, ops=[("M", 1), ("I", 1), ("M", 1), ("M", 1)],
+                          cells_computed=12)
+    assert W.cigar_string(r) == "1M1I2M"
+    assert W.cigar_string(W.AlignmentResult(3, 1, 1, 2, 2, None, 4)) == ""
+    path = tmp_path / "out.tsv"
+    W.write_results_tsv([("q0", "s0", r)], path)
+    lines = path.read_text().splitlines()
+    assert lines[0].split("\t") == list(W.TSV_HEADER) and lines[1] == "q0\ts0\t5\t0\t4\t0\t3\t1M1I2M"
+    assert W.median_rate([3.0, 1.0, 2.0]) == 2.0 and W.median_rate([4.0, 1.0, 2.0, 3.0]) == 2.5
+    with pytest.raises(ValueError):
+        W.median_rate([])
+    hw = W.HardwareModel.b200(ops_per_cell=8, cells_per_instruction=2)
+    assert abs(W.theoretical_peak(hw) - 9306.24) < 0.01
+    with pytest.raises(ValueError):
+        W.HardwareModel(0, 1.0, 1.0)
