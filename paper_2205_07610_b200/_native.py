@@ -24,7 +24,7 @@ EXPORTED_SYMBOLS = (
     "wsb_ctx_sm_count", "wsb_batch_create", "wsb_batch_create_async", "wsb_batch_create_packed_async", "wsb_batch_destroy", "wsb_batch_score", "wsb_batch_fetch_scores",
     "wsb_batch_traceback", "wsb_batch_fetch_traceback", "wsb_batch_total_cells", "wsb_score_batch",
     "wsb_traceback_batch", "wsb_merged_state_exact", "wsb_f16_range_ok", "wsb_plan_shards", "wsb_batch_has_faults", "wsb_pinned_alloc",
-    "wsb_pinned_free",
+    "wsb_pinned_free", "wsb_batch_total_runs",
 )
 
 
@@ -71,6 +71,8 @@ def load():
     lib.wsb_score_batch.argtypes = [p, p, ci, ci, p, p, p, i64, p, p, p, i64, p, p, i64, p, p, p, p]
     lib.wsb_traceback_batch.argtypes = [p, p, ci, p, p, p, i64, p, p, p, i64, p, p, i64, p, p, p, p, p, p, i64, p, p]
     lib.wsb_batch_has_faults.argtypes = [p]
+    lib.wsb_batch_total_runs.argtypes = [p]
+    lib.wsb_batch_total_runs.restype = i64
     lib.wsb_pinned_alloc.argtypes = [ctypes.c_size_t, p]
     lib.wsb_pinned_free.argtypes = [p]
     lib.wsb_pinned_free.restype = None
@@ -258,20 +260,21 @@ class Batch:
 
     def fetch_traceback(self, cigar_cap: int | None = None):
         n = self.n_pairs
-        out = {k: np.empty(n, np.int32) for k in ("score", "q_start", "q_end", "s_start", "s_end", "status")}
-        off = np.zeros(n + 1, np.int64)
-        cap = int(cigar_cap) if cigar_cap is not None else max(16 * n, 1024)
-        while True:
-            cig = np.empty(cap, np.uint32)
-            rc = self._lib.wsb_batch_fetch_traceback(self._h, _ptr(out["score"]), _ptr(out["q_start"]),
-                                                     _ptr(out["q_end"]), _ptr(out["s_start"]), _ptr(out["s_end"]),
-                                                     _ptr(cig), cap, _ptr(off), _ptr(out["status"]))
-            if rc == WSB_E_CAPACITY and cigar_cap is None:
-                cap = int(off[n])
-                continue
-            if rc:
-                raise status_exception(rc, self.ctx.last_error())
-            break
+        big = n >= 65536
+        alloc = pinned_empty if big else (lambda k, dt=np.int32: np.empty(k, dt))
+        out = {k: alloc(n) for k in ("score", "q_start", "q_end", "s_start", "s_end")}
+        self.has_faults = bool(self._lib.wsb_batch_has_faults(self._h))
+        status = np.empty(n, np.int32) if self.has_faults else None
+        off = alloc(n + 1, np.int64)
+        total = int(self._lib.wsb_batch_total_runs(self._h))
+        cap = int(cigar_cap) if cigar_cap is not None else max(total, 1)   # exact: one download, no retry
+        cig = alloc(cap, np.uint32)
+        rc = self._lib.wsb_batch_fetch_traceback(self._h, _ptr(out["score"]), _ptr(out["q_start"]), _ptr(out["q_end"]),
+                                                 _ptr(out["s_start"]), _ptr(out["s_end"]), _ptr(cig), cap, _ptr(off),
+                                                 _ptr(status))
+        if rc:
+            raise status_exception(rc, self.ctx.last_error())
+        out["status"] = status if status is not None else np.zeros(n, np.int32)
         out["cigar"] = cig[:int(off[n])]
         out["cigar_off"] = off
         return out

@@ -190,6 +190,7 @@ def _run_shard(device: int, queries: SequencePool, subjects: SequencePool, pair_
             if cfg.result_mode == "traceback":
                 out["ms"], out["launches"] = batch.traceback(scheme, cfg.align_type)
                 out["tb"] = batch.fetch_traceback()
+                out["faults"] = batch.has_faults
             else:
                 out["ms"], out["launches"] = batch.score(scheme, cfg.align_type, variant)
                 out["scores"] = batch.fetch_scores()
@@ -262,6 +263,10 @@ def run_batch(job: BatchJob) -> BatchReport:
         ss = np.zeros(n, np.int32); se = np.empty(n, np.int32); status = np.zeros(n, np.int32)
     if single and cfg.result_mode != "traceback":
         pass
+    elif cfg.result_mode == "traceback" and single:   # one shard: the fetched arrays are the result arrays
+        tb = outs[0]["tb"]
+        score, qs, qe, ss, se, status = tb["score"], tb["q_start"], tb["q_end"], tb["s_start"], tb["s_end"], tb["status"]
+        runs, run_off = tb["cigar"], tb["cigar_off"]
     elif cfg.result_mode == "traceback":
         counts = np.zeros(n, np.int64)
         for idx, out in zip(shard_index, outs):
@@ -291,7 +296,7 @@ def run_batch(job: BatchJob) -> BatchReport:
             score[idx], qe[idx], se[idx], status[idx] = sc_, ei, ej, st
         if cfg.align_type != "global":  # start is unknown without a traceback pass: both span ends carry the argmax cell (batch.py:111-115)
             qs[:] = qe; ss[:] = se
-    any_fault = cfg.result_mode == "traceback" or any(o.get("faults", True) for o in outs if o)
+    any_fault = any(o.get("faults", True) for o in outs if o)
     bad = np.nonzero(status)[0] if any_fault else ()
     if len(bad):
         i = int(bad[0])

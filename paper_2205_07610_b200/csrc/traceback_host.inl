@@ -224,6 +224,8 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
     return status;
 }
 
+extern "C" int64_t wsb_batch_total_runs(const wsb_batch* b) { return (b && b->tb.valid) ? b->tb.total_runs : -1; }
+
 extern "C" int wsb_batch_fetch_traceback(wsb_batch* b, int32_t* out_score, int32_t* q_start, int32_t* q_end,
                                          int32_t* s_start, int32_t* s_end, uint32_t* cigar, int64_t cigar_cap,
                                          int64_t* cigar_off, int32_t* status) {
