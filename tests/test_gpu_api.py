@@ -142,3 +142,34 @@ def test_packed_pools_give_identical_results():
                     assert (getattr(ra, f) == getattr(rb, f)).all(), (flagged, cfg.align_type, f)
                 if ra.runs is not None:
                     assert (ra.runs == rb.runs).all() and (ra.run_off == rb.run_off).all()
+
+
+@pytest.mark.parametrize("result_mode", ["score_only", "traceback"])
+def test_multi_shard_assembly_on_one_gpu(monkeypatch, result_mode):
+    """run_batch(devices=[...]) with three shards: every shard gets its own context (here all on GPU 0, one context per
+    shard thread) and the results are scattered back into pair order, identical to the single-shard run."""
+    from paper_2205_07610_b200 import _native as N, batch as B
+    rng = np.random.default_rng(33)
+    n = 900
+    lens = rng.integers(30, 400, n)
+    qs = [rng.integers(0, 4, int(L)).astype(np.uint8) for L in lens]
+    ss = [rng.integers(0, 4, int(L * rng.uniform(0.7, 1.3)) + 1).astype(np.uint8) for L in lens]
+
+    def pool(seqs):
+        ln = np.array([len(s) for s in seqs], np.int32)
+        off = np.zeros(len(seqs), np.int64); off[1:] = np.cumsum(ln[:-1])
+        return W.SequencePool(np.concatenate(seqs), off, ln)
+
+    pairs = np.stack([rng.permutation(n), rng.permutation(n)], 1).astype(np.int32)
+    cfg = W.AlignConfig("local" if result_mode == "score_only" else "semiglobal", "affine", result_mode)
+    job1 = W.BatchJob(pool(qs), pool(ss), pairs, cfg, W.ScoringScheme(), devices=[0])
+    one = W.run_batch(job1)
+    made = []
+    monkeypatch.setattr(B, "get_context", lambda device: made.append(N.Context(0)) or made[-1])
+    job3 = W.BatchJob(pool(qs), pool(ss), pairs, cfg, W.ScoringScheme(), devices=[0, 0, 0])
+    three = W.run_batch(job3)
+    assert len(made) == 3 and len(three.shard_cells) == 3 and sum(three.shard_cells) == one.total_cells == three.total_cells
+    assert max(three.shard_cells) - min(three.shard_cells) <= 400 * 520     # balanced to within one large pair
+    assert list(one.results) == list(three.results)
+    for c in made:
+        c.close()
