@@ -96,6 +96,7 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
     float total_ms = score_ms;
     int launches = score_launches;
     uint32_t* d_codes = nullptr;
+    uint32_t* d_run_tmp = nullptr;
     int64_t* d_code_off = nullptr;
     int32_t* d_cnt = nullptr;
     int64_t* d_chunk_off = nullptr;
@@ -107,6 +108,7 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
     int status = WSB_OK;
     auto cleanup = [&]() {
         if (d_codes) cudaFree(d_codes);
+        if (d_run_tmp) cudaFree(d_run_tmp);
         if (d_code_off) cudaFree(d_code_off);
         if (d_cnt) cudaFree(d_cnt);
         if (d_chunk_off) cudaFree(d_chunk_off);
@@ -146,7 +148,9 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
             if (d_code_off) cudaFree(d_code_off);
             if (d_cnt) cudaFree(d_cnt);
             if (d_chunk_off) cudaFree(d_chunk_off);
-            d_code_off = nullptr; d_cnt = nullptr; d_chunk_off = nullptr;
+            if (d_run_tmp) cudaFree(d_run_tmp);
+            d_code_off = nullptr; d_cnt = nullptr; d_chunk_off = nullptr; d_run_tmp = nullptr;
+            TB_TRY(cudaMalloc((void**)&d_run_tmp, sizeof(uint32_t) * (size_t)kTbTmpRuns * (size_t)count));
             TB_TRY(cudaMalloc((void**)&d_code_off, sizeof(int64_t) * (size_t)count));
             TB_TRY(cudaMalloc((void**)&d_cnt, sizeof(int32_t) * (size_t)(count + 1)));
             TB_TRY(cudaMalloc((void**)&d_chunk_off, sizeof(int64_t) * (size_t)(count + 1)));
@@ -173,7 +177,7 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
         prm.end_i = b->d_i; prm.end_j = b->d_j; prm.start_i = tb.d_qs; prm.start_j = tb.d_ss;
         prm.w_score = b->d_score; prm.w_i = b->d_i; prm.w_j = b->d_j;
         prm.n_runs = d_cnt; prm.run_off = d_chunk_off; prm.runs = nullptr;
-        prm.tb_p = P; prm.tb_k = K; prm.one = 1;
+        prm.tb_p = P; prm.tb_k = K; prm.one = 1; prm.run_tmp = d_run_tmp;
 
         TB_TRY(cudaEventRecord(e0, ctx->stream));
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((count + gpb - 1) / gpb, max_grid));

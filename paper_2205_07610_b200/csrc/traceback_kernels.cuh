@@ -45,6 +45,8 @@ struct TbParams {
     uint32_t* runs;                               // out (pass 2): runs of the launch, forward order
     int32_t tb_p, tb_k;                           // lane-group shape the codes were written with
     int32_t one;                                  // 1, opaque to the compiler (keeps plane-bit adds on the FMA pipe)
+    uint32_t* run_tmp;                            // pass 1 parks up to kTbTmpRuns runs per pair here (reverse order), so
+                                                  // that pass 2 is a copy for all but the most fragmented alignments
 };
 
 // code block geometry shared by fill and walk
@@ -282,7 +284,10 @@ __device__ __forceinline__ uint32_t tb_code_at(const uint32_t* code, int i, int 
     return origin | ((bits >> 14) & 4u) | ((bits >> 21) & 8u);
 }
 
-// PASS 1 counts the runs and records the start cell; PASS 2 writes the runs in forward order.
+constexpr int kTbTmpRuns = 64;
+
+// PASS 1 counts the runs, records the start cell and parks the first kTbTmpRuns runs (in walk order); PASS 2 writes the
+// runs in forward order: a reversed copy of the parked runs, or a second walk for alignments with more runs than that.
 template <int ATYPE, int PASS>
 __global__ void tb_walk_kernel(const TbParams prm) {
     const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -299,12 +304,23 @@ __global__ void tb_walk_kernel(const TbParams prm) {
     uint32_t* out = nullptr;
     int64_t w = 0;
     if (PASS == 2) { out = prm.runs + prm.run_off[u]; w = prm.n_runs[u]; }
+    uint32_t* tmp = prm.run_tmp ? prm.run_tmp + u * kTbTmpRuns : nullptr;
+    if (PASS == 2 && tmp && w <= kTbTmpRuns) {   // the walk of pass 1 already produced every run
+        for (int k = 0; k < (int)w; ++k) out[k] = tmp[w - 1 - k];
+        return;
+    }
     int count = 0;
     int cur_op = -1, cur_len = 0;
+    auto flush = [&]() {
+        const uint32_t word = ((uint32_t)cur_len << 2) | (uint32_t)cur_op;
+        if (PASS == 1 && tmp && count < kTbTmpRuns) tmp[count] = word;
+        ++count;
+        if (PASS == 2) out[--w] = word;
+    };
     auto emit = [&](int op, int len) {
         if (len <= 0) return;
         if (op == cur_op) { cur_len += len; return; }
-        if (cur_op >= 0) { ++count; if (PASS == 2) out[--w] = ((uint32_t)cur_len << 2) | (uint32_t)cur_op; }
+        if (cur_op >= 0) flush();
         cur_op = op; cur_len = len;
     };
     int state = 0;  // 0: at H, 1: inside a vertical run (E), 2: inside a horizontal run (F)
@@ -331,7 +347,7 @@ __global__ void tb_walk_kernel(const TbParams prm) {
         if (i == 0 && j > 0) { emit(2, j); j = 0; }
         else if (j == 0 && i > 0) { emit(1, i); i = 0; }
     }
-    if (cur_op >= 0) { ++count; if (PASS == 2) out[--w] = ((uint32_t)cur_len << 2) | (uint32_t)cur_op; }
+    if (cur_op >= 0) flush();
     if (PASS == 1) {
         prm.n_runs[u] = count;
         prm.start_i[p] = i;
