@@ -984,6 +984,8 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
                 int per_sm = 0;
                 CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lfn, g.long_nw * 32, 0));
                 per_sm = std::max(per_sm, 1);
+                static const char* occ = getenv("WSB_LONG_MAX_BLOCKS");  // tuning aid: cap resident blocks per SM
+                if (occ && occ[0]) per_sm = std::max(1, std::min(per_sm, atoi(occ)));
                 grid = (int)std::max<int64_t>(1, std::min<int64_t>(g.n_units, (int64_t)ctx->sm_count * per_sm));
             }
             const int64_t rows = ((int64_t)g.max_m + 31) / 32 * 32 + 64;
