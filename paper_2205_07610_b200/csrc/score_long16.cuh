@@ -65,7 +65,12 @@ __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long16_kernel(const 
             qp[v] = prm.q_codes + prm.q_off[prm.pair_q[pidx[v]]];
             sp[v] = prm.s_codes + prm.s_off[prm.pair_s[pidx[v]]];
         }
-        const int m = prm.q_len[prm.pair_q[pidx[0]]], n = prm.s_len[prm.pair_s[pidx[0]]];   // same for both pairs
+        // global / semiglobal: both pairs have the same shape (planner); local: shapes may differ, the unit runs
+        // max(m) x max(n) and the shorter alignment sees never-improving pad rows / columns beyond its own matrix
+        int mv[2], nv[2];
+#pragma unroll
+        for (int v = 0; v < 2; ++v) { mv[v] = prm.q_len[prm.pair_q[pidx[v]]]; nv[v] = prm.s_len[prm.pair_s[pidx[v]]]; }
+        const int m = max(mv[0], mv[1]), n = max(nv[0], nv[1]);
         const int nstages = (n + W - 1) / W;
 
         int best_v[2], best_i[2], best_j[2];
@@ -86,7 +91,7 @@ __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long16_kernel(const 
                 unsigned nib[2] = {0x88u, 0x88u};   // pad column: sign fill -> sigma in {0, -1}, never improving
 #pragma unroll
                 for (int v = 0; v < 2; ++v)
-                    if (col0 + c < n) {
+                    if (col0 + c < nv[v]) {
                         const unsigned x = sp[v][col0 + c];
                         if (x < 4) nib[v] = (x + 4u * v) | ((x + 4u * v) | 8u) << 4;
                         else flagged_subject = true;
@@ -118,9 +123,9 @@ __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long16_kernel(const 
             auto fetch_chunk = [&](int chunk) {
                 const int row0 = 32 * chunk;
                 if (row0 >= m) return;
-                const int idx = min(row0 + t, m - 1);
-                pre_a = row_word(qp[0][idx]);
-                pre_b = row_word(qp[1][idx]);
+                const int idx = row0 + t;   // rows beyond an alignment's own query are pads: mismatch against everything
+                pre_a = idx < mv[0] ? row_word(qp[0][idx]) : mism4;
+                pre_b = idx < mv[1] ? row_word(qp[1][idx]) : mism4;
                 if (!first) {
                     const int need = p_base + min(m, row0 + 32);
                     while (prog[pw_id] < need) __nanosleep(40);

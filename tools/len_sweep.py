@@ -13,7 +13,7 @@ for L in [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "300,400,512,60
     q = rng.integers(0, 4, n * L, dtype=np.uint8); s = rng.integers(0, 4, n * L, dtype=np.uint8)
     off = np.arange(n, dtype=np.int64) * L; ln = np.full(n, L, np.int32); idx = np.arange(n, dtype=np.int32)
     b = N.Batch(ctx, q, off, ln, s, off, ln, idx, idx)
-    best = min(b.score(sch, atype, "i32")[0] for _ in range(3))
+    best = min(b.score(sch, atype, os.environ.get("SWEEP_VARIANT", "i32"))[0] for _ in range(3))
     r = b.fetch_scores()
     print(f"{atype} L={L:6d} pairs={n:7d} {best:9.3f} ms {b.total_cells / best / 1e6:8.1f} GCUPS  checksum {int(r[0].astype(np.int64).sum())} {int(r[1].astype(np.int64).sum())} {int(r[2].astype(np.int64).sum())}", flush=True)
     b.close()
