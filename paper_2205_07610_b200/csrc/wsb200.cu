@@ -102,7 +102,15 @@ struct wsb_batch {
     int64_t *d_qoff = nullptr, *d_soff = nullptr;
     int32_t *d_qlen = nullptr, *d_slen = nullptr, *d_pq = nullptr, *d_ps = nullptr;
     int32_t *d_score = nullptr, *d_i = nullptr, *d_j = nullptr;
-    std::vector<int32_t> m, n;  // per pair lengths (host)
+    // per pair lengths (host).  Regular batches (pair i = (i, i), equal-length reads) keep one value instead of a vector.
+    struct LenVec {
+        std::vector<int32_t> v;
+        int32_t uni = -1;
+        int32_t operator[](int64_t p) const { return uni >= 0 ? uni : v[(size_t)p]; }
+        int32_t& slot(int64_t p) { return v[(size_t)p]; }
+        void resize(size_t k) { v.resize(k); }
+    };
+    LenVec m, n;
     bool uniform = false;       // every pair has the same (m, n)
     int64_t total_cells = 0;
     std::map<std::tuple<int, int, int, int, int, int, int>, Plan> plans;
@@ -346,40 +354,6 @@ static int batch_create_impl(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t
     if (!b) return WSB_E_NOMEM;
     b->ctx = ctx; b->n_q = n_q; b->n_s = n_s; b->n_pairs = n_pairs;
 
-    // per-pair lengths, index validation and the uniformity test, split over host threads
-    try { b->m.resize((size_t)n_pairs); b->n.resize((size_t)n_pairs); } catch (...) { delete b; return WSB_E_NOMEM; }
-    const int nthr = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency())), n_pairs / 65536 + 1));
-    std::vector<int> bad(nthr, 0), uni(nthr, 1);
-    std::vector<int64_t> cells(nthr, 0);
-    const int m0 = (pair_q[0] >= 0 && pair_q[0] < n_q) ? q_len[pair_q[0]] : -1;
-    const int n0 = (pair_s[0] >= 0 && pair_s[0] < n_s) ? s_len[pair_s[0]] : -1;
-    auto work = [&](int k) {
-        const int64_t lo = n_pairs * k / nthr, hi = n_pairs * (k + 1) / nthr;
-        int64_t acc = 0;
-        for (int64_t p = lo; p < hi; ++p) {
-            const int a = pair_q[p], c = pair_s[p];
-            if (a < 0 || a >= n_q || c < 0 || c >= n_s) { bad[k] = 1; b->m[p] = b->n[p] = 0; continue; }
-            const int mm = q_len[a], nn = s_len[c];
-            if (mm < 0 || nn < 0) { bad[k] = 1; continue; }
-            b->m[p] = mm; b->n[p] = nn;
-            acc += (int64_t)mm * nn;
-            if (mm != m0 || nn != n0) uni[k] = 0;
-        }
-        cells[k] = acc;
-    };
-    if (nthr == 1) work(0);
-    else {
-        std::vector<std::thread> th;
-        for (int k = 0; k < nthr; ++k) th.emplace_back(work, k);
-        for (auto& x : th) x.join();
-    }
-    b->uniform = true;
-    for (int k = 0; k < nthr; ++k) {
-        if (bad[k]) { delete b; return WSB_E_ARG; }
-        if (!uni[k]) b->uniform = false;
-        b->total_cells += cells[k];
-    }
-
     // metadata scans, one host thread each: furthest sequence end of either pool (pools need not be packed in order)
     // and the arithmetic-progression test of the six index / offset / length arrays
     int64_t q_total = 0, s_total = 0;
@@ -401,6 +375,48 @@ static int batch_create_impl(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t
             for (auto& x : th) x.join();
         } else { total_q(); total_s(); }
     }
+    // regular batch: identity pair list over equal-length reads -> nothing to validate or tabulate per pair
+    const bool regular = ap_pair[0] && p0[0] == 0 && pd[0] == 1 && ap_pair[1] && p0[1] == 0 && pd[1] == 1 && ap_len[0] &&
+                         ld[0] == 0 && ap_len[1] && ld[1] == 0 && n_pairs <= n_q && n_pairs <= n_s && l0[0] >= 0 && l0[1] >= 0;
+    // per-pair lengths, index validation and the uniformity test, split over host threads
+    if (!regular) {
+        try { b->m.resize((size_t)n_pairs); b->n.resize((size_t)n_pairs); } catch (...) { delete b; return WSB_E_NOMEM; }
+    }
+    const int nthr = regular ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency())), n_pairs / 65536 + 1));
+    std::vector<int> bad(nthr, 0), uni(nthr, 1);
+    std::vector<int64_t> cells(nthr, 0);
+    const int m0 = (pair_q[0] >= 0 && pair_q[0] < n_q) ? q_len[pair_q[0]] : -1;
+    const int n0 = (pair_s[0] >= 0 && pair_s[0] < n_s) ? s_len[pair_s[0]] : -1;
+    auto work = [&](int k) {
+        const int64_t lo = n_pairs * k / nthr, hi = n_pairs * (k + 1) / nthr;
+        int64_t acc = 0;
+        for (int64_t p = lo; p < hi; ++p) {
+            const int a = pair_q[p], c = pair_s[p];
+            if (a < 0 || a >= n_q || c < 0 || c >= n_s) { bad[k] = 1; b->m.slot(p) = b->n.slot(p) = 0; continue; }
+            const int mm = q_len[a], nn = s_len[c];
+            if (mm < 0 || nn < 0) { bad[k] = 1; continue; }
+            b->m.slot(p) = mm; b->n.slot(p) = nn;
+            acc += (int64_t)mm * nn;
+            if (mm != m0 || nn != n0) uni[k] = 0;
+        }
+        cells[k] = acc;
+    };
+    if (regular) {
+        b->m.uni = l0[0]; b->n.uni = l0[1];
+        cells[0] = (int64_t)n_pairs * l0[0] * l0[1];
+    } else if (nthr == 1) work(0);
+    else {
+        std::vector<std::thread> th;
+        for (int k = 0; k < nthr; ++k) th.emplace_back(work, k);
+        for (auto& x : th) x.join();
+    }
+    b->uniform = true;
+    for (int k = 0; k < nthr; ++k) {
+        if (bad[k]) { delete b; return WSB_E_ARG; }
+        if (!uni[k]) b->uniform = false;
+        b->total_cells += cells[k];
+    }
+
     // Pieces: the pairs are cut into up to eight ranges; piece k needs the pool bytes up to the furthest sequence end
     // any pair of pieces 0..k references, so the pools go up in address order, one slice per piece, and a piece can be
     // scored while the slices of later pieces are still on the bus.  (Arbitrary pair lists degrade gracefully: the
