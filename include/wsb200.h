@@ -130,6 +130,7 @@ int wsb_batch_has_faults(const wsb_batch* b);
 int wsb_pinned_alloc(size_t bytes, void** out);
 void wsb_pinned_free(void* block);
 
+int64_t wsb_batch_h2d_bytes(const wsb_batch* b);   /* bytes uploaded at creation (arrays generated on the device excluded) */
 int64_t wsb_batch_total_runs(const wsb_batch* b);  /* CIGAR runs of the last traceback (size the cigar buffer with it); -1 if none */
 int64_t wsb_batch_total_cells(const wsb_batch* b); /* sum of m*n over pairs (BatchReport.total_cells, batch.py:243-247) */
 

@@ -24,7 +24,7 @@ EXPORTED_SYMBOLS = (
     "wsb_ctx_sm_count", "wsb_batch_create", "wsb_batch_create_async", "wsb_batch_create_packed_async", "wsb_batch_destroy", "wsb_batch_score", "wsb_batch_fetch_scores",
     "wsb_batch_traceback", "wsb_batch_fetch_traceback", "wsb_batch_total_cells", "wsb_score_batch",
     "wsb_traceback_batch", "wsb_merged_state_exact", "wsb_f16_range_ok", "wsb_plan_shards", "wsb_batch_has_faults", "wsb_pinned_alloc",
-    "wsb_pinned_free", "wsb_batch_total_runs",
+    "wsb_pinned_free", "wsb_batch_total_runs", "wsb_batch_h2d_bytes",
 )
 
 
@@ -71,6 +71,8 @@ def load():
     lib.wsb_score_batch.argtypes = [p, p, ci, ci, p, p, p, i64, p, p, p, i64, p, p, i64, p, p, p, p]
     lib.wsb_traceback_batch.argtypes = [p, p, ci, p, p, p, i64, p, p, p, i64, p, p, i64, p, p, p, p, p, p, i64, p, p]
     lib.wsb_batch_has_faults.argtypes = [p]
+    lib.wsb_batch_h2d_bytes.argtypes = [p]
+    lib.wsb_batch_h2d_bytes.restype = i64
     lib.wsb_batch_total_runs.argtypes = [p]
     lib.wsb_batch_total_runs.restype = i64
     lib.wsb_pinned_alloc.argtypes = [ctypes.c_size_t, p]
@@ -213,11 +215,11 @@ class Batch:
                 ctx._h, _ptr(pools[0]), _ptr(pools[2]) if len(pools[2]) else None, len(pools[2]), _ptr(meta[0]), _ptr(meta[1]),
                 len(meta[1]), _ptr(pools[1]), _ptr(pools[3]) if len(pools[3]) else None, len(pools[3]), _ptr(meta[2]),
                 _ptr(meta[3]), len(meta[3]), _ptr(meta[4]), _ptr(meta[5]), self.n_pairs, ctypes.byref(h))
-        self.h2d_bytes = int(sum(a.nbytes for a in self._keep))
         if rc:
             self._keep = None
             raise status_exception(rc, ctx.last_error())
         self._h = h
+        self.h2d_bytes = int(self._lib.wsb_batch_h2d_bytes(h))   # what actually crossed the bus (regular metadata is generated on the device)
 
     @property
     def total_cells(self) -> int:

@@ -128,6 +128,7 @@ struct wsb_batch {
     int64_t piece_end[kMaxPieces] = {};
     cudaEvent_t piece_ev[kMaxPieces] = {};
     bool upload_pending = false;
+    int64_t h2d_bytes = 0;               // bytes that actually crossed the bus at creation (generated arrays excluded)
     TracebackState tb;  // traceback_kernels.cuh
 };
 
@@ -450,7 +451,8 @@ static int batch_create_impl(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t
     int rc;
     {
 #define UPG(dst, src, cnt, ap, a0, d) \
-        if ((rc = (ap) ? generate(ctx, &b->dst, a0, d, cnt) : upload(ctx, &b->dst, src, cnt)) != WSB_OK) { wsb_batch_destroy(b); return rc; }
+        if ((rc = (ap) ? generate(ctx, &b->dst, a0, d, cnt) : upload(ctx, &b->dst, src, cnt)) != WSB_OK) { wsb_batch_destroy(b); return rc; } \
+        if (!(ap)) b->h2d_bytes += (int64_t)sizeof(*src) * (cnt);
         UPG(d_qoff, q_off, n_q, ap_off[0], o0[0], od[0]) UPG(d_soff, s_off, n_s, ap_off[1], o0[1], od[1])
         UPG(d_qlen, q_len, n_q, ap_len[0], l0[0], ld[0]) UPG(d_slen, s_len, n_s, ap_len[1], l0[1], ld[1])
         UPG(d_pq, pair_q, n_pairs, ap_pair[0], p0[0], pd[0]) UPG(d_ps, pair_s, n_pairs, ap_pair[1], p0[1], pd[1])
@@ -471,8 +473,9 @@ static int batch_create_impl(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t
     if (pk.s_packed && (e = ctx->alloc((void**)&stage_s, (size_t)(s_total / 4 + 2))) != cudaSuccess) return fail(e);
     auto send = [&](const uint8_t* codes, const uint8_t* packed, uint8_t* stage, uint8_t* dst, int64_t lo, int64_t hi) -> cudaError_t {
         if (hi <= lo) return cudaSuccess;
-        if (!packed) return cudaMemcpyAsync(dst + lo, codes + lo, (size_t)(hi - lo), cudaMemcpyHostToDevice, ctx->copy_stream);
+        if (!packed) { b->h2d_bytes += hi - lo; return cudaMemcpyAsync(dst + lo, codes + lo, (size_t)(hi - lo), cudaMemcpyHostToDevice, ctx->copy_stream); }
         const int64_t b0 = lo / 4, b1 = (hi + 3) / 4;   // packed bytes covering symbols [lo, hi)
+        b->h2d_bytes += b1 - b0;
         cudaError_t r = cudaMemcpyAsync(stage + b0, packed + b0, (size_t)(b1 - b0), cudaMemcpyHostToDevice, ctx->copy_stream);
         if (r != cudaSuccess) return r;
         unpack2_kernel<<<(unsigned)((b1 - b0 + 255) / 256), 256, 0, ctx->copy_stream>>>(stage + b0, b0, lo, hi, dst);
@@ -545,6 +548,7 @@ extern "C" int wsb_batch_create(wsb_ctx* ctx, const uint8_t* q_codes, const int6
 }
 
 extern "C" int64_t wsb_batch_total_cells(const wsb_batch* b) { return b ? b->total_cells : 0; }
+extern "C" int64_t wsb_batch_h2d_bytes(const wsb_batch* b) { return b ? b->h2d_bytes : 0; }
 extern "C" int wsb_batch_has_faults(const wsb_batch* b) { return (b && b->last_plan && b->last_plan->any_error) ? 1 : 0; }
 
 // Page-locked host blocks for result downloads, recycled process-wide (cudaHostAlloc of tens of MB costs milliseconds).
