@@ -310,7 +310,11 @@ def run_batch(job: BatchJob) -> BatchReport:
     results = ResultArray(score, qs, qe, ss, se, cell_counts, runs, run_off)
     if n <= 4096:  # small batches: a plain list like the reference's; larger ones stay array-backed (same Sequence API)
         results = list(results)
-    d2h = sum(4 * 4 * len(idx) for idx in shard_index) + (runs.nbytes if runs is not None else 0)
+    # bytes actually downloaded: score + end cell (+ starts and run offsets in traceback mode, + status only on faults)
+    words = (5 if cfg.result_mode == "traceback" else 3) + (1 if any_fault else 0)
+    d2h = sum(4 * words * len(idx) for idx in shard_index)
+    if runs is not None:
+        d2h += runs.nbytes + 8 * (n + 1)
     if not shard_cells:
         shard_cells = [int(outs[0].get("cells", 0))]
     return BatchReport(results=results, wall_time=wall, total_cells=int(sum(o.get("cells", 0) for o in outs)),
