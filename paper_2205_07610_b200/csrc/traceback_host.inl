@@ -62,9 +62,9 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
     if (rc) return rc;
     const Plan* score_plan = b->last_plan;
 
-    if (!tb.d_qs) CUDA_TRY(ctx, cudaMalloc((void**)&tb.d_qs, sizeof(int32_t) * (size_t)np));
-    if (!tb.d_ss) CUDA_TRY(ctx, cudaMalloc((void**)&tb.d_ss, sizeof(int32_t) * (size_t)np));
-    if (!tb.d_run_off) CUDA_TRY(ctx, cudaMalloc((void**)&tb.d_run_off, sizeof(int64_t) * (size_t)(np + 1)));
+    if (!tb.d_qs) CUDA_TRY(ctx, ctx->alloc((void**)&tb.d_qs, sizeof(int32_t) * (size_t)np));
+    if (!tb.d_ss) CUDA_TRY(ctx, ctx->alloc((void**)&tb.d_ss, sizeof(int32_t) * (size_t)np));
+    if (!tb.d_run_off) CUDA_TRY(ctx, ctx->alloc((void**)&tb.d_run_off, sizeof(int64_t) * (size_t)(np + 1)));
 
     // 2. chunks of consecutive pairs under the scratch budget
     int max_m = 0, max_n = 0;
@@ -107,12 +107,12 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
     tb.total_runs = 0;
     int status = WSB_OK;
     auto cleanup = [&]() {
-        if (d_codes) cudaFree(d_codes);
-        if (d_run_tmp) cudaFree(d_run_tmp);
-        if (d_code_off) cudaFree(d_code_off);
-        if (d_cnt) cudaFree(d_cnt);
-        if (d_chunk_off) cudaFree(d_chunk_off);
-        if (d_scan_tmp) cudaFree(d_scan_tmp);
+        if (d_codes) ctx->release(d_codes);
+        if (d_run_tmp) ctx->release(d_run_tmp);
+        if (d_code_off) ctx->release(d_code_off);
+        if (d_cnt) ctx->release(d_cnt);
+        if (d_chunk_off) ctx->release(d_chunk_off);
+        if (d_scan_tmp) ctx->release(d_scan_tmp);
     };
 #define TB_TRY(expr)                                                                               \
     do {                                                                                           \
@@ -139,28 +139,28 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
             ++count;
         }
         if ((size_t)words > codes_cap) {
-            if (d_codes) cudaFree(d_codes);
+            if (d_codes) ctx->release(d_codes);
             d_codes = nullptr;
-            TB_TRY(cudaMalloc((void**)&d_codes, sizeof(uint32_t) * (size_t)std::max<int64_t>(words, 1)));
+            TB_TRY(ctx->alloc((void**)&d_codes, sizeof(uint32_t) * (size_t)std::max<int64_t>(words, 1)));
             codes_cap = (size_t)words;
         }
         if (count > chunk_cap) {
-            if (d_code_off) cudaFree(d_code_off);
-            if (d_cnt) cudaFree(d_cnt);
-            if (d_chunk_off) cudaFree(d_chunk_off);
-            if (d_run_tmp) cudaFree(d_run_tmp);
+            if (d_code_off) ctx->release(d_code_off);
+            if (d_cnt) ctx->release(d_cnt);
+            if (d_chunk_off) ctx->release(d_chunk_off);
+            if (d_run_tmp) ctx->release(d_run_tmp);
             d_code_off = nullptr; d_cnt = nullptr; d_chunk_off = nullptr; d_run_tmp = nullptr;
-            TB_TRY(cudaMalloc((void**)&d_run_tmp, sizeof(uint32_t) * (size_t)kTbTmpRuns * (size_t)count));
-            TB_TRY(cudaMalloc((void**)&d_code_off, sizeof(int64_t) * (size_t)count));
-            TB_TRY(cudaMalloc((void**)&d_cnt, sizeof(int32_t) * (size_t)(count + 1)));
-            TB_TRY(cudaMalloc((void**)&d_chunk_off, sizeof(int64_t) * (size_t)(count + 1)));
+            TB_TRY(ctx->alloc((void**)&d_run_tmp, sizeof(uint32_t) * (size_t)kTbTmpRuns * (size_t)count));
+            TB_TRY(ctx->alloc((void**)&d_code_off, sizeof(int64_t) * (size_t)count));
+            TB_TRY(ctx->alloc((void**)&d_cnt, sizeof(int32_t) * (size_t)(count + 1)));
+            TB_TRY(ctx->alloc((void**)&d_chunk_off, sizeof(int64_t) * (size_t)(count + 1)));
             chunk_cap = count;
             size_t need = 0;
             TB_TRY(cub::DeviceScan::ExclusiveSum(nullptr, need, d_cnt, d_chunk_off, (int)(count + 1), ctx->stream));
             if (need > scan_tmp_bytes) {
-                if (d_scan_tmp) cudaFree(d_scan_tmp);
+                if (d_scan_tmp) ctx->release(d_scan_tmp);
                 d_scan_tmp = nullptr;
-                TB_TRY(cudaMalloc(&d_scan_tmp, need));
+                TB_TRY(ctx->alloc(&d_scan_tmp, need));
                 scan_tmp_bytes = need;
             }
         }
@@ -195,11 +195,11 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
             const int64_t want = std::max<int64_t>((tb.total_runs + chunk_runs) * 3 / 2 + 1024,
                                                    (int64_t)((double)(tb.total_runs + chunk_runs) * np / (first + count)) + 1024);
             uint32_t* bigger = nullptr;
-            TB_TRY(cudaMalloc((void**)&bigger, sizeof(uint32_t) * (size_t)want));
+            TB_TRY(ctx->alloc((void**)&bigger, sizeof(uint32_t) * (size_t)want));
             if (tb.d_runs && tb.total_runs)
                 TB_TRY(cudaMemcpyAsync(bigger, tb.d_runs, sizeof(uint32_t) * (size_t)tb.total_runs, cudaMemcpyDeviceToDevice, ctx->stream));
             TB_TRY(cudaStreamSynchronize(ctx->stream));
-            if (tb.d_runs) cudaFree(tb.d_runs);
+            if (tb.d_runs) ctx->release(tb.d_runs);
             tb.d_runs = bigger; tb.runs_cap = want;
         }
         prm.runs = tb.d_runs + tb.total_runs;

@@ -310,6 +310,9 @@ extern "C" void wsb_batch_destroy(wsb_batch* b) {
                     b->d_bnd, (void*)b->d_redo, (void*)b->d_redo_long, b->stage_blocks[0], b->stage_blocks[1], b->stage_blocks[2], b->stage_blocks[3]})
         if (p) b->ctx->release(p);
     for (auto& kv : b->plans) if (kv.second.d_units) cudaFree(kv.second.d_units);
+    // traceback buffers come from the context's block cache
+    for (void* p : {(void*)b->tb.d_qs, (void*)b->tb.d_ss, (void*)b->tb.d_run_off, (void*)b->tb.d_runs}) if (p) b->ctx->release(p);
+    b->tb.d_qs = b->tb.d_ss = nullptr; b->tb.d_run_off = nullptr; b->tb.d_runs = nullptr;
     b->tb.release();
     delete b;
 }

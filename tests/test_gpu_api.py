@@ -112,7 +112,7 @@ def test_pool_inputs_and_lazy_results():
     for k in (0, 1, n // 2, n - 1):
         score, end = oracle.ref_score(q[k], s[k], "local", True, 2, -1, 2, 1)
         assert (rep.results[k].score, rep.results[k].q_end, rep.results[k].s_end) == (score, end[0], end[1])
-    assert rep.gpu_launches >= 1 and rep.h2d_bytes > 2 * n * 40 and rep.kernel_ms > 0
+    assert rep.gpu_launches >= 1 and rep.h2d_bytes >= 2 * n * 40 and rep.kernel_ms > 0   # regular metadata is generated on the device
 
 
 def test_packed_pools_give_identical_results():
