@@ -168,7 +168,8 @@ def dist_sum(x, world):
 def cpu_sample(cfg, seconds_target=12.0, seed=7):
     """Oracle port (plain C restatement of refdp, OpenMP over pairs) on a bounded sample of the workload."""
     import oracle
-    threads = oracle.max_threads()
+    # all host cores, whatever OMP_NUM_THREADS says (torchrun sets it to 1 for its workers)
+    threads = max(oracle.max_threads(), len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1))
     L = cfg["length"]
     sch = cfg["scheme"]
     if cfg.get("pareto"):  # bounded sample of the length distribution: cap 6000 bp keeps a pair under ~0.1 s of one core
