@@ -370,7 +370,7 @@ def main():
                 "e2e": {"value": e2e_value, "unit": "GCUPS", "h2d_bytes_per_step": int(rep.h2d_bytes) * world,
                         "d2h_bytes_per_step": int(rep.d2h_bytes) * world, "steps": e2e_steps},
                 "gpu_launches": launches, "clocks": clocks, "wall_s_timed_region": wall}
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:   # the CPU baseline is timed on rank 0 at N = 1 only
             rate, threads, pairs, dt = cpu_sample(cfg)
             line["cpu_baseline"] = {"value": rate, "unit": "GCUPS", "cores": threads, "kind": "port",
                                     "sample": f"{pairs} pairs of {L if L else 'pareto(cap 6000)'} bp ({dt:.1f} s), oracle/wsoracle.c with OpenMP"}
