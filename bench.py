@@ -311,7 +311,10 @@ def main():
 
     # end to end through the public API: host buffers in, host results out, every step
     pair_arr = np.stack([idx, idx], 1)
-    host_q, host_s = W.SequencePool(*pool_q), W.SequencePool(*pool_s)
+    if cfg.get("pareto"):
+        host_q, host_s = W.SequencePool(*pool_q), W.SequencePool(*pool_s)
+    else:   # a reads matrix: one row per read (run_batch then needs no offset / length / pair arrays on the device side)
+        host_q, host_s = W.SequencePool.from_uniform(q_pin), W.SequencePool.from_uniform(s_pin)
     if args.host_format == "packed2":   # packed once, outside the timed region: the host format of the input, not a step
         host_q, host_s = host_q.to_packed(), host_s.to_packed()
         keep_packed = [pinned(hp.packed) for hp in (host_q, host_s)]

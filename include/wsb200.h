@@ -103,6 +103,13 @@ int wsb_batch_create_packed_async(wsb_ctx* ctx, const uint8_t* q_packed, const i
                                   const int64_t* q_off, const int32_t* q_len, int64_t n_q, const uint8_t* s_packed,
                                   const int64_t* s_flag_pos, int64_t n_s_flags, const int64_t* s_off, const int32_t* s_len,
                                   int64_t n_s, const int32_t* pair_q, const int32_t* pair_s, int64_t n_pairs, wsb_batch** out);
+/* Regular batch without metadata arrays: n_pairs reads of q_len symbols back to back in the query pool, n_pairs reads
+ * of s_len symbols in the subject pool, pair i = (read i, read i).  Give each pool either as bytes (x_codes) or in the
+ * 2-bit layout (x_packed, no flagged symbols), the other pointer null; both pools in the same form.  Offsets, lengths
+ * and the pair list are generated on the device and nothing is scanned on the host. */
+int wsb_batch_create_uniform_async(wsb_ctx* ctx, const uint8_t* q_codes, const uint8_t* q_packed, int32_t q_len,
+                                   const uint8_t* s_codes, const uint8_t* s_packed, int32_t s_len, int64_t n_pairs,
+                                   wsb_batch** out);
 void wsb_batch_destroy(wsb_batch* b);
 
 /* Score every pair on the device; results stay in HBM until wsb_batch_fetch_scores.  kernel_ms (optional) receives

@@ -21,7 +21,7 @@ WSB_OK, WSB_E_CUDA, WSB_E_ARG, WSB_E_NOMEM, WSB_E_LENGTH, WSB_E_RANGE, WSB_E_SCH
 
 EXPORTED_SYMBOLS = (
     "wsb_strerror", "wsb_version", "wsb_device_count", "wsb_ctx_create", "wsb_ctx_destroy", "wsb_last_error",
-    "wsb_ctx_sm_count", "wsb_batch_create", "wsb_batch_create_async", "wsb_batch_create_packed_async", "wsb_batch_destroy", "wsb_batch_score", "wsb_batch_fetch_scores",
+    "wsb_ctx_sm_count", "wsb_batch_create", "wsb_batch_create_async", "wsb_batch_create_packed_async", "wsb_batch_create_uniform_async", "wsb_batch_destroy", "wsb_batch_score", "wsb_batch_fetch_scores",
     "wsb_batch_traceback", "wsb_batch_fetch_traceback", "wsb_batch_total_cells", "wsb_score_batch",
     "wsb_traceback_batch", "wsb_merged_state_exact", "wsb_f16_range_ok", "wsb_plan_shards", "wsb_batch_has_faults", "wsb_pinned_alloc",
     "wsb_pinned_free", "wsb_batch_total_runs", "wsb_batch_h2d_bytes",
@@ -60,6 +60,7 @@ def load():
     lib.wsb_batch_create.argtypes = [p, p, p, p, i64, p, p, p, i64, p, p, i64, p]
     lib.wsb_batch_create_async.argtypes = [p, p, p, p, i64, p, p, p, i64, p, p, i64, p]
     lib.wsb_batch_create_packed_async.argtypes = [p, p, p, i64, p, p, i64, p, p, i64, p, p, i64, p, p, i64, p]
+    lib.wsb_batch_create_uniform_async.argtypes = [p, p, p, i32, p, p, i32, i64, p]
     lib.wsb_batch_destroy.argtypes = [p]
     lib.wsb_batch_destroy.restype = None
     lib.wsb_batch_score.argtypes = [p, p, ci, ci, p, p]
@@ -220,6 +221,28 @@ class Batch:
             raise status_exception(rc, ctx.last_error())
         self._h = h
         self.h2d_bytes = int(self._lib.wsb_batch_h2d_bytes(h))   # what actually crossed the bus (regular metadata is generated on the device)
+
+    @classmethod
+    def uniform(cls, ctx: Context, q_pool, q_len: int, s_pool, s_len: int, n_pairs: int, packed: bool = False) -> "Batch":
+        """Regular batch (wsb_batch_create_uniform_async): read i of either pool at i * length, pair i = (i, i); the pools
+        are byte arrays or, with packed=True, 2-bit packed arrays without flagged symbols."""
+        self = cls.__new__(cls)
+        self._lib = load()
+        self.ctx = ctx
+        self.n_pairs = int(n_pairs)
+        pools = [np.ascontiguousarray(q_pool, np.uint8), np.ascontiguousarray(s_pool, np.uint8)]
+        self._keep = pools
+        h = ctypes.c_void_p()
+        qa = (None, _ptr(pools[0])) if packed else (_ptr(pools[0]), None)
+        sa = (None, _ptr(pools[1])) if packed else (_ptr(pools[1]), None)
+        rc = self._lib.wsb_batch_create_uniform_async(ctx._h, qa[0], qa[1], int(q_len), sa[0], sa[1], int(s_len),
+                                                      self.n_pairs, ctypes.byref(h))
+        if rc:
+            self._keep = None
+            raise status_exception(rc, ctx.last_error())
+        self._h = h
+        self.h2d_bytes = int(self._lib.wsb_batch_h2d_bytes(h))
+        return self
 
     @property
     def total_cells(self) -> int:

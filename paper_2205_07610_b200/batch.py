@@ -103,6 +103,11 @@ class BatchJob:
         # the device wants the two index columns as separate contiguous arrays: split once, here
         self._pair_q = np.ascontiguousarray(self._pair_array[:, 0])
         self._pair_s = np.ascontiguousarray(self._pair_array[:, 1])
+        # pair i = (i, i)?  (checked once here; lets run_batch take the metadata-free upload for uniform pools)
+        n = len(self._pair_q)
+        self._identity = bool(n and self._pair_q[0] == 0 and self._pair_q[-1] == n - 1 and
+                              np.array_equal(self._pair_q, self._pair_s) and
+                              np.array_equal(self._pair_q, np.arange(n, dtype=np.int32)))
 
 
 class ResultArray(_SequenceABC):
@@ -175,10 +180,18 @@ def _variant_for(job: BatchJob, cfg: AlignConfig) -> str:
 
 
 def _run_shard(device: int, queries: SequencePool, subjects: SequencePool, pair_q: np.ndarray, pair_s: np.ndarray,
-               cfg: AlignConfig, scheme: ScoringScheme, variant: str, out: dict):
+               cfg: AlignConfig, scheme: ScoringScheme, variant: str, out: dict, regular: bool = False):
     try:
         ctx = get_context(device)
-        if queries.packed is not None and subjects.packed is not None:   # 2-bit pools: a quarter of the bytes to upload
+        both_packed = queries.packed is not None and subjects.packed is not None
+        no_flags = both_packed and not (queries.flag_pos is not None and len(queries.flag_pos)) and \
+            not (subjects.flag_pos is not None and len(subjects.flag_pos))
+        if regular and len(pair_q) >= 65536 and (no_flags or (queries.packed is None and subjects.packed is None)):
+            # uniform pools, identity pairs: no offset / length / pair arrays at all
+            batch = N.Batch.uniform(ctx, queries.packed if both_packed else queries.codes, queries.uniform_len,
+                                    subjects.packed if both_packed else subjects.codes, subjects.uniform_len,
+                                    len(pair_q), packed=both_packed)
+        elif queries.packed is not None and subjects.packed is not None:   # 2-bit pools: a quarter of the bytes to upload
             batch = N.Batch(ctx, None, queries.off, queries.len, None, subjects.off, subjects.len, pair_q, pair_s,
                             packed=((queries.packed, queries.flag_pos), (subjects.packed, subjects.flag_pos)))
         else:
@@ -237,7 +250,9 @@ def run_batch(job: BatchJob) -> BatchReport:
         if len(idx) == 0:
             continue
         if len(devices) == 1:  # no thread hop for the common single-GPU case
-            _run_shard(dev, queries, subjects, pair_q, pair_s, cfg, job.scheme, variant, out)
+            regular = (job._identity and queries.uniform_len is not None and subjects.uniform_len is not None and
+                       n <= len(queries) and n <= len(subjects))
+            _run_shard(dev, queries, subjects, pair_q, pair_s, cfg, job.scheme, variant, out, regular)
             continue
         th = threading.Thread(target=_run_shard, name=f"waveseq-gpu-{dev}",
                               args=(dev, queries, subjects, pair_q[idx], pair_s[idx], cfg, job.scheme, variant, out))

@@ -342,15 +342,19 @@ __global__ void set_flags_kernel(const int64_t* idx, int64_t n, int64_t limit, u
 struct PackedPools {   // optional: pools given in the 2-bit layout (+ sorted-or-not lists of flagged symbol positions)
     const uint8_t* q_packed = nullptr; const int64_t* q_flags = nullptr; int64_t n_q_flags = 0;
     const uint8_t* s_packed = nullptr; const int64_t* s_flags = nullptr; int64_t n_s_flags = 0;
+    // optional: the caller vouches for a regular batch (read k of either pool at k * length, pair i = (i, i)); the
+    // metadata arrays may then be null and nothing is scanned
+    int32_t uniform_q_len = -1, uniform_s_len = -1;
 };
 
 static int batch_create_impl(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t* q_off, const int32_t* q_len,
                              int64_t n_q, const uint8_t* s_codes, const int64_t* s_off, const int32_t* s_len,
                              int64_t n_s, const int32_t* pair_q, const int32_t* pair_s, int64_t n_pairs,
                              const PackedPools& pk, wsb_batch** out) {
-    if (!ctx || !out || (!q_codes && !pk.q_packed) || !q_off || !q_len || (!s_codes && !pk.s_packed) || !s_off || !s_len ||
-        !pair_q || !pair_s ||
-        n_q <= 0 || n_s <= 0 || n_pairs <= 0 || n_pairs > (int64_t)0x7fffffff)
+    const bool vouched = pk.uniform_q_len >= 0 && pk.uniform_s_len >= 0;
+    if (!ctx || !out || (!q_codes && !pk.q_packed) || (!s_codes && !pk.s_packed) ||
+        (!vouched && (!q_off || !q_len || !s_off || !s_len || !pair_q || !pair_s)) ||
+        n_q <= 0 || n_s <= 0 || n_pairs <= 0 || n_pairs > (int64_t)0x7fffffff || (vouched && (n_pairs > n_q || n_pairs > n_s)))
         return WSB_E_ARG;
     *out = nullptr;
     CUDA_TRY(ctx, cudaSetDevice(ctx->device));
@@ -367,7 +371,11 @@ static int batch_create_impl(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t
     {
         auto total_q = [&] { int64_t x = 0; for (int64_t k = 0; k < n_q; ++k) x = std::max(x, q_off[k] + q_len[k]); q_total = x; };
         auto total_s = [&] { int64_t x = 0; for (int64_t k = 0; k < n_s; ++k) x = std::max(x, s_off[k] + s_len[k]); s_total = x; };
-        if (n_pairs >= 65536) {
+        if (vouched) {
+            q_total = n_q * pk.uniform_q_len; s_total = n_s * pk.uniform_s_len;
+            for (int k = 0; k < 2; ++k) { ap_off[k] = ap_len[k] = ap_pair[k] = true; p0[k] = 0; pd[k] = 1; ld[k] = 0; o0[k] = 0; }
+            od[0] = l0[0] = pk.uniform_q_len; od[1] = l0[1] = pk.uniform_s_len;
+        } else if (n_pairs >= 65536) {
             std::thread th[8] = {
                 std::thread(total_q), std::thread(total_s),
                 std::thread([&] { ap_off[0] = is_progression(q_off, n_q, o0[0], od[0]); }),
@@ -389,8 +397,8 @@ static int batch_create_impl(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t
     const int nthr = regular ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency())), n_pairs / 65536 + 1));
     std::vector<int> bad(nthr, 0), uni(nthr, 1);
     std::vector<int64_t> cells(nthr, 0);
-    const int m0 = (pair_q[0] >= 0 && pair_q[0] < n_q) ? q_len[pair_q[0]] : -1;
-    const int n0 = (pair_s[0] >= 0 && pair_s[0] < n_s) ? s_len[pair_s[0]] : -1;
+    const int m0 = regular ? l0[0] : (pair_q[0] >= 0 && pair_q[0] < n_q) ? q_len[pair_q[0]] : -1;
+    const int n0 = regular ? l0[1] : (pair_s[0] >= 0 && pair_s[0] < n_s) ? s_len[pair_s[0]] : -1;
     auto work = [&](int k) {
         const int64_t lo = n_pairs * k / nthr, hi = n_pairs * (k + 1) / nthr;
         int64_t acc = 0;
@@ -443,7 +451,10 @@ static int batch_create_impl(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t
         for (int k = 0; k < n_pieces; ++k)   // boundaries on multiples of 2048 pairs (packed units never straddle pieces)
             b->piece_end[k] = k + 1 == n_pieces ? n_pairs : std::min<int64_t>(n_pairs, (n_pairs * (k + 1) / n_pieces + 2047) / 2048 * 2048);
         if (n_pieces == 1) { need_q[0] = q_total; need_s[0] = s_total; }
-        else {
+        else if (regular) {   // pair p needs the pool bytes up to (p + 1) * length
+            for (int k = 0; k < n_pieces; ++k) { need_q[k] = b->piece_end[k] * l0[0]; need_s[k] = b->piece_end[k] * l0[1]; }
+            need_q[n_pieces - 1] = q_total; need_s[n_pieces - 1] = s_total;
+        } else {
             std::vector<std::thread> th;
             for (int k = 0; k < n_pieces; ++k) th.emplace_back(piece_work, k);
             for (auto& x : th) x.join();
@@ -537,6 +548,15 @@ extern "C" int wsb_batch_create_packed_async(wsb_ctx* ctx, const uint8_t* q_pack
     pk.q_packed = q_packed; pk.q_flags = q_flag_pos; pk.n_q_flags = n_q_flags;
     pk.s_packed = s_packed; pk.s_flags = s_flag_pos; pk.n_s_flags = n_s_flags;
     return batch_create_impl(ctx, nullptr, q_off, q_len, n_q, nullptr, s_off, s_len, n_s, pair_q, pair_s, n_pairs, pk, out);
+}
+
+extern "C" int wsb_batch_create_uniform_async(wsb_ctx* ctx, const uint8_t* q_codes, const uint8_t* q_packed, int32_t q_len,
+                                              const uint8_t* s_codes, const uint8_t* s_packed, int32_t s_len, int64_t n_pairs,
+                                              wsb_batch** out) {
+    if (q_len < 0 || s_len < 0 || (!q_codes == !q_packed) || (!s_codes == !s_packed) || (!q_codes != !s_codes)) return WSB_E_ARG;
+    PackedPools pk;
+    pk.q_packed = q_packed; pk.s_packed = s_packed; pk.uniform_q_len = q_len; pk.uniform_s_len = s_len;
+    return batch_create_impl(ctx, q_codes, nullptr, nullptr, n_pairs, s_codes, nullptr, nullptr, n_pairs, nullptr, nullptr, n_pairs, pk, out);
 }
 
 extern "C" int wsb_batch_create(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t* q_off, const int32_t* q_len,

@@ -17,6 +17,7 @@ class SequencePool:
     def __init__(self, codes: np.ndarray, off: np.ndarray, lengths: np.ndarray, ids=None):
         self.packed = None       # optional 2-bit form of the pool (from_packed): what run_batch uploads when present
         self.flag_pos = None
+        self.uniform_len = None  # set by from_uniform: read k starts at k * uniform_len
         self._codes = np.ascontiguousarray(codes, np.uint8) if codes is not None else None
         self.off = np.ascontiguousarray(off, np.int64)
         self.len = np.ascontiguousarray(lengths, np.int32)
@@ -59,7 +60,9 @@ class SequencePool:
             v = np.concatenate([v, np.zeros(pad, np.uint8)])
         v = v.reshape(-1, 4)
         packed = (v[:, 0] | (v[:, 1] << 2) | (v[:, 2] << 4) | (v[:, 3] << 6)).astype(np.uint8)
-        return SequencePool.from_packed(packed, self.off, self.len, flags, self.ids)
+        out = SequencePool.from_packed(packed, self.off, self.len, flags, self.ids)
+        out.uniform_len = self.uniform_len
+        return out
 
     def __getitem__(self, k: int) -> Sequence:
         """Materialise one Sequence (reference type) on demand."""
@@ -85,4 +88,6 @@ class SequencePool:
     def from_uniform(cls, codes2d: np.ndarray) -> "SequencePool":
         """Pool over the rows of an (n_sequences, length) uint8 matrix, without copying."""
         n, length = codes2d.shape
-        return cls(codes2d.reshape(-1), np.arange(n, dtype=np.int64) * length, np.full(n, length, np.int32))
+        pool = cls(codes2d.reshape(-1), np.arange(n, dtype=np.int64) * length, np.full(n, length, np.int32))
+        pool.uniform_len = int(length)
+        return pool
