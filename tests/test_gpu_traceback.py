@@ -115,3 +115,20 @@ def test_multi_stage_and_chunked(ctx, monkeypatch):
     pairs = [(i, i) for i in range(len(qs))]
     for at in ("global", "local", "semiglobal"):
         assert_tb_equal(gpu_traceback(ctx, qs, ss, pairs, scheme, at), oracle_traceback(qs, ss, pairs, scheme, at), at)
+
+
+@pytest.mark.parametrize("align_type,gap_model", COMBOS)
+def test_empty_and_single_symbol_sides(ctx, align_type, gap_model):
+    """The Python API refuses empty sequences like the reference (core.py:103-104); the C ABI accepts them and resolves
+    them like refdp's zero-row / zero-column matrices.  One-symbol sides run through the kernels."""
+    rng = np.random.default_rng(3)
+    seqs = [np.zeros(0, np.uint8), codes("A"), codes("N"), codes("C"), random_codes(rng, 7), random_codes(rng, 130),
+            random_codes(rng, 600)]
+    pairs = [(a, b) for a in range(len(seqs)) for b in range(len(seqs))]
+    scheme = scheme_of((2, -1, 2, 1) if gap_model == "affine" else (2, -1, 1, 1), gap_model)
+    want = oracle_traceback(seqs, seqs, pairs, scheme, align_type)
+    got = gpu_traceback(ctx, seqs, seqs, pairs, scheme, align_type)
+    assert_tb_equal(got, want, f"{align_type}/{gap_model}")
+    from helpers import assert_scores_equal, gpu_scores, oracle_scores
+    assert_scores_equal(gpu_scores(ctx, seqs, seqs, pairs, scheme, align_type), oracle_scores(seqs, seqs, pairs, scheme, align_type),
+                        f"{align_type}/{gap_model}")
