@@ -351,7 +351,8 @@ def main():
     except OSError:
         pass
     roofline = {"bound": "alu_issue", "achieved": per_gpu, "peak": peak, "unit": "GCUPS", "frac": per_gpu / peak,
-                "traffic": traffic, "peak_source": "N_SM*128*f_SM*W/I_cell with f_SM = sm_max_mhz of MEASURED_PEAKS.json",
+                "traffic": traffic, "peak_source": "N_SM*128*f_SM*W/I_cell with f_SM = " + ("sm_max_mhz of MEASURED_PEAKS.json" if "sm_max_mhz" in peaks
+                                                                          else "1965 MHz (fallback: MEASURED_PEAKS.json absent)"),
                 "i_cell": cfg["i_cell"], "cells_per_thread_instr": width, "n_sm": n_sm, "f_ghz": f_ghz}
     if clocks.get("sm_mhz"):
         cyc_peak = n_sm * 128 * clocks["sm_mhz"] / 1e3 * width / cfg["i_cell"]
