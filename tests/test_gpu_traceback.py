@@ -132,3 +132,38 @@ def test_empty_and_single_symbol_sides(ctx, align_type, gap_model):
     from helpers import assert_scores_equal, gpu_scores, oracle_scores
     assert_scores_equal(gpu_scores(ctx, seqs, seqs, pairs, scheme, align_type), oracle_scores(seqs, seqs, pairs, scheme, align_type),
                         f"{align_type}/{gap_model}")
+
+
+@pytest.mark.parametrize("align_type", ["global", "local", "semiglobal"])
+def test_long_pairs_rescore_to_their_score(ctx, align_type):
+    """Lengths the oracle's full matrices cannot hold: the CIGAR must re-score (from first principles) to the score the
+    score-only long-read kernel reports, and consume exactly the recorded spans (the reference's own contract for
+    align_traceback, tests/test_traceback.py:85-100)."""
+    import paper_2205_07610_b200 as W
+    from helpers import gpu_scores
+    rng = np.random.default_rng(2205)
+    scheme = scheme_of((2, -1, 2, 1), "affine")
+    qs, ss = [], []
+    for L in (21_000, 9_000):
+        q = random_codes(rng, L)
+        qs.append(q); ss.append(mutate_codes(rng, q, 0.06, 0.03, 0.03))
+    if align_type != "global":   # a short read against a long window
+        qs.append(ss[0][5000:5400].copy()); ss.append(ss[0])
+    pairs = [(i, i) for i in range(len(qs))]
+    got = gpu_traceback(ctx, qs, ss, pairs, scheme, align_type)
+    score = gpu_scores(ctx, qs, ss, pairs, scheme, align_type)
+    assert (got["score"] == score[0]).all()
+    for k in range(len(qs)):
+        ops = unpack_runs(got["cigar"][int(got["cigar_off"][k]):int(got["cigar_off"][k + 1])])
+        res = W.AlignmentResult(int(got["score"][k]), int(got["q_start"][k]), int(got["q_end"][k]), int(got["s_start"][k]),
+                                int(got["s_end"][k]), ops, len(qs[k]) * len(ss[k]))
+        q = W.Sequence(f"q{k}", qs[k], np.zeros(len(qs[k]), bool))
+        s = W.Sequence(f"s{k}", ss[k], np.zeros(len(ss[k]), bool))
+        assert W.rescore_alignment(res, q, s, scheme) == res.score
+        if align_type == "global":
+            assert (res.q_start, res.q_end, res.s_start, res.s_end) == (0, len(qs[k]), 0, len(ss[k]))
+        elif align_type == "semiglobal":
+            assert res.q_end == len(qs[k]) or res.s_end == len(ss[k])
+        assert all(a[0] != b[0] for a, b in zip(ops, ops[1:]))      # runs arrive merged
+    if align_type != "global":
+        assert got["score"][2] == 800 and (got["s_start"][2], got["s_end"][2]) == (5000, 5400)
