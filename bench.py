@@ -340,8 +340,10 @@ def main():
     f_ghz = float(peaks.get("sm_max_mhz", 1965.0)) / 1e3
     n_sm = ctx.sm_count
     # dominant kernel: cfg3 int32 fill, cfg5 int32 long-read kernel; cfg4's equal-shape pairs run two per block in packed int16
-    width = 1 if (variant == "i32" or args.workload in ("cfg3", "cfg5")) else 2
-    dtype = "i32" if width == 1 else ("s16x2" if args.workload == "cfg4" else "f16x2")
+    # cfg3: the direction-code fill of a uniform batch runs packed int16 (two alignments per thread) unless switched off
+    tb16 = args.workload == "cfg3" and not os.environ.get("WSB_TB_NO16")
+    width = 1 if (variant == "i32" or args.workload == "cfg5" or (args.workload == "cfg3" and not tb16)) else 2
+    dtype = "i32" if width == 1 else ("s16x2" if args.workload in ("cfg3", "cfg4") else "f16x2")
     peak = n_sm * 128 * f_ghz * width / cfg["i_cell"]
     per_gpu = value / world
     traffic = None

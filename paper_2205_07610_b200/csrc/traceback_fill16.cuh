@@ -1,0 +1,212 @@
+// traceback_fill16.cuh -- packed int16 direction-code fill: two alignments of a uniform batch per thread (sm_100a).
+//
+// Same wavefront, same bit planes and the same code-block layout as tb_fill_kernel (traceback_kernels.cuh), so the walk
+// kernels read either fill's output.  The two alignments of a unit live in the 16-bit halves of every value, and the
+// four "max with who-won" steps of the Gotoh cell become one VIMNMX.S16x2 each: the instruction returns the packed
+// maximum AND one predicate per half ("the first operand won"), which the int32 form needs ISETP + SEL for.  Per packed
+// cell (two matrix cells): 4 VIMNMX.S16x2, 8 predicated plane-bit adds (ptxas splits them between IMAD and LEA, i.e.
+// between the FMA and the ALU pipe), 5 VIADD.16x2, and HSET2.EQ + LOP3 for the substitution score -- 19 instructions
+// for two cells where the int32 fill issues 16 for one.
+//
+// Substitution: symbols travel as the half-precision bit patterns 0x4000 | code (normal numbers, so the comparison is
+// exact whatever the denormal mode); flagged query symbols are 0x4004, flagged or padded subject symbols 0x4005, which
+// never compare equal (core.py:147-151: flagged symbols never match, even N-N).
+//
+// Scope (the host checks it, traceback_host.inl): affine gaps, global or semiglobal, every pair of the launch has the same
+// (m, n) with n <= P*K (one stage, no border scratch), and the int16 range rule below holds.  Everything else -- local
+// alignments (their stop encoding needs H itself), ragged batches, long reads -- stays on the int32 fill.
+#pragma once
+#include "traceback_kernels.cuh"
+
+#include <cuda_fp16.h>
+
+namespace wsb {
+
+constexpr int kNeg16 = -24000;   // "minus infinity" of the packed fill: below every reachable value, never extended twice
+
+// the packed fill is exact while every reachable value stays inside int16 with room for one more step below kNeg16
+__host__ __device__ inline bool tb_fill16_range_ok(int m, int n, int match, int mismatch, int alpha, int beta) {
+    const int64_t lo = 3ll * alpha + (int64_t)beta * (m + n) + (mismatch < 0 ? -mismatch : mismatch) + (match < 0 ? -match : match);
+    const int64_t hi = (int64_t)(match > 0 ? match : 0) * (m < n ? m : n) + alpha + beta;
+    return lo <= 8000 && hi <= 32000 && alpha <= 4000 && beta <= 4000;
+}
+
+__device__ __forceinline__ unsigned pk16(int v) { return ((unsigned)v & 0xffffu) * 0x00010001u; }
+__device__ __forceinline__ int lo16(unsigned v) { return (int)(short)(v & 0xffffu); }
+__device__ __forceinline__ int hi16(unsigned v) { return (int)v >> 16; }
+
+// packed max(a, b), "a wins ties"; the plane bit goes to wlo / whi where a won in the low / high half
+__device__ __forceinline__ unsigned max_mark2(unsigned a, unsigned b, uint32_t& wlo, uint32_t& whi, uint32_t bit, int one) {
+    unsigned r;
+    asm("{\n\t.reg .pred pl, ph;\n\t.reg .s16 r0, r1, a0, a1;\n\t"
+        "max.s16x2 %0, %3, %4;\n\t"
+        "mov.b32 {r0, r1}, %0;\n\t"
+        "mov.b32 {a0, a1}, %3;\n\t"
+        "setp.eq.s16 pl, r0, a0;\n\t"
+        "setp.eq.s16 ph, r1, a1;\n\t"
+        "@pl mad.lo.u32 %1, %6, %5, %1;\n\t"
+        "@ph mad.lo.u32 %2, %6, %5, %2;\n\t"
+        "}" : "=r"(r), "+r"(wlo), "+r"(whi) : "r"(a), "r"(b), "r"(bit), "r"(one));
+    return r;
+}
+
+template <int P, int K, int ATYPE>
+__global__ void __launch_bounds__(kThreads) tb_fill16_kernel(const TbParams prm) {
+    constexpr int GPB = kThreads / P;
+    constexpr int NW = K / 8;
+    constexpr bool GLOBAL_EDGES = ATYPE == AT_GLOBAL;
+    static_assert(ATYPE != AT_LOCAL, "local alignments use the int32 fill");
+    static_assert(K % 8 == 0, "K must pack into whole code words");
+
+    const int tid = threadIdx.x;
+    const int t = tid & (P - 1);
+    const int gib = tid / P;
+    const int64_t group_global = (int64_t)blockIdx.x * GPB + gib;
+    const int64_t n_groups = (int64_t)gridDim.x * GPB;
+    const int alpha = prm.alpha, beta = prm.beta, one = prm.one;
+    const unsigned nb2 = pk16(-beta), na2 = pk16(-alpha);
+    const unsigned base2 = pk16(prm.mismatch + alpha), delta2 = pk16(prm.match - prm.mismatch);
+    const unsigned neg2 = pk16(kNeg16);
+    const int64_t n_units = (prm.n_pairs + 1) / 2;
+
+    // all lane groups of a warp run the same number of rounds (the shuffles below are warp-wide); a group without a unit
+    // recomputes the last one and keeps its results to itself
+    const int64_t rounds = (n_units + n_groups - 1) / n_groups;
+    for (int64_t rd = 0; rd < rounds; ++rd) {
+        const int64_t u_raw = rd * n_groups + group_global;
+        const bool live = u_raw < n_units;
+        const int64_t u = live ? u_raw : n_units - 1;
+        const bool twin = 2 * u + 1 < prm.n_pairs;   // an odd tail computes its only alignment in both halves
+        const int64_t ua = 2 * u, ub = twin ? ua + 1 : ua;
+        const int64_t pa = prm.first_pair + ua, pb = prm.first_pair + ub;
+        const int qa_i = prm.pair_q[pa], sa_i = prm.pair_s[pa], qb_i = prm.pair_q[pb], sb_i = prm.pair_s[pb];
+        const int m = prm.q_len[qa_i], n = prm.s_len[sa_i];
+        const uint8_t* qa = prm.q_codes + prm.q_off[qa_i];
+        const uint8_t* qb = prm.q_codes + prm.q_off[qb_i];
+        const uint8_t* sa = prm.s_codes + prm.s_off[sa_i];
+        const uint8_t* sb = prm.s_codes + prm.s_off[sb_i];
+        uint32_t* code_a = prm.codes + prm.code_off[ua];
+        uint32_t* code_b = prm.codes + prm.code_off[ub];
+        const int col0 = t * K;
+
+        unsigned ss[K], AL[K], EP[K];
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+            unsigned x = 5u, y = 5u;
+            if (col0 + c < n) {
+                x = sa[col0 + c]; y = sb[col0 + c];
+                x = x < 4u ? x : 5u; y = y < 4u ? y : 5u;
+            }
+            ss[c] = (0x4000u | x) | ((0x4000u | y) << 16);
+            AL[c] = pk16(edge_h(GLOBAL_EDGES, col0 + c + 1, alpha, beta) - alpha);
+            EP[c] = neg2;
+        }
+        const unsigned al_top = pk16(edge_h(GLOBAL_EDGES, col0, alpha, beta) - alpha);
+        unsigned al_diag = al_top, all = neg2, fpl = neg2;
+        int edge = edge_h(GLOBAL_EDGES, 1, alpha, beta);
+        if (t == 0) all = pk16(edge - alpha);
+        const int cap_rel = n - 1 - col0;
+        const bool has_cap = cap_rel >= 0 && cap_rel < K;
+        int bv_a = GLOBAL_EDGES ? kNeg32 : 0, bi_a = 0, bj_a = ATYPE == AT_SEMI ? n : 0;
+        int bv_b = bv_a, bi_b = bi_a, bj_b = bj_a;
+
+        auto q_at = [&](int it) {
+            const int idx = min(max(it - t - 1, 0), m - 1);
+            unsigned a = qa[idx], b = qb[idx];
+            a = a < 4u ? a : 4u; b = b < 4u ? b : 4u;
+            return (0x4000u | a) | ((0x4000u | b) << 16);
+        };
+        unsigned q_cur = q_at(1), q_nxt = q_at(2);
+        const int it_end = m + P - 1;
+        for (int it = 1; it <= it_end; ++it) {
+            const unsigned q_nn = q_at(it + 2);
+            const int r = it - t;
+            unsigned out_al = all, out_fp = fpl;
+            if (r >= 1 && r <= m) {
+                const __half2 qh = *reinterpret_cast<const __half2*>(&q_cur);
+                unsigned ad = al_diag, fl = fpl, al = all;
+                uint32_t wa[NW], wb[NW];
+#pragma unroll
+                for (int w8 = 0; w8 < NW; ++w8) {
+                    uint32_t wd_a = 0u, wm_a = 0u, we_a = 0u, wf_a = 0u, wd_b = 0u, wm_b = 0u, we_b = 0u, wf_b = 0u;
+#pragma unroll
+                    for (int c8 = 0; c8 < 8; ++c8) {
+                        const int c = w8 * 8 + c8;
+                        const unsigned hit = __heq2_mask(qh, *reinterpret_cast<const __half2*>(&ss[c]));
+                        const unsigned d = __vadd2(__vadd2(ad, base2), hit & delta2);
+                        ad = AL[c];
+                        const unsigned e = max_mark2(EP[c], AL[c], we_a, we_b, 1u << (16 + c8), one);
+                        const unsigned f = max_mark2(fl, al, wf_a, wf_b, 1u << (24 + c8), one);
+                        EP[c] = __vadd2(e, nb2);
+                        fl = __vadd2(f, nb2);
+                        const unsigned m1 = max_mark2(d, e, wd_a, wd_b, 1u << c8, one);
+                        const unsigned h = max_mark2(m1, f, wm_a, wm_b, 1u << (8 + c8), one);
+                        al = __vadd2(h, na2);
+                        AL[c] = al;
+                    }
+                    wa[w8] = (wd_a | wm_a) | (we_a | wf_a);
+                    wb[w8] = (wd_b | wm_b) | (we_b | wf_b);
+                }
+                const int64_t at = ((int64_t)(it - 1) * P + t) * NW;   // wavefront-major, one stage
+                if (!live) {
+                } else if (NW == 2) {
+                    *reinterpret_cast<uint2*>(code_a + at) = make_uint2(wa[0], wa[1]);
+                    if (twin) *reinterpret_cast<uint2*>(code_b + at) = make_uint2(wb[0], wb[1]);
+                } else if (NW == 4) {
+                    *reinterpret_cast<uint4*>(code_a + at) = make_uint4(wa[0], wa[1], wa[2], wa[NW - 1]);
+                    if (twin) *reinterpret_cast<uint4*>(code_b + at) = make_uint4(wb[0], wb[1], wb[2], wb[NW - 1]);
+                } else {
+#pragma unroll
+                    for (int w8 = 0; w8 < NW; ++w8) { code_a[at + w8] = wa[w8]; if (twin) code_b[at + w8] = wb[w8]; }
+                }
+                out_al = al;
+                out_fp = fl;
+                if (ATYPE == AT_SEMI && has_cap && r < m) {   // last matrix column, rows above the last one
+                    const unsigned hv = select_reg<unsigned, K>(AL, cap_rel);
+                    const int va = lo16(hv) + alpha, vb = hi16(hv) + alpha;
+                    if (better_cell(va, r, n, bv_a, bi_a, bj_a)) { bv_a = va; bi_a = r; bj_a = n; }
+                    if (better_cell(vb, r, n, bv_b, bi_b, bj_b)) { bv_b = vb; bi_b = r; bj_b = n; }
+                }
+            }
+            unsigned nal = __shfl_up_sync(0xffffffffu, out_al, 1, P);
+            unsigned nfp = __shfl_up_sync(0xffffffffu, out_fp, 1, P);
+            al_diag = all;
+            if (t == 0) {
+                if (GLOBAL_EDGES) edge -= beta;
+                nal = pk16(edge - alpha); nfp = neg2;
+            }
+            all = nal; fpl = nfp;
+            if (r == 0) al_diag = al_top;
+            q_cur = q_nxt; q_nxt = q_nn;
+        }
+        // every lane's registers now hold row m of its strip
+        if (ATYPE == AT_SEMI) {
+#pragma unroll
+            for (int c = 0; c < K; ++c)
+                if (col0 + c < n) {
+                    const int va = lo16(AL[c]) + alpha, vb = hi16(AL[c]) + alpha;
+                    if (better_cell(va, m, col0 + c + 1, bv_a, bi_a, bj_a)) { bv_a = va; bi_a = m; bj_a = col0 + c + 1; }
+                    if (better_cell(vb, m, col0 + c + 1, bv_b, bi_b, bj_b)) { bv_b = vb; bi_b = m; bj_b = col0 + c + 1; }
+                }
+        }
+        if (GLOBAL_EDGES && has_cap) {
+            const unsigned hv = select_reg<unsigned, K>(AL, cap_rel);
+            bv_a = lo16(hv) + alpha; bv_b = hi16(hv) + alpha; bi_a = bi_b = m; bj_a = bj_b = n;
+        }
+        const unsigned gmask = group_mask<P>(tid & 31);
+#pragma unroll
+        for (int off = P / 2; off >= 1; off >>= 1) {
+            int ov = __shfl_xor_sync(gmask, bv_a, off, P), oi = __shfl_xor_sync(gmask, bi_a, off, P), oj = __shfl_xor_sync(gmask, bj_a, off, P);
+            if (better_cell(ov, oi, oj, bv_a, bi_a, bj_a)) { bv_a = ov; bi_a = oi; bj_a = oj; }
+            ov = __shfl_xor_sync(gmask, bv_b, off, P); oi = __shfl_xor_sync(gmask, bi_b, off, P); oj = __shfl_xor_sync(gmask, bj_b, off, P);
+            if (better_cell(ov, oi, oj, bv_b, bi_b, bj_b)) { bv_b = ov; bi_b = oi; bj_b = oj; }
+        }
+        if (t == 0 && live) {
+            prm.w_score[pa] = bv_a; prm.w_i[pa] = bi_a; prm.w_j[pa] = bj_a;
+            if (twin) { prm.w_score[pb] = bv_b; prm.w_i[pb] = bi_b; prm.w_j[pb] = bj_b; }
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace wsb

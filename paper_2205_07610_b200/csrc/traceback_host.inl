@@ -6,6 +6,8 @@
 // (WSB_TB_SCRATCH_MB, default 16 GiB).
 #include <cub/device/device_scan.cuh>
 
+#include "traceback_fill16.cuh"
+
 struct TbShape { int P, K; };
 static const TbShape kTbShapes[] = {{8, 16}, {8, 32}, {32, 16}, {16, 16}};
 
@@ -24,6 +26,15 @@ template <int P, int K> static TbFillFn tb_pick_fill(int atype, bool affine) {
         case AT_LOCAL: return affine ? tb_fill_kernel<P, K, AT_LOCAL, true> : tb_fill_kernel<P, K, AT_LOCAL, false>;
         default: return affine ? tb_fill_kernel<P, K, AT_SEMI, true> : tb_fill_kernel<P, K, AT_SEMI, false>;
     }
+}
+
+// packed int16 fill (traceback_fill16.cuh): uniform affine global / semiglobal batches of one stage
+static TbFillFn tb_pick_fill16(int shape, int atype) {
+    if (atype == AT_LOCAL) return nullptr;
+    const bool g = atype == AT_GLOBAL;
+    if (shape == 0) return g ? tb_fill16_kernel<8, 16, AT_GLOBAL> : tb_fill16_kernel<8, 16, AT_SEMI>;
+    if (shape == 1) return g ? tb_fill16_kernel<8, 32, AT_GLOBAL> : tb_fill16_kernel<8, 32, AT_SEMI>;
+    return nullptr;
 }
 
 template <int PASS> static void tb_launch_walk(int atype, const TbParams& prm, cudaStream_t stream) {
@@ -75,6 +86,12 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
     TbFillFn fill = shape == 0 ? tb_pick_fill<8, 16>(atype, affine)
                   : shape == 1 ? tb_pick_fill<8, 32>(atype, affine)
                   : shape == 2 ? tb_pick_fill<32, 16>(atype, affine) : tb_pick_fill<16, 16>(atype, affine);
+    // two alignments per thread in int16 halves where the batch allows it
+    static const bool no16 = getenv("WSB_TB_NO16") != nullptr;   // tuning aid
+    TbFillFn fill16 = nullptr;
+    if (!no16 && affine && b->uniform && max_m > 0 && max_n > 0 && max_n <= P * K && (!score_plan || score_plan->status.empty() || score_plan->status[0] == 0) &&
+        tb_fill16_range_ok(max_m, max_n, sch->match, sch->mismatch, sch->gap_open, sch->gap_extend))
+        fill16 = tb_pick_fill16(shape, atype);
     size_t budget_words = (size_t)16384 << 18;  // 16 GiB in 32-bit words (a B200 carries 180 GB)
     if (const char* e = getenv("WSB_TB_SCRATCH_MB")) { const long mb = atol(e); if (mb > 0) budget_words = (size_t)mb << 18; }
 
@@ -83,6 +100,12 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
     per_sm = std::max(per_sm, 1);
     const int gpb = kThreads / P;
     const int max_grid = ctx->sm_count * per_sm;
+    int max_grid16 = 0;
+    if (fill16) {
+        int per_sm16 = 0;
+        CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm16, fill16, kThreads, 0));
+        max_grid16 = ctx->sm_count * std::max(per_sm16, 1);
+    }
     const bool multi_stage = max_n > P * K;
     const int64_t bnd_rows = multi_stage ? (int64_t)max_m + 2 : 0;
     const size_t bnd_need = (size_t)bnd_rows * sizeof(int2) * (size_t)max_grid * gpb;
@@ -180,8 +203,14 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
         prm.tb_p = P; prm.tb_k = K; prm.one = 1; prm.run_tmp = d_run_tmp;
 
         TB_TRY(cudaEventRecord(e0, ctx->stream));
-        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((count + gpb - 1) / gpb, max_grid));
-        fill<<<grid, kThreads, 0, ctx->stream>>>(prm);
+        if (fill16) {
+            const int64_t units = (count + 1) / 2;
+            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((units + gpb - 1) / gpb, max_grid16));
+            fill16<<<grid, kThreads, 0, ctx->stream>>>(prm);
+        } else {
+            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((count + gpb - 1) / gpb, max_grid));
+            fill<<<grid, kThreads, 0, ctx->stream>>>(prm);
+        }
         TB_TRY(cudaGetLastError());
         TB_TRY(cudaMemsetAsync(d_cnt + count, 0, sizeof(int32_t), ctx->stream));
         tb_launch_walk<1>(atype, prm, ctx->stream);

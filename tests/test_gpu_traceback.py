@@ -167,3 +167,33 @@ def test_long_pairs_rescore_to_their_score(ctx, align_type):
         assert all(a[0] != b[0] for a, b in zip(ops, ops[1:]))      # runs arrive merged
     if align_type != "global":
         assert got["score"][2] == 800 and (got["s_start"][2], got["s_end"][2]) == (5000, 5400)
+
+
+@pytest.mark.parametrize("align_type", ["global", "semiglobal"])
+def test_packed_int16_fill_uniform_batches(ctx, align_type):
+    """Uniform affine global / semiglobal batches of one stage take the packed int16 fill (traceback_fill16.cuh): two
+    alignments per thread.  Odd counts, flagged symbols on both sides, rectangular shapes, several schemes."""
+    rng = np.random.default_rng(1607)
+    for (m, n, count), sch in zip([(250, 250, 301), (100, 128, 64), (37, 256, 33), (250, 90, 17), (1, 1, 5), (200, 256, 1),
+                                   (129, 131, 40), (256, 255, 9)],
+                                  [(2, -1, 2, 1), (2, -1, 2, 1), (1, -3, 5, 2), (2, -1, 2, 1), (2, -1, 2, 1), (5, -4, 10, 1),
+                                   (3, -2, 0, 1), (2, -1, 2, 1)]):
+        scheme = scheme_of(sch, "affine")
+        qs, ss = [], []
+        for k in range(count):
+            q = random_codes(rng, m)
+            if k % 2 == 0 and m == n:
+                s = mutate_codes(rng, q, 0.05, 0.0, 0.0)
+                cut = int(rng.integers(1, max(2, n - 1)))
+                s = np.concatenate([s[:cut], s[cut + 1:], random_codes(rng, 1)]) if k % 4 == 0 and n >= 3 else s   # one deletion
+            else:
+                s = random_codes(rng, n)
+            if k % 5 == 0:
+                q = q.copy(); q[rng.integers(0, m)] = 4
+            if k % 7 == 0:
+                s = s.copy(); s[rng.integers(0, n)] = 4
+            assert len(q) == m and len(s) == n
+            qs.append(q); ss.append(s)
+        pairs = [(i, i) for i in range(count)]
+        assert_tb_equal(gpu_traceback(ctx, qs, ss, pairs, scheme, align_type), oracle_traceback(qs, ss, pairs, scheme, align_type),
+                        f"{align_type} {m}x{n} {sch}")
