@@ -22,31 +22,70 @@
 
 namespace wsb {
 
-constexpr int kNeg16 = -24000;   // "minus infinity" of the packed fill: below every reachable value, never extended twice
+#ifndef WSB_TB16_ALU_E
+#define WSB_TB16_ALU_E 0
+#endif
+constexpr bool kMarkE = WSB_TB16_ALU_E != 0;   // 1: set the "E extends" plane bits on the ALU pipe (measured 9 % slower: the packed adds already live there)
+#ifndef WSB_TB16_FMA_ADDS
+#define WSB_TB16_FMA_ADDS 0
+#endif
+// Values are stored biased by kBias16 per half, so that every half is a non-negative number: subtracting a packed
+// non-negative constant with ONE 32-bit operation then never borrows across the halves, and the three "minus gap cost"
+// steps of the cell can issue as IMAD on the FMA pipe instead of VIADD.16x2 on the ALU pipe (bit mask: 1 = E - beta,
+// 2 = F - beta, 4 = H - alpha).
+constexpr int kFmaAdds = WSB_TB16_FMA_ADDS;
+constexpr int kBias16 = 16384;
+constexpr int kNeg16 = -16000;   // "minus infinity" of the packed fill: below every reachable value, never extended twice
 
 // the packed fill is exact while every reachable value stays inside int16 with room for one more step below kNeg16
 __host__ __device__ inline bool tb_fill16_range_ok(int m, int n, int match, int mismatch, int alpha, int beta) {
     const int64_t lo = 3ll * alpha + (int64_t)beta * (m + n) + (mismatch < 0 ? -mismatch : mismatch) + (match < 0 ? -match : match);
     const int64_t hi = (int64_t)(match > 0 ? match : 0) * (m < n ? m : n) + alpha + beta;
-    return lo <= 8000 && hi <= 32000 && alpha <= 4000 && beta <= 4000;
+    return lo <= 8000 && hi <= 16000 && alpha <= 300 && beta <= 300;
 }
 
-__device__ __forceinline__ unsigned pk16(int v) { return ((unsigned)v & 0xffffu) * 0x00010001u; }
-__device__ __forceinline__ int lo16(unsigned v) { return (int)(short)(v & 0xffffu); }
-__device__ __forceinline__ int hi16(unsigned v) { return (int)v >> 16; }
+__device__ __forceinline__ unsigned pk16(int v) { return ((unsigned)v & 0xffffu) * 0x00010001u; }          // plain, both halves
+__device__ __forceinline__ unsigned pk16b(int v) { return (unsigned)(v + kBias16) * 0x00010001u; }           // biased value
+__device__ __forceinline__ int lo16(unsigned v) { return (int)(v & 0xffffu) - kBias16; }
+__device__ __forceinline__ int hi16(unsigned v) { return (int)(v >> 16) - kBias16; }
+// x - cost in both halves (cost = c * 0x10001, 0 <= c <= every half of x): one IMAD, or VIADD.16x2 with the negated halves
+template <bool ON_FMA>
+__device__ __forceinline__ unsigned sub_cost(unsigned x, unsigned cost32, unsigned neg2, int one) {
+    if (ON_FMA) {
+        unsigned r;
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(one), "r"(0u - cost32), "r"(x));
+        return r;
+    }
+    return __vadd2(x, neg2);
+}
 
-// packed max(a, b), "a wins ties"; the plane bit goes to wlo / whi where a won in the low / high half
+// packed max(a, b), "a wins ties"; the plane bit goes to wlo / whi where a won in the low / high half.  The bit is
+// set on the FMA pipe (IMAD with the opaque multiplier one == 1) or, ON_ALU, on the ALU pipe (predicated LOP3): the cell
+// mixes both so that neither pipe carries the whole load.
+template <bool ON_ALU>
 __device__ __forceinline__ unsigned max_mark2(unsigned a, unsigned b, uint32_t& wlo, uint32_t& whi, uint32_t bit, int one) {
     unsigned r;
-    asm("{\n\t.reg .pred pl, ph;\n\t.reg .s16 r0, r1, a0, a1;\n\t"
-        "max.s16x2 %0, %3, %4;\n\t"
-        "mov.b32 {r0, r1}, %0;\n\t"
-        "mov.b32 {a0, a1}, %3;\n\t"
-        "setp.eq.s16 pl, r0, a0;\n\t"
-        "setp.eq.s16 ph, r1, a1;\n\t"
-        "@pl mad.lo.u32 %1, %6, %5, %1;\n\t"
-        "@ph mad.lo.u32 %2, %6, %5, %2;\n\t"
-        "}" : "=r"(r), "+r"(wlo), "+r"(whi) : "r"(a), "r"(b), "r"(bit), "r"(one));
+    if (ON_ALU) {
+        asm("{\n\t.reg .pred pl, ph;\n\t.reg .s16 r0, r1, a0, a1;\n\t"
+            "max.s16x2 %0, %3, %4;\n\t"
+            "mov.b32 {r0, r1}, %0;\n\t"
+            "mov.b32 {a0, a1}, %3;\n\t"
+            "setp.eq.s16 pl, r0, a0;\n\t"
+            "setp.eq.s16 ph, r1, a1;\n\t"
+            "@pl or.b32 %1, %1, %5;\n\t"
+            "@ph or.b32 %2, %2, %5;\n\t"
+            "}" : "=r"(r), "+r"(wlo), "+r"(whi) : "r"(a), "r"(b), "r"(bit));
+    } else {
+        asm("{\n\t.reg .pred pl, ph;\n\t.reg .s16 r0, r1, a0, a1;\n\t"
+            "max.s16x2 %0, %3, %4;\n\t"
+            "mov.b32 {r0, r1}, %0;\n\t"
+            "mov.b32 {a0, a1}, %3;\n\t"
+            "setp.eq.s16 pl, r0, a0;\n\t"
+            "setp.eq.s16 ph, r1, a1;\n\t"
+            "@pl mad.lo.u32 %1, %6, %5, %1;\n\t"
+            "@ph mad.lo.u32 %2, %6, %5, %2;\n\t"
+            "}" : "=r"(r), "+r"(wlo), "+r"(whi) : "r"(a), "r"(b), "r"(bit), "r"(one));
+    }
     return r;
 }
 
@@ -65,8 +104,9 @@ __global__ void __launch_bounds__(kThreads) tb_fill16_kernel(const TbParams prm)
     const int64_t n_groups = (int64_t)gridDim.x * GPB;
     const int alpha = prm.alpha, beta = prm.beta, one = prm.one;
     const unsigned nb2 = pk16(-beta), na2 = pk16(-alpha);
-    const unsigned base2 = pk16(prm.mismatch + alpha), delta2 = pk16(prm.match - prm.mismatch);
-    const unsigned neg2 = pk16(kNeg16);
+    const unsigned cb32 = (unsigned)beta * 0x00010001u, ca32 = (unsigned)alpha * 0x00010001u;
+    const unsigned miss2 = pk16(prm.mismatch + alpha), hit2 = pk16(prm.match + alpha);   // sigma + alpha, both halves
+    const unsigned neg2 = pk16b(kNeg16);
     const int64_t n_units = (prm.n_pairs + 1) / 2;
 
     // all lane groups of a warp run the same number of rounds (the shuffles below are warp-wide); a group without a unit
@@ -98,13 +138,13 @@ __global__ void __launch_bounds__(kThreads) tb_fill16_kernel(const TbParams prm)
                 x = x < 4u ? x : 5u; y = y < 4u ? y : 5u;
             }
             ss[c] = (0x4000u | x) | ((0x4000u | y) << 16);
-            AL[c] = pk16(edge_h(GLOBAL_EDGES, col0 + c + 1, alpha, beta) - alpha);
+            AL[c] = pk16b(edge_h(GLOBAL_EDGES, col0 + c + 1, alpha, beta) - alpha);
             EP[c] = neg2;
         }
-        const unsigned al_top = pk16(edge_h(GLOBAL_EDGES, col0, alpha, beta) - alpha);
+        const unsigned al_top = pk16b(edge_h(GLOBAL_EDGES, col0, alpha, beta) - alpha);
         unsigned al_diag = al_top, all = neg2, fpl = neg2;
         int edge = edge_h(GLOBAL_EDGES, 1, alpha, beta);
-        if (t == 0) all = pk16(edge - alpha);
+        if (t == 0) all = pk16b(edge - alpha);
         const int cap_rel = n - 1 - col0;
         const bool has_cap = cap_rel >= 0 && cap_rel < K;
         int bv_a = GLOBAL_EDGES ? kNeg32 : 0, bi_a = 0, bj_a = ATYPE == AT_SEMI ? n : 0;
@@ -132,16 +172,16 @@ __global__ void __launch_bounds__(kThreads) tb_fill16_kernel(const TbParams prm)
 #pragma unroll
                     for (int c8 = 0; c8 < 8; ++c8) {
                         const int c = w8 * 8 + c8;
-                        const unsigned hit = __heq2_mask(qh, *reinterpret_cast<const __half2*>(&ss[c]));
-                        const unsigned d = __vadd2(__vadd2(ad, base2), hit & delta2);
+                        const unsigned eq = __heq2_mask(qh, *reinterpret_cast<const __half2*>(&ss[c]));
+                        const unsigned d = __vadd2(ad, (eq & hit2) | (~eq & miss2));   // one LOP3 selects per half
                         ad = AL[c];
-                        const unsigned e = max_mark2(EP[c], AL[c], we_a, we_b, 1u << (16 + c8), one);
-                        const unsigned f = max_mark2(fl, al, wf_a, wf_b, 1u << (24 + c8), one);
-                        EP[c] = __vadd2(e, nb2);
-                        fl = __vadd2(f, nb2);
-                        const unsigned m1 = max_mark2(d, e, wd_a, wd_b, 1u << c8, one);
-                        const unsigned h = max_mark2(m1, f, wm_a, wm_b, 1u << (8 + c8), one);
-                        al = __vadd2(h, na2);
+                        const unsigned e = max_mark2<kMarkE>(EP[c], AL[c], we_a, we_b, 1u << (16 + c8), one);
+                        const unsigned f = max_mark2<false>(fl, al, wf_a, wf_b, 1u << (24 + c8), one);
+                        EP[c] = sub_cost<(kFmaAdds & 1) != 0>(e, cb32, nb2, one);
+                        fl = sub_cost<(kFmaAdds & 2) != 0>(f, cb32, nb2, one);
+                        const unsigned m1 = max_mark2<false>(d, e, wd_a, wd_b, 1u << c8, one);
+                        const unsigned h = max_mark2<false>(m1, f, wm_a, wm_b, 1u << (8 + c8), one);
+                        al = sub_cost<(kFmaAdds & 4) != 0>(h, ca32, na2, one);
                         AL[c] = al;
                     }
                     wa[w8] = (wd_a | wm_a) | (we_a | wf_a);
@@ -173,7 +213,7 @@ __global__ void __launch_bounds__(kThreads) tb_fill16_kernel(const TbParams prm)
             al_diag = all;
             if (t == 0) {
                 if (GLOBAL_EDGES) edge -= beta;
-                nal = pk16(edge - alpha); nfp = neg2;
+                nal = pk16b(edge - alpha); nfp = neg2;
             }
             all = nal; fpl = nfp;
             if (r == 0) al_diag = al_top;

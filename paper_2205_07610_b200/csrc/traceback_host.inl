@@ -11,11 +11,13 @@
 struct TbShape { int P, K; };
 static const TbShape kTbShapes[] = {{8, 16}, {8, 32}, {32, 16}, {16, 16}};
 
-static int tb_pick_shape(int max_n) {
+static int tb_pick_shape(int max_n, bool packed16) {
     static const char* force = getenv("WSB_TB_SHAPE");  // tuning aid
     if (force && force[0]) return std::min(3, std::max(0, atoi(force)));
     if (max_n <= 128) return 0;
-    if (max_n <= 256) return 1;   // (8,32); (16,16) = index 3 doubles the resident warps but measured 2 % slower at 250 bp
+    // int32 fill: (8,32); (16,16) = index 3 doubles the resident warps but measured 2 % slower at 250 bp.  The packed int16
+    // fill is the other way round (1529 vs 1453 GCUPS on cfg3): its (8,32) form needs 198 registers
+    if (max_n <= 256) return packed16 ? 3 : 1;
     return 2;
 }
 
@@ -34,6 +36,7 @@ static TbFillFn tb_pick_fill16(int shape, int atype) {
     const bool g = atype == AT_GLOBAL;
     if (shape == 0) return g ? tb_fill16_kernel<8, 16, AT_GLOBAL> : tb_fill16_kernel<8, 16, AT_SEMI>;
     if (shape == 1) return g ? tb_fill16_kernel<8, 32, AT_GLOBAL> : tb_fill16_kernel<8, 32, AT_SEMI>;
+    if (shape == 3) return g ? tb_fill16_kernel<16, 16, AT_GLOBAL> : tb_fill16_kernel<16, 16, AT_SEMI>;
     return nullptr;
 }
 
@@ -81,17 +84,17 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
     int max_m = 0, max_n = 0;
     if (b->uniform) { max_m = b->m[0]; max_n = b->n[0]; }
     else for (int64_t p = 0; p < np; ++p) { max_m = std::max(max_m, b->m[p]); max_n = std::max(max_n, b->n[p]); }
-    const int shape = tb_pick_shape(max_n);
+    // two alignments per thread in int16 halves where the batch allows it
+    static const bool no16 = getenv("WSB_TB_NO16") != nullptr;   // tuning aid
+    const bool can16 = !no16 && affine && atype != AT_LOCAL && b->uniform && max_m > 0 && max_n > 0 &&
+                       (!score_plan || score_plan->status.empty() || score_plan->status[0] == 0) &&
+                       tb_fill16_range_ok(max_m, max_n, sch->match, sch->mismatch, sch->gap_open, sch->gap_extend);
+    const int shape = tb_pick_shape(max_n, can16);
     const int P = kTbShapes[shape].P, K = kTbShapes[shape].K;
     TbFillFn fill = shape == 0 ? tb_pick_fill<8, 16>(atype, affine)
                   : shape == 1 ? tb_pick_fill<8, 32>(atype, affine)
                   : shape == 2 ? tb_pick_fill<32, 16>(atype, affine) : tb_pick_fill<16, 16>(atype, affine);
-    // two alignments per thread in int16 halves where the batch allows it
-    static const bool no16 = getenv("WSB_TB_NO16") != nullptr;   // tuning aid
-    TbFillFn fill16 = nullptr;
-    if (!no16 && affine && b->uniform && max_m > 0 && max_n > 0 && max_n <= P * K && (!score_plan || score_plan->status.empty() || score_plan->status[0] == 0) &&
-        tb_fill16_range_ok(max_m, max_n, sch->match, sch->mismatch, sch->gap_open, sch->gap_extend))
-        fill16 = tb_pick_fill16(shape, atype);
+    TbFillFn fill16 = (can16 && max_n <= P * K) ? tb_pick_fill16(shape, atype) : nullptr;
     size_t budget_words = (size_t)16384 << 18;  // 16 GiB in 32-bit words (a B200 carries 180 GB)
     if (const char* e = getenv("WSB_TB_SCRATCH_MB")) { const long mb = atol(e); if (mb > 0) budget_words = (size_t)mb << 18; }
 
