@@ -89,8 +89,11 @@ __device__ __forceinline__ unsigned max_mark2(unsigned a, unsigned b, uint32_t& 
     return r;
 }
 
+#ifndef WSB_TB16_MINB
+#define WSB_TB16_MINB 1
+#endif
 template <int P, int K, int ATYPE>
-__global__ void __launch_bounds__(kThreads) tb_fill16_kernel(const TbParams prm) {
+__global__ void __launch_bounds__(kThreads, K >= 32 ? WSB_TB16_MINB : 1) tb_fill16_kernel(const TbParams prm) {
     constexpr int GPB = kThreads / P;
     constexpr int NW = K / 8;
     constexpr bool GLOBAL_EDGES = ATYPE == AT_GLOBAL;
