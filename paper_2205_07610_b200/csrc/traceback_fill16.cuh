@@ -89,11 +89,12 @@ __device__ __forceinline__ unsigned max_mark2(unsigned a, unsigned b, uint32_t& 
     return r;
 }
 
-#ifndef WSB_TB16_MINB
-#define WSB_TB16_MINB 1
-#endif
-template <int P, int K, int ATYPE>
-__global__ void __launch_bounds__(kThreads, K >= 32 ? WSB_TB16_MINB : 1) tb_fill16_kernel(const TbParams prm) {
+// RAGGED = false: every pair of the launch has the same (m, n) (checked on the host), so the two alignments of a unit
+// share every bound.  RAGGED = true: the halves carry pairs of different sizes; the unit runs max(m) rows, every half
+// stores and tracks only inside its own rectangle (junk outside it flows right / down only, never back in -- the
+// argument of the reference's packed mode, _kernels.py:557-562), and rejected or empty pairs ride along masked out.
+template <int P, int K, int ATYPE, bool RAGGED>
+__global__ void __launch_bounds__(kThreads) tb_fill16_kernel(const TbParams prm) {
     constexpr int GPB = kThreads / P;
     constexpr int NW = K / 8;
     constexpr bool GLOBAL_EDGES = ATYPE == AT_GLOBAL;
@@ -123,23 +124,30 @@ __global__ void __launch_bounds__(kThreads, K >= 32 ? WSB_TB16_MINB : 1) tb_fill
         const int64_t ua = 2 * u, ub = twin ? ua + 1 : ua;
         const int64_t pa = prm.first_pair + ua, pb = prm.first_pair + ub;
         const int qa_i = prm.pair_q[pa], sa_i = prm.pair_s[pa], qb_i = prm.pair_q[pb], sb_i = prm.pair_s[pb];
-        const int m = prm.q_len[qa_i], n = prm.s_len[sa_i];
+        int m_a = prm.q_len[qa_i], n_a = prm.s_len[sa_i];
+        int m_b = RAGGED ? prm.q_len[qb_i] : m_a, n_b = RAGGED ? prm.s_len[sb_i] : n_a;
+        bool keep_a = live, keep_b = live && twin;   // this half stores codes and reports a result
+        if (RAGGED) {   // rejected (negative code offset) or empty pairs: masked out, nothing read through their pointers
+            if (prm.code_off[ua] < 0 || m_a == 0 || n_a == 0) { m_a = 0; n_a = 0; keep_a = false; }
+            if (prm.code_off[ub] < 0 || m_b == 0 || n_b == 0) { m_b = 0; n_b = 0; keep_b = false; }
+        }
+        const int mm = max(m_a, m_b);
+        const int mm_w = RAGGED ? __reduce_max_sync(0xffffffffu, mm) : mm;
+        if (mm_w == 0) continue;
         const uint8_t* qa = prm.q_codes + prm.q_off[qa_i];
         const uint8_t* qb = prm.q_codes + prm.q_off[qb_i];
         const uint8_t* sa = prm.s_codes + prm.s_off[sa_i];
         const uint8_t* sb = prm.s_codes + prm.s_off[sb_i];
-        uint32_t* code_a = prm.codes + prm.code_off[ua];
-        uint32_t* code_b = prm.codes + prm.code_off[ub];
+        uint32_t* code_a = prm.codes + (keep_a ? prm.code_off[ua] : 0);
+        uint32_t* code_b = prm.codes + (keep_b ? prm.code_off[ub] : 0);
         const int col0 = t * K;
 
         unsigned ss[K], AL[K], EP[K];
 #pragma unroll
         for (int c = 0; c < K; ++c) {
             unsigned x = 5u, y = 5u;
-            if (col0 + c < n) {
-                x = sa[col0 + c]; y = sb[col0 + c];
-                x = x < 4u ? x : 5u; y = y < 4u ? y : 5u;
-            }
+            if (col0 + c < n_a) { x = sa[col0 + c]; x = x < 4u ? x : 5u; }
+            if (col0 + c < n_b) { y = sb[col0 + c]; y = y < 4u ? y : 5u; }
             ss[c] = (0x4000u | x) | ((0x4000u | y) << 16);
             AL[c] = pk16b(edge_h(GLOBAL_EDGES, col0 + c + 1, alpha, beta) - alpha);
             EP[c] = neg2;
@@ -148,24 +156,39 @@ __global__ void __launch_bounds__(kThreads, K >= 32 ? WSB_TB16_MINB : 1) tb_fill
         unsigned al_diag = al_top, all = neg2, fpl = neg2;
         int edge = edge_h(GLOBAL_EDGES, 1, alpha, beta);
         if (t == 0) all = pk16b(edge - alpha);
-        const int cap_rel = n - 1 - col0;
-        const bool has_cap = cap_rel >= 0 && cap_rel < K;
-        int bv_a = GLOBAL_EDGES ? kNeg32 : 0, bi_a = 0, bj_a = ATYPE == AT_SEMI ? n : 0;
-        int bv_b = bv_a, bi_b = bi_a, bj_b = bj_a;
+        const int cap_a = n_a - 1 - col0, cap_b = n_b - 1 - col0;   // register index of matrix column n, if in this strip
+        const bool has_cap_a = cap_a >= 0 && cap_a < K, has_cap_b = cap_b >= 0 && cap_b < K;
+        int bv_a = GLOBAL_EDGES ? kNeg32 : 0, bi_a = 0, bj_a = ATYPE == AT_SEMI ? n_a : 0;
+        int bv_b = bv_a, bi_b = 0, bj_b = ATYPE == AT_SEMI ? n_b : 0;
+
+        // row m of a half: semiglobal scans it, global reads H(m, n)
+        auto last_row = [&](bool second, int m, int n, bool has_cap, int cap_rel, int& bv, int& bi, int& bj) {
+            if (ATYPE == AT_SEMI) {
+#pragma unroll
+                for (int c = 0; c < K; ++c)
+                    if (col0 + c < n) {
+                        const int v = (second ? hi16(AL[c]) : lo16(AL[c])) + alpha;
+                        if (better_cell(v, m, col0 + c + 1, bv, bi, bj)) { bv = v; bi = m; bj = col0 + c + 1; }
+                    }
+            } else if (has_cap) {
+                const unsigned hv = select_reg<unsigned, K>(AL, cap_rel);
+                bv = (second ? hi16(hv) : lo16(hv)) + alpha; bi = m; bj = n;
+            }
+        };
 
         auto q_at = [&](int it) {
-            const int idx = min(max(it - t - 1, 0), m - 1);
-            unsigned a = qa[idx], b = qb[idx];
-            a = a < 4u ? a : 4u; b = b < 4u ? b : 4u;
+            unsigned a = 4u, b = 4u;
+            if (!RAGGED || m_a > 0) { a = qa[min(max(it - t - 1, 0), m_a - 1)]; a = a < 4u ? a : 4u; }
+            if (!RAGGED || m_b > 0) { b = qb[min(max(it - t - 1, 0), m_b - 1)]; b = b < 4u ? b : 4u; }
             return (0x4000u | a) | ((0x4000u | b) << 16);
         };
         unsigned q_cur = q_at(1), q_nxt = q_at(2);
-        const int it_end = m + P - 1;
+        const int it_end = mm_w + P - 1;
         for (int it = 1; it <= it_end; ++it) {
             const unsigned q_nn = q_at(it + 2);
             const int r = it - t;
             unsigned out_al = all, out_fp = fpl;
-            if (r >= 1 && r <= m) {
+            if (r >= 1 && r <= mm) {
                 const __half2 qh = *reinterpret_cast<const __half2*>(&q_cur);
                 unsigned ad = al_diag, fl = fpl, al = all;
                 uint32_t wa[NW], wb[NW];
@@ -191,24 +214,32 @@ __global__ void __launch_bounds__(kThreads, K >= 32 ? WSB_TB16_MINB : 1) tb_fill
                     wb[w8] = (wd_b | wm_b) | (we_b | wf_b);
                 }
                 const int64_t at = ((int64_t)(it - 1) * P + t) * NW;   // wavefront-major, one stage
-                if (!live) {
-                } else if (NW == 2) {
-                    *reinterpret_cast<uint2*>(code_a + at) = make_uint2(wa[0], wa[1]);
-                    if (twin) *reinterpret_cast<uint2*>(code_b + at) = make_uint2(wb[0], wb[1]);
+                const bool st_a = keep_a && (!RAGGED || r <= m_a), st_b = keep_b && (!RAGGED || r <= m_b);
+                if (NW == 2) {
+                    if (st_a) *reinterpret_cast<uint2*>(code_a + at) = make_uint2(wa[0], wa[1]);
+                    if (st_b) *reinterpret_cast<uint2*>(code_b + at) = make_uint2(wb[0], wb[1]);
                 } else if (NW == 4) {
-                    *reinterpret_cast<uint4*>(code_a + at) = make_uint4(wa[0], wa[1], wa[2], wa[NW - 1]);
-                    if (twin) *reinterpret_cast<uint4*>(code_b + at) = make_uint4(wb[0], wb[1], wb[2], wb[NW - 1]);
+                    if (st_a) *reinterpret_cast<uint4*>(code_a + at) = make_uint4(wa[0], wa[1], wa[2], wa[NW - 1]);
+                    if (st_b) *reinterpret_cast<uint4*>(code_b + at) = make_uint4(wb[0], wb[1], wb[2], wb[NW - 1]);
                 } else {
 #pragma unroll
-                    for (int w8 = 0; w8 < NW; ++w8) { code_a[at + w8] = wa[w8]; if (twin) code_b[at + w8] = wb[w8]; }
+                    for (int w8 = 0; w8 < NW; ++w8) { if (st_a) code_a[at + w8] = wa[w8]; if (st_b) code_b[at + w8] = wb[w8]; }
                 }
                 out_al = al;
                 out_fp = fl;
-                if (ATYPE == AT_SEMI && has_cap && r < m) {   // last matrix column, rows above the last one
-                    const unsigned hv = select_reg<unsigned, K>(AL, cap_rel);
-                    const int va = lo16(hv) + alpha, vb = hi16(hv) + alpha;
-                    if (better_cell(va, r, n, bv_a, bi_a, bj_a)) { bv_a = va; bi_a = r; bj_a = n; }
-                    if (better_cell(vb, r, n, bv_b, bi_b, bj_b)) { bv_b = vb; bi_b = r; bj_b = n; }
+                if (ATYPE == AT_SEMI) {   // last matrix column, rows above the last one
+                    if (has_cap_a && r < m_a) {
+                        const int v = lo16(select_reg<unsigned, K>(AL, cap_a)) + alpha;
+                        if (better_cell(v, r, n_a, bv_a, bi_a, bj_a)) { bv_a = v; bi_a = r; bj_a = n_a; }
+                    }
+                    if (has_cap_b && r < m_b) {
+                        const int v = hi16(select_reg<unsigned, K>(AL, cap_b)) + alpha;
+                        if (better_cell(v, r, n_b, bv_b, bi_b, bj_b)) { bv_b = v; bi_b = r; bj_b = n_b; }
+                    }
+                }
+                if (RAGGED) {   // the shorter half of a unit finishes before the registers reach row max(m)
+                    if (r == m_a && m_a < mm) last_row(false, m_a, n_a, has_cap_a, cap_a, bv_a, bi_a, bj_a);
+                    if (r == m_b && m_b < mm) last_row(true, m_b, n_b, has_cap_b, cap_b, bv_b, bi_b, bj_b);
                 }
             }
             unsigned nal = __shfl_up_sync(0xffffffffu, out_al, 1, P);
@@ -222,20 +253,9 @@ __global__ void __launch_bounds__(kThreads, K >= 32 ? WSB_TB16_MINB : 1) tb_fill
             if (r == 0) al_diag = al_top;
             q_cur = q_nxt; q_nxt = q_nn;
         }
-        // every lane's registers now hold row m of its strip
-        if (ATYPE == AT_SEMI) {
-#pragma unroll
-            for (int c = 0; c < K; ++c)
-                if (col0 + c < n) {
-                    const int va = lo16(AL[c]) + alpha, vb = hi16(AL[c]) + alpha;
-                    if (better_cell(va, m, col0 + c + 1, bv_a, bi_a, bj_a)) { bv_a = va; bi_a = m; bj_a = col0 + c + 1; }
-                    if (better_cell(vb, m, col0 + c + 1, bv_b, bi_b, bj_b)) { bv_b = vb; bi_b = m; bj_b = col0 + c + 1; }
-                }
-        }
-        if (GLOBAL_EDGES && has_cap) {
-            const unsigned hv = select_reg<unsigned, K>(AL, cap_rel);
-            bv_a = lo16(hv) + alpha; bv_b = hi16(hv) + alpha; bi_a = bi_b = m; bj_a = bj_b = n;
-        }
+        // every lane's registers now hold row max(m) of its strip
+        if (m_a == mm && m_a > 0) last_row(false, m_a, n_a, has_cap_a, cap_a, bv_a, bi_a, bj_a);
+        if (m_b == mm && m_b > 0) last_row(true, m_b, n_b, has_cap_b, cap_b, bv_b, bi_b, bj_b);
         const unsigned gmask = group_mask<P>(tid & 31);
 #pragma unroll
         for (int off = P / 2; off >= 1; off >>= 1) {
@@ -244,9 +264,9 @@ __global__ void __launch_bounds__(kThreads, K >= 32 ? WSB_TB16_MINB : 1) tb_fill
             ov = __shfl_xor_sync(gmask, bv_b, off, P); oi = __shfl_xor_sync(gmask, bi_b, off, P); oj = __shfl_xor_sync(gmask, bj_b, off, P);
             if (better_cell(ov, oi, oj, bv_b, bi_b, bj_b)) { bv_b = ov; bi_b = oi; bj_b = oj; }
         }
-        if (t == 0 && live) {
-            prm.w_score[pa] = bv_a; prm.w_i[pa] = bi_a; prm.w_j[pa] = bj_a;
-            if (twin) { prm.w_score[pb] = bv_b; prm.w_i[pb] = bi_b; prm.w_j[pb] = bj_b; }
+        if (t == 0) {
+            if (keep_a) { prm.w_score[pa] = bv_a; prm.w_i[pa] = bi_a; prm.w_j[pa] = bj_a; }
+            if (keep_b) { prm.w_score[pb] = bv_b; prm.w_i[pb] = bi_b; prm.w_j[pb] = bj_b; }
         }
         __syncwarp();
     }

@@ -30,13 +30,16 @@ template <int P, int K> static TbFillFn tb_pick_fill(int atype, bool affine) {
     }
 }
 
-// packed int16 fill (traceback_fill16.cuh): uniform affine global / semiglobal batches of one stage
-static TbFillFn tb_pick_fill16(int shape, int atype) {
+// packed int16 fill (traceback_fill16.cuh): affine global / semiglobal batches of one stage, two alignments per thread
+template <int P, int K> static TbFillFn tb_pick_fill16_shape(int atype, bool ragged) {
+    if (atype == AT_GLOBAL) return ragged ? tb_fill16_kernel<P, K, AT_GLOBAL, true> : tb_fill16_kernel<P, K, AT_GLOBAL, false>;
+    return ragged ? tb_fill16_kernel<P, K, AT_SEMI, true> : tb_fill16_kernel<P, K, AT_SEMI, false>;
+}
+static TbFillFn tb_pick_fill16(int shape, int atype, bool ragged) {
     if (atype == AT_LOCAL) return nullptr;
-    const bool g = atype == AT_GLOBAL;
-    if (shape == 0) return g ? tb_fill16_kernel<8, 16, AT_GLOBAL> : tb_fill16_kernel<8, 16, AT_SEMI>;
-    if (shape == 1) return g ? tb_fill16_kernel<8, 32, AT_GLOBAL> : tb_fill16_kernel<8, 32, AT_SEMI>;
-    if (shape == 3) return g ? tb_fill16_kernel<16, 16, AT_GLOBAL> : tb_fill16_kernel<16, 16, AT_SEMI>;
+    if (shape == 0) return tb_pick_fill16_shape<8, 16>(atype, ragged);
+    if (shape == 1) return tb_pick_fill16_shape<8, 32>(atype, ragged);
+    if (shape == 3) return tb_pick_fill16_shape<16, 16>(atype, ragged);
     return nullptr;
 }
 
@@ -86,15 +89,16 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
     else for (int64_t p = 0; p < np; ++p) { max_m = std::max(max_m, b->m[p]); max_n = std::max(max_n, b->n[p]); }
     // two alignments per thread in int16 halves where the batch allows it
     static const bool no16 = getenv("WSB_TB_NO16") != nullptr;   // tuning aid
-    const bool can16 = !no16 && affine && atype != AT_LOCAL && b->uniform && max_m > 0 && max_n > 0 &&
-                       (!score_plan || score_plan->status.empty() || score_plan->status[0] == 0) &&
+    const bool can16 = !no16 && affine && atype != AT_LOCAL && max_m > 0 && max_n > 0 &&
                        tb_fill16_range_ok(max_m, max_n, sch->match, sch->mismatch, sch->gap_open, sch->gap_extend);
+    // equal-sized pairs without rejected ones share every bound; anything else takes the masked (ragged) form
+    const bool ragged16 = !b->uniform || !(!score_plan || score_plan->status.empty() || score_plan->status[0] == 0);
     const int shape = tb_pick_shape(max_n, can16);
     const int P = kTbShapes[shape].P, K = kTbShapes[shape].K;
     TbFillFn fill = shape == 0 ? tb_pick_fill<8, 16>(atype, affine)
                   : shape == 1 ? tb_pick_fill<8, 32>(atype, affine)
                   : shape == 2 ? tb_pick_fill<32, 16>(atype, affine) : tb_pick_fill<16, 16>(atype, affine);
-    TbFillFn fill16 = (can16 && max_n <= P * K) ? tb_pick_fill16(shape, atype) : nullptr;
+    TbFillFn fill16 = (can16 && max_n <= P * K) ? tb_pick_fill16(shape, atype, ragged16) : nullptr;
     size_t budget_words = (size_t)16384 << 18;  // 16 GiB in 32-bit words (a B200 carries 180 GB)
     if (const char* e = getenv("WSB_TB_SCRATCH_MB")) { const long mb = atol(e); if (mb > 0) budget_words = (size_t)mb << 18; }
 

@@ -197,3 +197,33 @@ def test_packed_int16_fill_uniform_batches(ctx, align_type):
         pairs = [(i, i) for i in range(count)]
         assert_tb_equal(gpu_traceback(ctx, qs, ss, pairs, scheme, align_type), oracle_traceback(qs, ss, pairs, scheme, align_type),
                         f"{align_type} {m}x{n} {sch}")
+
+
+@pytest.mark.parametrize("align_type", ["global", "semiglobal"])
+def test_packed_int16_fill_ragged_batches(ctx, align_type):
+    """Pairs of different sizes share a thread's halves (masked form of the packed fill): every half must store and track
+    only inside its own rectangle.  Includes empty sides, one-symbol sides, flagged symbols and an odd pair count."""
+    rng = np.random.default_rng(4242)
+    for sch, hi, count in (((2, -1, 2, 1), 256, 401), ((1, -3, 5, 2), 128, 77), ((5, -4, 10, 1), 200, 150)):
+        scheme = scheme_of(sch, "affine")
+        qs, ss = [], []
+        for k in range(count):
+            m = int(rng.integers(1, hi + 1)); n = int(rng.integers(1, hi + 1))
+            if k % 9 == 0:
+                m = int(rng.integers(1, 4))
+            if k % 11 == 0:
+                n = hi
+            q = random_codes(rng, m)
+            s = mutate_codes(rng, q, 0.06, 0.03, 0.03)[:hi] if k % 2 else random_codes(rng, n)
+            if k % 5 == 0:
+                q = q.copy(); q[rng.integers(0, len(q))] = 4
+            if k % 7 == 0 and len(s):
+                s = s.copy(); s[rng.integers(0, len(s))] = 4
+            if k in (13, 14, 200):
+                s = np.zeros(0, np.uint8)
+            if k in (14, 15):
+                q = np.zeros(0, np.uint8)
+            qs.append(q); ss.append(s)
+        pairs = [(i, i) for i in range(count)]
+        assert_tb_equal(gpu_traceback(ctx, qs, ss, pairs, scheme, align_type), oracle_traceback(qs, ss, pairs, scheme, align_type),
+                        f"{align_type} ragged {sch}")
