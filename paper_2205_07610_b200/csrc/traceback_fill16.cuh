@@ -12,9 +12,10 @@
 // exact whatever the denormal mode); flagged query symbols are 0x4004, flagged or padded subject symbols 0x4005, which
 // never compare equal (core.py:147-151: flagged symbols never match, even N-N).
 //
-// Scope (the host checks it, traceback_host.inl): affine gaps, global or semiglobal, every pair of the launch has the same
-// (m, n) with n <= P*K (one stage, no border scratch), and the int16 range rule below holds.  Everything else -- local
-// alignments (their stop encoding needs H itself), ragged batches, long reads -- stays on the int32 fill.
+// Scope (the host checks it, traceback_host.inl): affine gaps, every subject of the launch within one stage (n <= P*K,
+// no border scratch), and the int16 range rule below.  Linear gaps, longer reads and wider schemes stay on the int32
+// fill.  Local alignments add a fifth max per packed cell (0 against H: the "H == 0" stop plane, folded into the two
+// origin planes once per eight cells).
 #pragma once
 #include "traceback_kernels.cuh"
 
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(kThreads) tb_fill16_kernel(const TbParams prm)
     constexpr int GPB = kThreads / P;
     constexpr int NW = K / 8;
     constexpr bool GLOBAL_EDGES = ATYPE == AT_GLOBAL;
-    static_assert(ATYPE != AT_LOCAL, "local alignments use the int32 fill");
+    constexpr bool LOCAL = ATYPE == AT_LOCAL;   // end cells come from the score pass; H == 0 is stored as a stop code
     static_assert(K % 8 == 0, "K must pack into whole code words");
 
     const int tid = threadIdx.x;
@@ -111,6 +112,9 @@ __global__ void __launch_bounds__(kThreads) tb_fill16_kernel(const TbParams prm)
     const unsigned cb32 = (unsigned)beta * 0x00010001u, ca32 = (unsigned)alpha * 0x00010001u;
     const unsigned miss2 = pk16(prm.mismatch + alpha), hit2 = pk16(prm.match + alpha);   // sigma + alpha, both halves
     const unsigned neg2 = pk16b(kNeg16);
+    // biased zero for the local stop test, kept opaque (times one == 1): as an immediate ptxas 12.9 moves it to the second
+    // operand of VIMNMX.S16x2 and keeps using the "first operand won" predicates unchanged, which marks the wrong side
+    const unsigned zero2 = pk16b(0) * (unsigned)one;
     const int64_t n_units = (prm.n_pairs + 1) / 2;
 
     // all lane groups of a warp run the same number of rounds (the shuffles below are warp-wide); a group without a unit
@@ -195,6 +199,7 @@ __global__ void __launch_bounds__(kThreads) tb_fill16_kernel(const TbParams prm)
 #pragma unroll
                 for (int w8 = 0; w8 < NW; ++w8) {
                     uint32_t wd_a = 0u, wm_a = 0u, we_a = 0u, wf_a = 0u, wd_b = 0u, wm_b = 0u, we_b = 0u, wf_b = 0u;
+                    uint32_t ws_a = 0u, ws_b = 0u;   // local: "H == 0" plane, folded into the two origin planes below
 #pragma unroll
                     for (int c8 = 0; c8 < 8; ++c8) {
                         const int c = w8 * 8 + c8;
@@ -206,9 +211,14 @@ __global__ void __launch_bounds__(kThreads) tb_fill16_kernel(const TbParams prm)
                         EP[c] = sub_cost<(kFmaAdds & 1) != 0>(e, cb32, nb2, one);
                         fl = sub_cost<(kFmaAdds & 2) != 0>(f, cb32, nb2, one);
                         const unsigned m1 = max_mark2<false>(d, e, wd_a, wd_b, 1u << c8, one);
-                        const unsigned h = max_mark2<false>(m1, f, wm_a, wm_b, 1u << (8 + c8), one);
+                        unsigned h = max_mark2<false>(m1, f, wm_a, wm_b, 1u << (8 + c8), one);
+                        if (LOCAL) h = max_mark2<false>(zero2, h, ws_a, ws_b, 1u << c8, one);   // 0 wins ties: stop iff H <= 0
                         al = sub_cost<(kFmaAdds & 4) != 0>(h, ca32, na2, one);
                         AL[c] = al;
+                    }
+                    if (LOCAL) {   // stop = "F wins" with the diagonal bit set (tb_code_at): pd = (pd && pm) || stop, pm = pm && !stop
+                        wd_a = (wd_a & (wm_a >> 8)) | ws_a; wm_a &= ~(ws_a << 8);
+                        wd_b = (wd_b & (wm_b >> 8)) | ws_b; wm_b &= ~(ws_b << 8);
                     }
                     wa[w8] = (wd_a | wm_a) | (we_a | wf_a);
                     wb[w8] = (wd_b | wm_b) | (we_b | wf_b);
@@ -237,7 +247,7 @@ __global__ void __launch_bounds__(kThreads) tb_fill16_kernel(const TbParams prm)
                         if (better_cell(v, r, n_b, bv_b, bi_b, bj_b)) { bv_b = v; bi_b = r; bj_b = n_b; }
                     }
                 }
-                if (RAGGED) {   // the shorter half of a unit finishes before the registers reach row max(m)
+                if (RAGGED && !LOCAL) {   // the shorter half of a unit finishes before the registers reach row max(m)
                     if (r == m_a && m_a < mm) last_row(false, m_a, n_a, has_cap_a, cap_a, bv_a, bi_a, bj_a);
                     if (r == m_b && m_b < mm) last_row(true, m_b, n_b, has_cap_b, cap_b, bv_b, bi_b, bj_b);
                 }
@@ -254,6 +264,7 @@ __global__ void __launch_bounds__(kThreads) tb_fill16_kernel(const TbParams prm)
             q_cur = q_nxt; q_nxt = q_nn;
         }
         // every lane's registers now hold row max(m) of its strip
+        if (LOCAL) { __syncwarp(); continue; }
         if (m_a == mm && m_a > 0) last_row(false, m_a, n_a, has_cap_a, cap_a, bv_a, bi_a, bj_a);
         if (m_b == mm && m_b > 0) last_row(true, m_b, n_b, has_cap_b, cap_b, bv_b, bi_b, bj_b);
         const unsigned gmask = group_mask<P>(tid & 31);

@@ -30,13 +30,13 @@ template <int P, int K> static TbFillFn tb_pick_fill(int atype, bool affine) {
     }
 }
 
-// packed int16 fill (traceback_fill16.cuh): affine global / semiglobal batches of one stage, two alignments per thread
+// packed int16 fill (traceback_fill16.cuh): affine batches of one stage, two alignments per thread
 template <int P, int K> static TbFillFn tb_pick_fill16_shape(int atype, bool ragged) {
     if (atype == AT_GLOBAL) return ragged ? tb_fill16_kernel<P, K, AT_GLOBAL, true> : tb_fill16_kernel<P, K, AT_GLOBAL, false>;
+    if (atype == AT_LOCAL) return ragged ? tb_fill16_kernel<P, K, AT_LOCAL, true> : tb_fill16_kernel<P, K, AT_LOCAL, false>;
     return ragged ? tb_fill16_kernel<P, K, AT_SEMI, true> : tb_fill16_kernel<P, K, AT_SEMI, false>;
 }
 static TbFillFn tb_pick_fill16(int shape, int atype, bool ragged) {
-    if (atype == AT_LOCAL) return nullptr;
     if (shape == 0) return tb_pick_fill16_shape<8, 16>(atype, ragged);
     if (shape == 1) return tb_pick_fill16_shape<8, 32>(atype, ragged);
     if (shape == 3) return tb_pick_fill16_shape<16, 16>(atype, ragged);
@@ -89,7 +89,7 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
     else for (int64_t p = 0; p < np; ++p) { max_m = std::max(max_m, b->m[p]); max_n = std::max(max_n, b->n[p]); }
     // two alignments per thread in int16 halves where the batch allows it
     static const bool no16 = getenv("WSB_TB_NO16") != nullptr;   // tuning aid
-    const bool can16 = !no16 && affine && atype != AT_LOCAL && max_m > 0 && max_n > 0 &&
+    const bool can16 = !no16 && affine && max_m > 0 && max_n > 0 &&
                        tb_fill16_range_ok(max_m, max_n, sch->match, sch->mismatch, sch->gap_open, sch->gap_extend);
     // equal-sized pairs without rejected ones share every bound; anything else takes the masked (ragged) form
     const bool ragged16 = !b->uniform || !(!score_plan || score_plan->status.empty() || score_plan->status[0] == 0);

@@ -248,3 +248,22 @@ def test_wire_formats_and_bench_conventions(tmp_path):
     assert abs(W.theoretical_peak(hw) - 9306.24) < 0.01
     with pytest.raises(ValueError):
         W.HardwareModel(0, 1.0, 1.0)
+
+
+def test_packed_traceback_fill_keeps_its_max_operand_order():
+    """max_mark2 (traceback_fill16.cuh) relies on VIMNMX.S16x2's per-half "first operand won" predicates.  ptxas 12.9
+    moves an immediate operand into second place WITHOUT adjusting the predicate uses (seen with the local stop test's
+    zero), so the built library must not contain a predicated packed max with an immediate operand."""
+    import shutil, subprocess
+    lib = N.library_path() if hasattr(N, "library_path") else os.path.join(os.path.dirname(N.__file__), "libwsb200.so")
+    dump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(lib) or not os.path.exists(dump):
+        pytest.skip("library or cuobjdump not available")
+    names = subprocess.run([dump, "-elf", lib], capture_output=True, text=True).stdout
+    funcs = sorted(set(re.findall(r"_ZN3wsb16tb_fill16_kernel\w+", names)))
+    assert funcs, "packed fill kernels missing from the library"
+    sass = subprocess.run([dump, "-sass", *sum((["-fun", f] for f in funcs), []), lib], capture_output=True, text=True).stdout
+    maxes = [ln for ln in sass.splitlines() if "VIMNMX.S16x2" in ln]
+    assert len(maxes) > 100
+    bad = [ln for ln in maxes if re.search(r"VIMNMX\.S16x2 R\d+, P[0-6], P[0-6], R\d+, (0x|-0x|c\[)", ln)]
+    assert not bad, bad[:3]

@@ -169,9 +169,9 @@ def test_long_pairs_rescore_to_their_score(ctx, align_type):
         assert got["score"][2] == 800 and (got["s_start"][2], got["s_end"][2]) == (5000, 5400)
 
 
-@pytest.mark.parametrize("align_type", ["global", "semiglobal"])
+@pytest.mark.parametrize("align_type", ["global", "semiglobal", "local"])
 def test_packed_int16_fill_uniform_batches(ctx, align_type):
-    """Uniform affine global / semiglobal batches of one stage take the packed int16 fill (traceback_fill16.cuh): two
+    """Uniform affine batches of one stage take the packed int16 fill (traceback_fill16.cuh): two
     alignments per thread.  Odd counts, flagged symbols on both sides, rectangular shapes, several schemes."""
     rng = np.random.default_rng(1607)
     for (m, n, count), sch in zip([(250, 250, 301), (100, 128, 64), (37, 256, 33), (250, 90, 17), (1, 1, 5), (200, 256, 1),
@@ -199,7 +199,7 @@ def test_packed_int16_fill_uniform_batches(ctx, align_type):
                         f"{align_type} {m}x{n} {sch}")
 
 
-@pytest.mark.parametrize("align_type", ["global", "semiglobal"])
+@pytest.mark.parametrize("align_type", ["global", "semiglobal", "local"])
 def test_packed_int16_fill_ragged_batches(ctx, align_type):
     """Pairs of different sizes share a thread's halves (masked form of the packed fill): every half must store and track
     only inside its own rectangle.  Includes empty sides, one-symbol sides, flagged symbols and an odd pair count."""

@@ -14,9 +14,10 @@ bad = 0
 for rd in range(rounds):
     os.environ["WSB_TB_SCRATCH_MB"] = str(int(rng.choice([1, 4, 64, 4096])))
     n = int(rng.integers(10, 300))
+    short = rng.random() < 0.5   # every subject within one stage: affine global / semiglobal take the packed int16 fill
     qs, ss = [], []
     for k in range(n):
-        m = int(rng.integers(1, 1200)) if rng.random() < 0.3 else int(rng.integers(1, 300))
+        m = int(rng.integers(1, 1200)) if (rng.random() < 0.3 and not short) else int(rng.integers(1, 300))
         q = rng.integers(0, 4, m).astype(np.uint8)
         if rng.random() < 0.6:
             keep = rng.random(m) > 0.04
@@ -27,6 +28,7 @@ for rd in range(rounds):
         else:
             s = rng.integers(0, 4, int(rng.integers(1, 400))).astype(np.uint8)
         if len(s) == 0: s = np.array([1], np.uint8)
+        if short: s = s[:int(rng.choice([128, 256]))].copy()
         if rng.random() < 0.15: q[int(rng.integers(0, len(q)))] = 4
         if rng.random() < 0.15: s[int(rng.integers(0, len(s)))] = 4
         qs.append(q); ss.append(s)
