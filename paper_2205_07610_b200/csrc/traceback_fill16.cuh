@@ -63,6 +63,23 @@ __device__ __forceinline__ unsigned sub_cost(unsigned x, unsigned cost32, unsign
 // packed max(a, b), "a wins ties"; the plane bit goes to wlo / whi where a won in the low / high half.  The bit is
 // set on the FMA pipe (IMAD with the opaque multiplier one == 1) or, ON_ALU, on the ALU pipe (predicated LOP3): the cell
 // mixes both so that neither pipe carries the whole load.
+// a[idx] for a register array (K a power of two): a binary tree of K - 1 selects under log2(K) predicates, where the
+// linear compare-and-select chain of select_reg costs 2K instructions -- it runs on every row of a semiglobal fill
+template <int K>
+__device__ __forceinline__ unsigned pick_reg(const unsigned (&a)[K], int idx) {
+    static_assert((K & (K - 1)) == 0, "power of two");
+    unsigned v[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) v[i] = a[i];
+#pragma unroll
+    for (int width = K / 2, bit = 1; width >= 1; width /= 2, bit *= 2) {
+        const bool odd = (idx & bit) != 0;
+#pragma unroll
+        for (int i = 0; i < width; ++i) v[i] = odd ? v[2 * i + 1] : v[2 * i];
+    }
+    return v[0];
+}
+
 template <bool ON_ALU>
 __device__ __forceinline__ unsigned max_mark2(unsigned a, unsigned b, uint32_t& wlo, uint32_t& whi, uint32_t bit, int one) {
     unsigned r;
@@ -142,8 +159,8 @@ __global__ void __launch_bounds__(kThreads) tb_fill16_kernel(const TbParams prm)
         const uint8_t* qb = prm.q_codes + prm.q_off[qb_i];
         const uint8_t* sa = prm.s_codes + prm.s_off[sa_i];
         const uint8_t* sb = prm.s_codes + prm.s_off[sb_i];
-        uint32_t* code_a = prm.codes + (keep_a ? prm.code_off[ua] : 0);
-        uint32_t* code_b = prm.codes + (keep_b ? prm.code_off[ub] : 0);
+        uint32_t* code_a = prm.codes + ((!RAGGED || keep_a) ? prm.code_off[ua] : 0);
+        uint32_t* code_b = prm.codes + ((!RAGGED || keep_b) ? prm.code_off[ub] : 0);
         const int col0 = t * K;
 
         unsigned ss[K], AL[K], EP[K];
@@ -224,7 +241,9 @@ __global__ void __launch_bounds__(kThreads) tb_fill16_kernel(const TbParams prm)
                     wb[w8] = (wd_b | wm_b) | (we_b | wf_b);
                 }
                 const int64_t at = ((int64_t)(it - 1) * P + t) * NW;   // wavefront-major, one stage
-                const bool st_a = keep_a && (!RAGGED || r <= m_a), st_b = keep_b && (!RAGGED || r <= m_b);
+                // equal-sized pairs: no guards -- an odd tail's second half and a group without a unit of its own recompute an
+                // existing alignment and store the same words to the same place
+                const bool st_a = !RAGGED || (keep_a && r <= m_a), st_b = !RAGGED || (keep_b && r <= m_b);
                 if (NW == 2) {
                     if (st_a) *reinterpret_cast<uint2*>(code_a + at) = make_uint2(wa[0], wa[1]);
                     if (st_b) *reinterpret_cast<uint2*>(code_b + at) = make_uint2(wb[0], wb[1]);
@@ -239,11 +258,11 @@ __global__ void __launch_bounds__(kThreads) tb_fill16_kernel(const TbParams prm)
                 out_fp = fl;
                 if (ATYPE == AT_SEMI) {   // last matrix column, rows above the last one
                     if (has_cap_a && r < m_a) {
-                        const int v = lo16(select_reg<unsigned, K>(AL, cap_a)) + alpha;
+                        const int v = lo16(pick_reg<K>(AL, cap_a)) + alpha;
                         if (better_cell(v, r, n_a, bv_a, bi_a, bj_a)) { bv_a = v; bi_a = r; bj_a = n_a; }
                     }
                     if (has_cap_b && r < m_b) {
-                        const int v = hi16(select_reg<unsigned, K>(AL, cap_b)) + alpha;
+                        const int v = hi16(pick_reg<K>(AL, cap_b)) + alpha;
                         if (better_cell(v, r, n_b, bv_b, bi_b, bj_b)) { bv_b = v; bi_b = r; bj_b = n_b; }
                     }
                 }
