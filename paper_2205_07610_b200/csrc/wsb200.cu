@@ -121,7 +121,7 @@ struct wsb_batch {
     int32_t* d_redo = nullptr;   // packed int16 kernel: list of pairs to re-score (slot 0 = count, list from slot 4)
     // Piecewise upload: piece k covers pairs [piece_end[k-1], piece_end[k]) and is complete (pools included) once
     // piece_ev[k] has fired on the copy stream; the first score call after creation launches piece by piece.
-    static constexpr int kMaxPieces = 8;
+    static constexpr int kMaxPieces = 16;
     int n_pieces = 0;
     int n_pieces_usable = 0;             // 1: score only after the whole upload (packed pools with flagged positions)
     void* stage_blocks[4] = {};          // packed-pool staging areas, released with the batch
@@ -434,7 +434,10 @@ static int batch_create_impl(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t
     // scored while the slices of later pieces are still on the bus.  (Arbitrary pair lists degrade gracefully: the
     // first piece then simply waits for most of the pool.)
     int n_pieces = 1;
-    if (n_pairs >= 262144 && q_total + s_total >= ((int64_t)32 << 20)) n_pieces = wsb_batch::kMaxPieces;
+    if (n_pairs >= 262144 && q_total + s_total >= ((int64_t)32 << 20)) {
+        static const int want = [] { const char* e = getenv("WSB_PIECES"); return e ? atoi(e) : 8; }();   // tuning aid
+        n_pieces = std::min<int>(wsb_batch::kMaxPieces, std::max(1, want));
+    }
     b->n_pieces = n_pieces;
     std::vector<int64_t> need_q((size_t)n_pieces, 0), need_s((size_t)n_pieces, 0);
     {
