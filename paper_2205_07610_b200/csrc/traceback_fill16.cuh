@@ -63,16 +63,18 @@ __device__ __forceinline__ unsigned sub_cost(unsigned x, unsigned cost32, unsign
 // packed max(a, b), "a wins ties"; the plane bit goes to wlo / whi where a won in the low / high half.  The bit is
 // set on the FMA pipe (IMAD with the opaque multiplier one == 1) or, ON_ALU, on the ALU pipe (predicated LOP3): the cell
 // mixes both so that neither pipe carries the whole load.
-// a[idx] for a register array (K a power of two): a binary tree of K - 1 selects under log2(K) predicates, where the
-// linear compare-and-select chain of select_reg costs 2K instructions -- it runs on every row of a semiglobal fill
+// a[idx] for a register array: a binary tree of selects under log2 predicates (the array is padded to a power of two with
+// copies of its last element), where the linear compare-and-select chain of select_reg costs 2K instructions -- it runs
+// on every row of a semiglobal fill
 template <int K>
 __device__ __forceinline__ unsigned pick_reg(const unsigned (&a)[K], int idx) {
-    static_assert((K & (K - 1)) == 0, "power of two");
-    unsigned v[K];
+    constexpr int N = K <= 8 ? 8 : K <= 16 ? 16 : K <= 32 ? 32 : 64;
+    static_assert(K <= N, "strip too wide");
+    unsigned v[N];
 #pragma unroll
-    for (int i = 0; i < K; ++i) v[i] = a[i];
+    for (int i = 0; i < N; ++i) v[i] = a[i < K ? i : K - 1];
 #pragma unroll
-    for (int width = K / 2, bit = 1; width >= 1; width /= 2, bit *= 2) {
+    for (int width = N / 2, bit = 1; width >= 1; width /= 2, bit *= 2) {
         const bool odd = (idx & bit) != 0;
 #pragma unroll
         for (int i = 0; i < width; ++i) v[i] = odd ? v[2 * i + 1] : v[2 * i];

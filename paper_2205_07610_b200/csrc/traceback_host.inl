@@ -9,14 +9,15 @@
 #include "traceback_fill16.cuh"
 
 struct TbShape { int P, K; };
-static const TbShape kTbShapes[] = {{8, 16}, {8, 32}, {32, 16}, {16, 16}};
+static const TbShape kTbShapes[] = {{8, 16}, {8, 32}, {32, 16}, {16, 16}, {8, 24}};   // index 4: packed int16 fill only
 
 static int tb_pick_shape(int max_n, bool packed16) {
     static const char* force = getenv("WSB_TB_SHAPE");  // tuning aid
-    if (force && force[0]) return std::min(3, std::max(0, atoi(force)));
+    if (force && force[0]) return std::min(packed16 ? 4 : 3, std::max(0, atoi(force)));
     if (max_n <= 128) return 0;
     // int32 fill: (8,32); (16,16) = index 3 doubles the resident warps but measured 2 % slower at 250 bp.  The packed int16
     // fill is the other way round (1529 vs 1453 GCUPS on cfg3): its (8,32) form needs 198 registers
+    if (packed16 && max_n <= 192) return 4;   // (8,24): 150 bp reads fill 78 % of the strip instead of 59 % of 256 columns
     if (max_n <= 256) return packed16 ? 3 : 1;
     return 2;
 }
@@ -40,6 +41,7 @@ static TbFillFn tb_pick_fill16(int shape, int atype, bool ragged) {
     if (shape == 0) return tb_pick_fill16_shape<8, 16>(atype, ragged);
     if (shape == 1) return tb_pick_fill16_shape<8, 32>(atype, ragged);
     if (shape == 3) return tb_pick_fill16_shape<16, 16>(atype, ragged);
+    if (shape == 4) return tb_pick_fill16_shape<8, 24>(atype, ragged);
     return nullptr;
 }
 
@@ -97,7 +99,8 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
     const int P = kTbShapes[shape].P, K = kTbShapes[shape].K;
     TbFillFn fill = shape == 0 ? tb_pick_fill<8, 16>(atype, affine)
                   : shape == 1 ? tb_pick_fill<8, 32>(atype, affine)
-                  : shape == 2 ? tb_pick_fill<32, 16>(atype, affine) : tb_pick_fill<16, 16>(atype, affine);
+                  : shape == 2 ? tb_pick_fill<32, 16>(atype, affine)
+                  : shape == 3 ? tb_pick_fill<16, 16>(atype, affine) : tb_pick_fill<8, 32>(atype, affine);   // 4: never launched
     TbFillFn fill16 = (can16 && max_n <= P * K) ? tb_pick_fill16(shape, atype, ragged16) : nullptr;
     size_t budget_words = (size_t)16384 << 18;  // 16 GiB in 32-bit words (a B200 carries 180 GB)
     if (const char* e = getenv("WSB_TB_SCRATCH_MB")) { const long mb = atol(e); if (mb > 0) budget_words = (size_t)mb << 18; }

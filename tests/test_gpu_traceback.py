@@ -175,9 +175,9 @@ def test_packed_int16_fill_uniform_batches(ctx, align_type):
     alignments per thread.  Odd counts, flagged symbols on both sides, rectangular shapes, several schemes."""
     rng = np.random.default_rng(1607)
     for (m, n, count), sch in zip([(250, 250, 301), (100, 128, 64), (37, 256, 33), (250, 90, 17), (1, 1, 5), (200, 256, 1),
-                                   (129, 131, 40), (256, 255, 9)],
+                                   (129, 131, 40), (256, 255, 9), (150, 150, 101), (180, 192, 21)],
                                   [(2, -1, 2, 1), (2, -1, 2, 1), (1, -3, 5, 2), (2, -1, 2, 1), (2, -1, 2, 1), (5, -4, 10, 1),
-                                   (3, -2, 0, 1), (2, -1, 2, 1)]):
+                                   (3, -2, 0, 1), (2, -1, 2, 1), (2, -1, 2, 1), (4, -3, 3, 2)]):
         scheme = scheme_of(sch, "affine")
         qs, ss = [], []
         for k in range(count):
@@ -204,7 +204,7 @@ def test_packed_int16_fill_ragged_batches(ctx, align_type):
     """Pairs of different sizes share a thread's halves (masked form of the packed fill): every half must store and track
     only inside its own rectangle.  Includes empty sides, one-symbol sides, flagged symbols and an odd pair count."""
     rng = np.random.default_rng(4242)
-    for sch, hi, count in (((2, -1, 2, 1), 256, 401), ((1, -3, 5, 2), 128, 77), ((5, -4, 10, 1), 200, 150)):
+    for sch, hi, count in (((2, -1, 2, 1), 256, 401), ((1, -3, 5, 2), 128, 77), ((5, -4, 10, 1), 200, 150), ((2, -1, 2, 1), 190, 99)):
         scheme = scheme_of(sch, "affine")
         qs, ss = [], []
         for k in range(count):
