@@ -114,7 +114,7 @@ __device__ __forceinline__ unsigned max_mark2(unsigned a, unsigned b, uint32_t& 
 // stores and tracks only inside its own rectangle (junk outside it flows right / down only, never back in -- the
 // argument of the reference's packed mode, _kernels.py:557-562), and rejected or empty pairs ride along masked out.
 template <int P, int K, int ATYPE, bool RAGGED>
-__global__ void __launch_bounds__(kThreads) tb_fill16_kernel(const TbParams prm) {
+__global__ void __launch_bounds__(kThreads, K <= 16 ? 4 : 1) tb_fill16_kernel(const TbParams prm) {
     constexpr int GPB = kThreads / P;
     constexpr int NW = K / 8;
     constexpr bool GLOBAL_EDGES = ATYPE == AT_GLOBAL;

@@ -278,7 +278,7 @@ __device__ __forceinline__ uint32_t tb_code_at(const uint32_t* code, int i, int 
     const int t = col / K, c = col - t * K;
     const int it = i + t;
     const int64_t word = (((int64_t)st * (m + P - 1) + (it - 1)) * P + t) * (K / 8) + c / 8;
-    const uint32_t bits = code[word] >> (c % 8);
+    const uint32_t bits = __ldcg(code + word) >> (c % 8);   // L2 only: random 4-byte reads
     const bool pd = bits & 1u, pm = bits & 0x100u;
     const uint32_t origin = pm ? (pd ? 1u : 2u) : ((LOCAL && pd) ? 0u : 3u);   // local: "F wins" + diagonal bit = stop
     return origin | ((bits >> 14) & 4u) | ((bits >> 21) & 8u);
@@ -289,18 +289,9 @@ constexpr int kTbTmpRuns = 128;   // unrelated 250 bp reads average 77 runs, 99t
 // PASS 1 counts the runs, records the start cell and parks the first kTbTmpRuns runs (in walk order); PASS 2 writes the
 // runs in forward order: a reversed copy of the parked runs, or a second walk for alignments with more runs than that.
 template <int ATYPE, int PASS>
-__global__ void tb_walk_kernel(const TbParams prm) {
-    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= prm.n_pairs) return;
-    const int64_t p = prm.first_pair + u;
-    const int m = prm.q_len[prm.pair_q[p]], n = prm.s_len[prm.pair_s[p]];
-    if (prm.code_off[u] < 0) {  // rejected pair: no alignment
-        if (PASS == 1) { prm.n_runs[u] = 0; prm.start_i[p] = 0; prm.start_j[p] = 0; }
-        return;
-    }
-    const uint32_t* code = prm.codes + prm.code_off[u];
+__device__ __forceinline__ void tb_walk_pair(const TbParams& prm, int64_t u, int64_t p, int m, int n, const uint32_t* code,
+                                             int i, int j) {
     const int P = prm.tb_p, K = prm.tb_k;
-    int i = prm.end_i[p], j = prm.end_j[p];
     uint32_t* out = nullptr;
     int64_t w = 0;
     if (PASS == 2) { out = prm.runs + prm.run_off[u]; w = prm.n_runs[u]; }
@@ -353,6 +344,19 @@ __global__ void tb_walk_kernel(const TbParams prm) {
         prm.start_i[p] = i;
         prm.start_j[p] = j;
     }
+}
+
+template <int ATYPE, int PASS>
+__global__ void tb_walk_kernel(const TbParams prm) {
+    const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= prm.n_pairs) return;
+    const int64_t p = prm.first_pair + u;
+    const int m = prm.q_len[prm.pair_q[p]], n = prm.s_len[prm.pair_s[p]];
+    if (prm.code_off[u] < 0) {  // rejected pair: no alignment
+        if (PASS == 1) { prm.n_runs[u] = 0; prm.start_i[p] = 0; prm.start_j[p] = 0; }
+        return;
+    }
+    tb_walk_pair<ATYPE, PASS>(prm, u, p, m, n, prm.codes + prm.code_off[u], prm.end_i[p], prm.end_j[p]);
 }
 
 __global__ void add_base_kernel(const int64_t* chunk_off, int64_t base, int64_t count, int64_t* out) {
