@@ -12,9 +12,9 @@
 // exact whatever the denormal mode); flagged query symbols are 0x4004, flagged or padded subject symbols 0x4005, which
 // never compare equal (core.py:147-151: flagged symbols never match, even N-N).
 //
-// Scope (the host checks it, traceback_host.inl): affine gaps, every subject of the launch within one stage (n <= P*K,
-// no border scratch), and the int16 range rule below.  Linear gaps, longer reads and wider schemes stay on the int32
-// fill.  Local alignments add a fifth max per packed cell (0 against H: the "H == 0" stop plane, folded into the two
+// Scope (the host checks it, traceback_host.inl): every subject of the launch within one stage (n <= P*K, no border
+// scratch) and the int16 range rule below; affine or linear gaps (AFFINE = false drops E / F and their planes: two
+// packed maxes per cell).  Longer reads and wider schemes stay on the int32 fill.  Local alignments add a fifth max per packed cell (0 against H: the "H == 0" stop plane, folded into the two
 // origin planes once per eight cells).
 #pragma once
 #include "traceback_kernels.cuh"
@@ -113,7 +113,7 @@ __device__ __forceinline__ unsigned max_mark2(unsigned a, unsigned b, uint32_t& 
 // share every bound.  RAGGED = true: the halves carry pairs of different sizes; the unit runs max(m) rows, every half
 // stores and tracks only inside its own rectangle (junk outside it flows right / down only, never back in -- the
 // argument of the reference's packed mode, _kernels.py:557-562), and rejected or empty pairs ride along masked out.
-template <int P, int K, int ATYPE, bool RAGGED>
+template <int P, int K, int ATYPE, bool RAGGED, bool AFFINE = true>
 __global__ void __launch_bounds__(kThreads, K <= 16 ? 4 : 1) tb_fill16_kernel(const TbParams prm) {
     constexpr int GPB = kThreads / P;
     constexpr int NW = K / 8;
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(kThreads, K <= 16 ? 4 : 1) tb_fill16_kernel(co
         uint32_t* code_b = prm.codes + ((!RAGGED || keep_b) ? prm.code_off[ub] : 0);
         const int col0 = t * K;
 
-        unsigned ss[K], AL[K], EP[K];
+        unsigned ss[K], AL[K], EP[AFFINE ? K : 1];
 #pragma unroll
         for (int c = 0; c < K; ++c) {
             unsigned x = 5u, y = 5u;
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, K <= 16 ? 4 : 1) tb_fill16_kernel(co
             if (col0 + c < n_b) { y = sb[col0 + c]; y = y < 4u ? y : 5u; }
             ss[c] = (0x4000u | x) | ((0x4000u | y) << 16);
             AL[c] = pk16b(edge_h(GLOBAL_EDGES, col0 + c + 1, alpha, beta) - alpha);
-            EP[c] = neg2;
+            if (AFFINE) EP[c] = neg2;
         }
         const unsigned al_top = pk16b(edge_h(GLOBAL_EDGES, col0, alpha, beta) - alpha);
         unsigned al_diag = al_top, all = neg2, fpl = neg2;
@@ -225,10 +225,13 @@ __global__ void __launch_bounds__(kThreads, K <= 16 ? 4 : 1) tb_fill16_kernel(co
                         const unsigned eq = __heq2_mask(qh, *reinterpret_cast<const __half2*>(&ss[c]));
                         const unsigned d = __vadd2(ad, (eq & hit2) | (~eq & miss2));   // one LOP3 selects per half
                         ad = AL[c];
-                        const unsigned e = max_mark2<kMarkE>(EP[c], AL[c], we_a, we_b, 1u << (16 + c8), one);
-                        const unsigned f = max_mark2<false>(fl, al, wf_a, wf_b, 1u << (24 + c8), one);
-                        EP[c] = sub_cost<(kFmaAdds & 1) != 0>(e, cb32, nb2, one);
-                        fl = sub_cost<(kFmaAdds & 2) != 0>(f, cb32, nb2, one);
+                        unsigned e = AL[c], f = al;   // linear gaps: E = H(up) - alpha, F = H(left) - alpha, no extension planes
+                        if (AFFINE) {
+                            e = max_mark2<kMarkE>(EP[c], AL[c], we_a, we_b, 1u << (16 + c8), one);
+                            f = max_mark2<false>(fl, al, wf_a, wf_b, 1u << (24 + c8), one);
+                            EP[c] = sub_cost<(kFmaAdds & 1) != 0>(e, cb32, nb2, one);
+                            fl = sub_cost<(kFmaAdds & 2) != 0>(f, cb32, nb2, one);
+                        }
                         const unsigned m1 = max_mark2<false>(d, e, wd_a, wd_b, 1u << c8, one);
                         unsigned h = max_mark2<false>(m1, f, wm_a, wm_b, 1u << (8 + c8), one);
                         if (LOCAL) h = max_mark2<false>(zero2, h, ws_a, ws_b, 1u << c8, one);   // 0 wins ties: stop iff H <= 0

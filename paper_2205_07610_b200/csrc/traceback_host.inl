@@ -31,17 +31,20 @@ template <int P, int K> static TbFillFn tb_pick_fill(int atype, bool affine) {
     }
 }
 
-// packed int16 fill (traceback_fill16.cuh): affine batches of one stage, two alignments per thread
-template <int P, int K> static TbFillFn tb_pick_fill16_shape(int atype, bool ragged) {
-    if (atype == AT_GLOBAL) return ragged ? tb_fill16_kernel<P, K, AT_GLOBAL, true> : tb_fill16_kernel<P, K, AT_GLOBAL, false>;
-    if (atype == AT_LOCAL) return ragged ? tb_fill16_kernel<P, K, AT_LOCAL, true> : tb_fill16_kernel<P, K, AT_LOCAL, false>;
-    return ragged ? tb_fill16_kernel<P, K, AT_SEMI, true> : tb_fill16_kernel<P, K, AT_SEMI, false>;
+// packed int16 fill (traceback_fill16.cuh): batches of one stage, two alignments per thread
+template <int P, int K, bool AFFINE> static TbFillFn tb_pick_fill16_gap(int atype, bool ragged) {
+    if (atype == AT_GLOBAL) return ragged ? tb_fill16_kernel<P, K, AT_GLOBAL, true, AFFINE> : tb_fill16_kernel<P, K, AT_GLOBAL, false, AFFINE>;
+    if (atype == AT_LOCAL) return ragged ? tb_fill16_kernel<P, K, AT_LOCAL, true, AFFINE> : tb_fill16_kernel<P, K, AT_LOCAL, false, AFFINE>;
+    return ragged ? tb_fill16_kernel<P, K, AT_SEMI, true, AFFINE> : tb_fill16_kernel<P, K, AT_SEMI, false, AFFINE>;
 }
-static TbFillFn tb_pick_fill16(int shape, int atype, bool ragged) {
-    if (shape == 0) return tb_pick_fill16_shape<8, 16>(atype, ragged);
-    if (shape == 1) return tb_pick_fill16_shape<8, 32>(atype, ragged);
-    if (shape == 3) return tb_pick_fill16_shape<16, 16>(atype, ragged);
-    if (shape == 4) return tb_pick_fill16_shape<8, 24>(atype, ragged);
+template <int P, int K> static TbFillFn tb_pick_fill16_shape(int atype, bool ragged, bool affine) {
+    return affine ? tb_pick_fill16_gap<P, K, true>(atype, ragged) : tb_pick_fill16_gap<P, K, false>(atype, ragged);
+}
+static TbFillFn tb_pick_fill16(int shape, int atype, bool ragged, bool affine) {
+    if (shape == 0) return tb_pick_fill16_shape<8, 16>(atype, ragged, affine);
+    if (shape == 1) return tb_pick_fill16_shape<8, 32>(atype, ragged, affine);
+    if (shape == 3) return tb_pick_fill16_shape<16, 16>(atype, ragged, affine);
+    if (shape == 4) return tb_pick_fill16_shape<8, 24>(atype, ragged, affine);
     return nullptr;
 }
 
@@ -91,8 +94,8 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
     else for (int64_t p = 0; p < np; ++p) { max_m = std::max(max_m, b->m[p]); max_n = std::max(max_n, b->n[p]); }
     // two alignments per thread in int16 halves where the batch allows it
     static const bool no16 = getenv("WSB_TB_NO16") != nullptr;   // tuning aid
-    const bool can16 = !no16 && affine && max_m > 0 && max_n > 0 &&
-                       tb_fill16_range_ok(max_m, max_n, sch->match, sch->mismatch, sch->gap_open, sch->gap_extend);
+    const bool can16 = !no16 && max_m > 0 && max_n > 0 &&
+                       tb_fill16_range_ok(max_m, max_n, sch->match, sch->mismatch, sch->gap_open, beta_eff);
     // equal-sized pairs without rejected ones share every bound; anything else takes the masked (ragged) form
     const bool ragged16 = !b->uniform || !(!score_plan || score_plan->status.empty() || score_plan->status[0] == 0);
     const int shape = tb_pick_shape(max_n, can16);
@@ -101,7 +104,7 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
                   : shape == 1 ? tb_pick_fill<8, 32>(atype, affine)
                   : shape == 2 ? tb_pick_fill<32, 16>(atype, affine)
                   : shape == 3 ? tb_pick_fill<16, 16>(atype, affine) : tb_pick_fill<8, 32>(atype, affine);   // 4: never launched
-    TbFillFn fill16 = (can16 && max_n <= P * K) ? tb_pick_fill16(shape, atype, ragged16) : nullptr;
+    TbFillFn fill16 = (can16 && max_n <= P * K) ? tb_pick_fill16(shape, atype, ragged16, affine) : nullptr;
     size_t budget_words = (size_t)16384 << 18;  // 16 GiB in 32-bit words (a B200 carries 180 GB)
     if (const char* e = getenv("WSB_TB_SCRATCH_MB")) { const long mb = atol(e); if (mb > 0) budget_words = (size_t)mb << 18; }
 

@@ -178,7 +178,8 @@ def test_packed_int16_fill_uniform_batches(ctx, align_type):
                                    (129, 131, 40), (256, 255, 9), (150, 150, 101), (180, 192, 21)],
                                   [(2, -1, 2, 1), (2, -1, 2, 1), (1, -3, 5, 2), (2, -1, 2, 1), (2, -1, 2, 1), (5, -4, 10, 1),
                                    (3, -2, 0, 1), (2, -1, 2, 1), (2, -1, 2, 1), (4, -3, 3, 2)]):
-        scheme = scheme_of(sch, "affine")
+        linear = (m + n) % 3 == 0   # a third of the shapes run the linear-gap form
+        scheme = scheme_of((sch[0], sch[1], max(1, sch[2]), max(1, sch[2])), "linear") if linear else scheme_of(sch, "affine")
         qs, ss = [], []
         for k in range(count):
             q = random_codes(rng, m)
@@ -204,8 +205,9 @@ def test_packed_int16_fill_ragged_batches(ctx, align_type):
     """Pairs of different sizes share a thread's halves (masked form of the packed fill): every half must store and track
     only inside its own rectangle.  Includes empty sides, one-symbol sides, flagged symbols and an odd pair count."""
     rng = np.random.default_rng(4242)
-    for sch, hi, count in (((2, -1, 2, 1), 256, 401), ((1, -3, 5, 2), 128, 77), ((5, -4, 10, 1), 200, 150), ((2, -1, 2, 1), 190, 99)):
-        scheme = scheme_of(sch, "affine")
+    for sch, hi, count in (((2, -1, 2, 1), 256, 401), ((1, -3, 5, 2), 128, 77), ((5, -4, 10, 1), 200, 150), ((2, -1, 2, 1), 190, 99),
+                           ((2, -1, 1, 1), 256, 203), ((3, -2, 4, 4), 150, 64)):
+        scheme = scheme_of(sch, "linear" if sch[2] == sch[3] and sch[2] in (1, 4) else "affine")
         qs, ss = [], []
         for k in range(count):
             m = int(rng.integers(1, hi + 1)); n = int(rng.integers(1, hi + 1))
