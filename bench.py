@@ -100,6 +100,7 @@ class ClockSampler(threading.Thread):
         super().__init__(daemon=True)
         self.index, self.samples, self.reasons, self.max_mhz = index, [], set(), None
         self._stop_evt = threading.Event()
+        self._sampled = threading.Event()
 
     def run(self):
         try:
@@ -117,11 +118,14 @@ class ClockSampler(threading.Thread):
                 for bit, name in names.items():
                     if mask & bit:
                         self.reasons.add(name)
+                self._sampled.set()
                 time.sleep(0.02)
         except Exception as exc:  # no NVML: report nothing rather than guess
             self.reasons.add(f"nvml_unavailable:{type(exc).__name__}")
+            self._sampled.set()
 
     def stop(self):
+        self._sampled.wait(timeout=2)   # a timed region of a few hundred microseconds (cfg1) ends before NVML is up
         self._stop_evt.set()
         self.join(timeout=2)
         med = float(np.median(self.samples)) if self.samples else None
