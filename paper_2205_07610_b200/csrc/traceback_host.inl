@@ -160,12 +160,25 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
         }                                                                                          \
     } while (0)
 
+    // first traceback after creation with the upload still in flight: chunks end on upload-piece boundaries and each fill
+    // waits only for its own piece, so the fill of piece k runs while pieces k+1.. are still on the bus
+    const bool by_piece = b->upload_pending && b->n_pieces > 1;
+    int piece = 0;
     int64_t first = 0;
     while (first < np) {
         // grow the chunk until the code budget is reached
         code_off.clear();
         int64_t words = 0, count = 0;
-        while (first + count < np) {
+        if (by_piece) while (piece + 1 < b->n_pieces && b->piece_end[piece] <= first) ++piece;
+        const int64_t chunk_stop = by_piece ? std::max(b->piece_end[piece], first + 1) : np;
+        // equal-sized pairs: the code offsets are an arithmetic progression, generated on the device (no per-pair host loop)
+        const bool regular = b->uniform && max_m > 0 && max_n > 0 && !ragged16;
+        const int64_t w_each = regular ? tb_code_words(max_m, max_n, P, K) : 0;
+        if (regular) {
+            count = std::min(std::min(np, chunk_stop) - first, std::max<int64_t>(1, (int64_t)budget_words / std::max<int64_t>(w_each, 1)));
+            words = w_each * count;
+        }
+        while (!regular && first + count < std::min(np, chunk_stop)) {
             const int64_t p = first + count;
             const bool faulty = score_plan && score_plan->status[p] != 0;
             const int64_t w = (b->m[p] > 0 && b->n[p] > 0 && !faulty) ? tb_code_words(b->m[p], b->n[p], P, K) : 0;
@@ -200,7 +213,12 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
                 scan_tmp_bytes = need;
             }
         }
-        TB_TRY(cudaMemcpyAsync(d_code_off, code_off.data(), sizeof(int64_t) * (size_t)count, cudaMemcpyHostToDevice, ctx->stream));
+        if (regular) {
+            fill_progression_kernel<int64_t><<<(unsigned)((count + 255) / 256), 256, 0, ctx->stream>>>(d_code_off, (int64_t)0, w_each, count);
+            TB_TRY(cudaGetLastError());
+        } else {
+            TB_TRY(cudaMemcpyAsync(d_code_off, code_off.data(), sizeof(int64_t) * (size_t)count, cudaMemcpyHostToDevice, ctx->stream));
+        }
 
         TbParams prm;
         prm.q_codes = b->d_qcodes; prm.q_off = b->d_qoff; prm.q_len = b->d_qlen;
@@ -215,6 +233,7 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
         prm.n_runs = d_cnt; prm.run_off = d_chunk_off; prm.runs = nullptr;
         prm.tb_p = P; prm.tb_k = K; prm.one = 1; prm.run_tmp = d_run_tmp;
 
+        if (by_piece) TB_TRY(cudaStreamWaitEvent(ctx->stream, b->piece_ev[piece], 0));
         TB_TRY(cudaEventRecord(e0, ctx->stream));
         if (fill16) {
             const int64_t units = (count + 1) / 2;
@@ -260,6 +279,7 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
         tb.total_runs += chunk_runs;
         first += count;
     }
+    b->upload_pending = false;
     TB_TRY(cudaMemcpyAsync(tb.d_run_off + np, &tb.total_runs, sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
     TB_TRY(cudaStreamSynchronize(ctx->stream));
 #undef TB_TRY

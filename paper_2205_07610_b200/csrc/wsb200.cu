@@ -1082,7 +1082,9 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
     // first call after creation: the uploads may still be in flight on the copy stream
     const bool piecewise = b->upload_pending && b->n_pieces > 1 && b->n_pieces_usable != 1 && !plan_only && plan.groups.size() == 1 &&
                            plan.groups[0].unit_off < 0 && plan.groups[0].long_nw == 0;
-    if (b->upload_pending && !piecewise && b->n_pieces > 0)
+    // plan_only (traceback of global / semiglobal batches): the caller fills chunk by chunk and waits per upload piece itself
+    const bool defer_upload = plan_only && b->upload_pending && b->n_pieces > 1 && b->n_pieces_usable != 1;
+    if (b->upload_pending && !piecewise && !defer_upload && b->n_pieces > 0)
         CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, b->piece_ev[b->n_pieces - 1], 0));
 
     bool any_s16 = false;
@@ -1181,7 +1183,7 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
         CUDA_TRY(ctx, cudaGetLastError());
         ++launches;
     }
-    b->upload_pending = false;
+    if (!defer_upload) b->upload_pending = false;
     for (int a = 0; a < wsb_ctx::kAux; ++a)
         if (aux_used[a]) {
             CUDA_TRY(ctx, cudaEventRecord(ctx->aux_done[a], ctx->aux[a]));
