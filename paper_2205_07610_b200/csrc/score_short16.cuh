@@ -1,8 +1,8 @@
-// score_short16.cuh -- packed int16x2 (DPX) LOCAL scoring of short reads that fit one stage.
+// score_short16.cuh -- packed int16x2 (DPX) LOCAL scoring of short reads that fit one stage: the headline kernel.
 //
 // Same lane-group wavefront, two alignments per register and two rows per trip as score_short.cuh, but in 16-bit
-// integers with the DPX packed instructions instead of half2 arithmetic.  What that buys (measured with
-// tools/ubench: 8.5 cycles per packed cell against 10.7 for the half2 mix):
+// integers with the DPX packed instructions instead of half2 arithmetic (the reference's own packed mode is int16
+// halves, _kernels.py:553-858).  What that buys:
 //   * the substitution scores of BOTH alignments come from ONE byte permute: the two query symbols of a row are kept as
 //     two "row words" (sigma(q, s) for s = 0..3 in the four bytes), each column keeps a 16-bit PRMT selector built from
 //     its two subject symbols, and PRMT(rowA, rowB, sel[c]) is the packed pair {sigma_B, sigma_A}, sign-extended;
@@ -16,6 +16,25 @@
 //   * a 16-bit value range: max_step * (m + n) up to 32 000 instead of 2 048.
 // Reference semantics: merged affine update _kernels.py:259-276, linear :113-126, end-cell rule :130-145.
 //
+// Loop shape: ONE row per loop trip, lane t one row behind lane t - 1 (half the wavefront ramp of the two-rows-per-trip
+// half2 kernel: 157 instead of 164 row steps for 150 bp).  All per-column state is updated in place by the instruction
+// that produces it, so the trip carries no register copies: TA = T - alpha and TG = T - gamma are written by their
+// VIADD, and instead of an H row the strip keeps D[c] = H(row, c - 1) + sigma(next row's symbol, c), the diagonal
+// candidate of the NEXT row, written by the VIADD that follows the cell's VIMNMX3 (the PRMT takes the next row's row
+// words, which are fetched one trip ahead anyway).  Per trip of K = 19 columns: 19 PRMT + 58 VIADD + 46 VIMNMX3 + the
+// row hand-over (3 SHFL, 3 SEL) + the record (1 VIMNMX.S16x2 with predicates + 10 predicated STS.128) = 155 SASS
+// instructions = 8.2 per packed cell pair (the half2 kernel: 336 per two rows = 8.8, on a ramp twice as long).
+// End-cell snapshot: the record test is the packed maximum itself (VIMNMX.S16x2 returns max(best, rowmax) AND one
+// predicate per half, "best won"); a half whose maximum rose parks the strip's TA row -- whole 16-byte quads that never
+// move -- in shared memory.  T == S <=> H == S for the global maximum S as long as gamma >= 1 (T is max(H, a gap state
+// that lost at least gamma against an earlier T <= S)), so after the sweep the winner finds the first column with
+// TA == S - alpha; schemes with a zero-cost gap step take the half2 kernel.
+//
+// Unit pipeline: while a lane group sweeps unit u, the sequences of unit u + 1 travel from global to shared memory with
+// cp.async (16-byte chunks of the aligned windows around the four sequences); their metadata chain (unit list -> pair
+// -> offsets / lengths) advances one dependent load per quarter of the sweep, so no warp ever waits for global memory
+// between two units.
+//
 // Limits (the planner checks them, otherwise the half2 / int32 kernels run): |match|, |mismatch| <= 127, mismatch <= 0 <=
 // match, merged-exact scheme, and no flagged (non-ACGT) SUBJECT symbol -- a selector can only pick one of the four
 // row-word bytes, so a flagged subject symbol has no exact encoding.  The kernel detects such a symbol while loading
@@ -27,79 +46,77 @@
 
 namespace wsb {
 
-constexpr int kShort16QRows = 200;  // query rows per lane group (150 bp reads + 4P + 2 pad rows at P = 8)
+constexpr int kShort16QRows = 172;   // query rows per lane group (reads up to 154 bp + 2P + 2 pad rows at P = 8)
+constexpr int kShort16Raw = 192;     // bytes of one staged sequence window (16-byte aligned start, up to 177 symbols)
+constexpr int kShort16MaxLen = kShort16Raw - 15;
 
 template <int P, int K> constexpr size_t short16_smem_bytes() {
-    return (size_t)2 * (K / 4 + 1) * kThreads * 16 + (size_t)(kThreads / P) * kShort16QRows * 8;
+    return (size_t)2 * (K / 4 + 1) * kThreads * 16          // row snapshots, one area per packed half
+           + (size_t)(kThreads / P) * kShort16QRows * 8     // row words of the current unit
+           + (size_t)(kThreads / P) * 4 * kShort16Raw       // staged sequences of the next unit
+           + (size_t)(kThreads / P) * 16 * 4;               // metadata of the next unit
 }
 
 __device__ __forceinline__ unsigned pack16(int x) { return ((unsigned)x & 0xffffu) * 0x10001u; }
 __device__ __forceinline__ int half16(unsigned w, int v) { return (int)(short)(v ? (w >> 16) : (w & 0xffffu)); }
 
-// Record test + snapshot for both halves: a half records when the row maximum raised its running best
-// (nb = max(best, rm) differs from best in that half).  The strip's H row goes to that half's snapshot area in 16-byte
-// chunks (one chunk every kThreads * 16 = 2048 bytes); stores are predicated, a row without a record costs issue slots only.
-#define WSB_S16_PRED                                   \
-    "{\n\t.reg .pred p, q;\n\t.reg .b32 c, l;\n\t"     \
-    "xor.b32 c, %0, %1;\n\t"                           \
-    "and.b32 l, c, 0xffff;\n\t"                        \
-    "setp.ne.u32 p, l, 0;\n\t"                         \
-    "setp.gt.u32 q, c, 0xffff;\n\t"
-#define WSB_S16_ST(off, a, b, c_, d)                                                  \
-    "@p st.shared.v4.b32 [%2+" #off "], {%" #a ", %" #b ", %" #c_ ", %" #d "};\n\t"   \
-    "@q st.shared.v4.b32 [%3+" #off "], {%" #a ", %" #b ", %" #c_ ", %" #d "};\n\t"
+// nb = max(best, rm) per half; a half whose maximum rose (best lost) parks the strip's H row: 16-byte chunks, one chunk
+// every kThreads * 16 = 2048 bytes, in that half's snapshot area.  Stores are predicated, a row without a record costs
+// issue slots only.  ptxas folds max + unpack + setp into ONE VIMNMX.S16x2 with two predicate results.
+#define WSB_S16_HEAD                                                    \
+    "{\n\t.reg .pred p, q;\n\t.reg .s16 r0, r1, a0, a1;\n\t"            \
+    "max.s16x2 %0, %1, %2;\n\t"                                         \
+    "mov.b32 {r0, r1}, %0;\n\t"                                         \
+    "mov.b32 {a0, a1}, %1;\n\t"                                         \
+    "setp.eq.s16 p, r0, a0;\n\t"                                        \
+    "setp.eq.s16 q, r1, a1;\n\t"
+#define WSB_S16_ST(off, a, b, c_, d)                                                   \
+    "@!p st.shared.v4.b32 [%3+" #off "], {%" #a ", %" #b ", %" #c_ ", %" #d "};\n\t"   \
+    "@!q st.shared.v4.b32 [%4+" #off "], {%" #a ", %" #b ", %" #c_ ", %" #d "};\n\t"
 
-template <int NC>
-__device__ __forceinline__ void record16_chunks(const unsigned* w, unsigned nb, unsigned best, unsigned addr_p, unsigned addr_q) {
-    static_assert(NC >= 1 && NC <= 5, "chunk group size");
-    if constexpr (NC == 4) {
-        asm volatile(WSB_S16_PRED WSB_S16_ST(0, 4, 5, 6, 7) WSB_S16_ST(2048, 8, 9, 10, 11) WSB_S16_ST(4096, 12, 13, 14, 15)
-                     WSB_S16_ST(6144, 16, 17, 18, 19) "}\n"
-                     :
-                     : "r"(nb), "r"(best), "r"(addr_p), "r"(addr_q), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]),
+template <int NCH>
+__device__ __forceinline__ unsigned record16(const unsigned (&w)[NCH * 4], unsigned best, unsigned rm, unsigned addr_p,
+                                             unsigned addr_q) {
+    static_assert(NCH == 4 || NCH == 5, "instantiated strip widths: K = 12..19");
+    unsigned nb;
+    if constexpr (NCH == 4) {
+        asm volatile(WSB_S16_HEAD WSB_S16_ST(0, 5, 6, 7, 8) WSB_S16_ST(2048, 9, 10, 11, 12) WSB_S16_ST(4096, 13, 14, 15, 16)
+                     WSB_S16_ST(6144, 17, 18, 19, 20) "}\n"
+                     : "=&r"(nb)
+                     : "r"(best), "r"(rm), "r"(addr_p), "r"(addr_q), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]),
                        "r"(w[5]), "r"(w[6]), "r"(w[7]), "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]),
                        "r"(w[14]), "r"(w[15])
                      : "memory");
-    }
-    if constexpr (NC == 5) {
-        asm volatile(WSB_S16_PRED WSB_S16_ST(0, 4, 5, 6, 7) WSB_S16_ST(2048, 8, 9, 10, 11) WSB_S16_ST(4096, 12, 13, 14, 15)
-                     WSB_S16_ST(6144, 16, 17, 18, 19) WSB_S16_ST(8192, 20, 21, 22, 23) "}\n"
-                     :
-                     : "r"(nb), "r"(best), "r"(addr_p), "r"(addr_q), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]),
+    } else {
+        asm volatile(WSB_S16_HEAD WSB_S16_ST(0, 5, 6, 7, 8) WSB_S16_ST(2048, 9, 10, 11, 12) WSB_S16_ST(4096, 13, 14, 15, 16)
+                     WSB_S16_ST(6144, 17, 18, 19, 20) WSB_S16_ST(8192, 21, 22, 23, 24) "}\n"
+                     : "=&r"(nb)
+                     : "r"(best), "r"(rm), "r"(addr_p), "r"(addr_q), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]),
                        "r"(w[5]), "r"(w[6]), "r"(w[7]), "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]),
                        "r"(w[14]), "r"(w[15]), "r"(w[16]), "r"(w[17]), "r"(w[18]), "r"(w[19])
                      : "memory");
     }
-    static_assert(NC == 4 || NC == 5, "instantiated strip widths: K = 12..19");
+    return nb;
 }
 
-// H[] row plus the iteration tag in the first spare word after the K columns (the snapshot then also records WHEN)
-template <int K> __device__ __forceinline__ void record16_rows(const unsigned (&h)[K], unsigned nb, unsigned best,
-                                                               unsigned snap_addr, unsigned tag) {
-    constexpr int NCH = K / 4 + 1;
-    unsigned w[NCH * 4];
-#pragma unroll
-    for (int c = 0; c < NCH * 4; ++c) w[c] = c < K ? h[c] : tag;
-    constexpr unsigned HS = NCH * kThreads * 16;  // byte distance between the two halves' snapshot areas
-    record16_chunks<NCH>(w, nb, best, snap_addr, snap_addr + HS);
+__device__ __forceinline__ void cp_async16(unsigned dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
-
-template <int NCH> __device__ __forceinline__ void record16_quads(const uint4 (&hq)[NCH], unsigned nb, unsigned best,
-                                                                  unsigned snap_addr) {
-    unsigned w[NCH * 4];
-#pragma unroll
-    for (int k = 0; k < NCH; ++k) { w[4 * k] = hq[k].x; w[4 * k + 1] = hq[k].y; w[4 * k + 2] = hq[k].z; w[4 * k + 3] = hq[k].w; }
-    constexpr unsigned HS = NCH * kThreads * 16;
-    record16_chunks<NCH>(w, nb, best, snap_addr, snap_addr + HS);
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
 
 template <int P, int K, int GAP>
 __global__ void __launch_bounds__(kThreads, 4) s16_local_short_kernel(const ScoreParams prm) {
     constexpr int GPB = kThreads / P;
-    constexpr int NCH = K / 4 + 1;
+    constexpr int NCH = K / 4 + 1;   // always at least one spare word after the K columns: it takes the row tag
+    constexpr int NW = NCH * 4;
+    static_assert(P >= 4, "lanes 0..3 of a group carry the metadata of the four sequences of a unit");
     extern __shared__ uint4 smem_dyn[];
     uint4 (*snap)[NCH][kThreads] = reinterpret_cast<uint4 (*)[NCH][kThreads]>(smem_dyn);
     uint2 (*qbuf)[kShort16QRows] = reinterpret_cast<uint2 (*)[kShort16QRows]>(smem_dyn + 2 * NCH * kThreads);
+    uint8_t (*raw)[4][kShort16Raw] = reinterpret_cast<uint8_t (*)[4][kShort16Raw]>(&qbuf[GPB][0]);
+    int (*meta)[16] = reinterpret_cast<int (*)[16]>(&raw[GPB][0][0]);   // per group: pidx[2], len[4], shift[4]
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
@@ -109,76 +126,103 @@ __global__ void __launch_bounds__(kThreads, 4) s16_local_short_kernel(const Scor
     const int64_t group_global = (int64_t)blockIdx.x * GPB + gib;
     const int64_t n_groups = (int64_t)gridDim.x * GPB;
     const unsigned snap_addr = (unsigned)__cvta_generic_to_shared(&snap[0][0][tid]);
+    constexpr unsigned HS = NCH * kThreads * 16;  // byte distance between the two halves' snapshot areas
 
     const int gamma = GAP == GAP_MERGED ? min(prm.alpha, prm.beta) : prm.alpha;
     const unsigned c_nalpha = pack16(-prm.alpha);
     const unsigned c_ngamma = pack16(-gamma);
     const unsigned mism4 = (unsigned)(prm.mismatch & 0xff) * 0x01010101u;
-    const unsigned match1 = (unsigned)(prm.match & 0xff);
-    // lane 0 sees the matrix' zero left border instead of a neighbour: x * keep + edge (IMAD, FMA pipe)
+    const unsigned dm1 = (unsigned)((prm.match ^ prm.mismatch) & 0xff);
+    // lane 0 sees the matrix' zero left border instead of a neighbour: x * keep (IMAD, FMA pipe).  0 stands for every
+    // border value: H = 0 exactly, and T - alpha, T - gamma <= 0 never win against the local floor.
     const unsigned keep = t == 0 ? 0u : 1u;
-    const unsigned edge_ta = t == 0 ? c_nalpha : 0u;
-    const unsigned edge_tg = t == 0 ? c_ngamma : 0u;
     const int col0 = t * K;
 
+    // ---- metadata chain of a unit, one dependent load per step; lane v (< 4) follows sequence v: 0 = query of pair 0,
+    // 1 = subject of pair 0, 2 = query of pair 1, 3 = subject of pair 1
     const int64_t rounds = (prm.n_units + n_groups - 1) / n_groups;
+    const int sv = t & 3, pv = sv >> 1;
+    const bool is_subject = (sv & 1) != 0;
+    int mt_p = -1, mt_seq = 0, mt_len = 0;
+    const uint8_t* mt_ptr = nullptr;
+    auto meta_step = [&](int step, int64_t u) {
+        if (step == 0) {          // unit -> pair
+            mt_p = -1;
+            if (u < prm.n_units) {
+                if (prm.units) mt_p = prm.units[u * 2 + pv];
+                else { const int64_t pp = prm.pair_base + u * 2 + pv; mt_p = pp < prm.n_pairs ? (int)pp : -1; }
+            }
+        } else if (step == 1) {   // pair -> sequence
+            mt_seq = mt_p >= 0 ? (is_subject ? prm.pair_s[mt_p] : prm.pair_q[mt_p]) : 0;
+        } else if (step == 2) {   // sequence -> window
+            mt_len = 0; mt_ptr = is_subject ? prm.s_codes : prm.q_codes;
+            if (mt_p >= 0) {
+                mt_len = is_subject ? prm.s_len[mt_seq] : prm.q_len[mt_seq];
+                mt_ptr += is_subject ? prm.s_off[mt_seq] : prm.q_off[mt_seq];
+            }
+        } else {                  // window -> shared memory; the metadata the sweep needs goes to the group's slot
+            const unsigned shift = (unsigned)(reinterpret_cast<uintptr_t>(mt_ptr) & 15u);
+            if (t < 4) {
+                meta[gib][2 + sv] = mt_len;
+                meta[gib][6 + sv] = (int)shift;
+                if (!is_subject) meta[gib][pv] = mt_p;
+            }
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+                const uint8_t* base = reinterpret_cast<const uint8_t*>(
+                    __shfl_sync(gmask, (unsigned long long)(reinterpret_cast<uintptr_t>(mt_ptr) & ~(uintptr_t)15), s, P));
+                const int bytes = __shfl_sync(gmask, mt_len > 0 ? mt_len + (int)shift : 0, s, P);
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(&raw[gib][s][0]);
+                for (int x = t * 16; x < bytes; x += P * 16) cp_async16(dst + x, base + x);
+            }
+        }
+    };
+
+    // prologue: the first unit of this group goes through the whole chain at once
+    if (rounds > 0) {
+#pragma unroll
+        for (int step = 0; step < 4; ++step) meta_step(step, group_global);
+    }
+
     for (int64_t rd = 0; rd < rounds; ++rd) {
-        const int64_t u = rd * n_groups + group_global;
-        int pidx[2], m[2], n[2];
-        const uint8_t* qp[2];
-        const uint8_t* sp[2];
-        int mm = 0;
+        cp_async_wait_all();
+        __syncwarp();
+        int pidx[2], m[2], n[2], qsh[2], ssh[2];
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
-            int p = -1;
-            if (u < prm.n_units) {
-                if (prm.units) p = prm.units[u * 2 + v];
-                else { const int64_t pp = prm.pair_base + u * 2 + v; p = pp < prm.n_pairs ? (int)pp : -1; }
-            }
-            pidx[v] = p; m[v] = 0; n[v] = 0; qp[v] = nullptr; sp[v] = nullptr;
-            if (p >= 0) {
-                const int a = prm.pair_q[p], b = prm.pair_s[p];
-                m[v] = prm.q_len[a]; n[v] = prm.s_len[b];
-                qp[v] = prm.q_codes + prm.q_off[a];
-                sp[v] = prm.s_codes + prm.s_off[b];
-            }
-            mm = max(mm, m[v]);
+            pidx[v] = meta[gib][v];
+            m[v] = meta[gib][2 + 2 * v]; n[v] = meta[gib][3 + 2 * v];
+            qsh[v] = meta[gib][6 + 2 * v]; ssh[v] = meta[gib][7 + 2 * v];
         }
-        const int mm_w = __reduce_max_sync(0xffffffffu, mm);
-        if (mm_w == 0) continue;
+        const int mm_w = __reduce_max_sync(0xffffffffu, max(m[0], m[1]));
+        const int64_t u_next = (rd + 1) * n_groups + group_global;
+        if (mm_w == 0) {   // nothing to sweep in this warp: still keep the pipeline of the next unit going
+            __syncwarp();
+            if (rd + 1 < rounds) {
+#pragma unroll
+                for (int step = 0; step < 4; ++step) meta_step(step, u_next);
+            }
+            continue;
+        }
 
-        // query buffer: 2P pad rows, the rows of both queries as row words, then pad rows for the ramp-down.  Loads are
-        // issued in batches of 8 per lane before any is consumed.
-        __syncwarp();
+        // query buffer: P pad rows, the rows of both queries as row words, then pad rows for the ramp-down
         {
-            constexpr int UNR = 8;
-            const int total = mm_w + 4 * P + 2;
-            for (int x0 = t; x0 < total; x0 += P * UNR) {
-                int raw[UNR][2];
-#pragma unroll
-                for (int k = 0; k < UNR; ++k) {
-                    const int row = x0 + P * k - 2 * P;
-#pragma unroll
-                    for (int v = 0; v < 2; ++v) raw[k][v] = (row >= 0 && row < m[v]) ? (int)qp[v][row] : 4;
-                }
-#pragma unroll
-                for (int k = 0; k < UNR; ++k) {
-                    const int x = x0 + P * k;
-                    uint2 rw;   // sigma(q, s) for s = 0..3: match in the byte of the query symbol, mismatch elsewhere
-                    rw.x = raw[k][0] < 4 ? (mism4 & ~(0xffu << (8 * raw[k][0]))) | (match1 << (8 * raw[k][0])) : mism4;
-                    rw.y = raw[k][1] < 4 ? (mism4 & ~(0xffu << (8 * raw[k][1]))) | (match1 << (8 * raw[k][1])) : mism4;
-                    if (x < total) qbuf[gib][x] = rw;
-                }
+            const int total = mm_w + 2 * P + 2;
+            for (int x = t; x < total; x += P) {
+                const int row = x - P;
+                uint2 rw;   // sigma(q, s) for s = 0..3: match in the byte of the query symbol, mismatch elsewhere
+                unsigned c0 = 4, c1 = 4;
+                if (row >= 0 && row < m[0]) c0 = raw[gib][0][qsh[0] + row];
+                if (row >= 0 && row < m[1]) c1 = raw[gib][2][qsh[1] + row];
+                rw.x = c0 < 4 ? mism4 ^ (dm1 << (8 * c0)) : mism4;
+                rw.y = c1 < 4 ? mism4 ^ (dm1 << (8 * c1)) : mism4;
+                qbuf[gib][x] = rw;
             }
         }
-        // per column: PRMT selector of the two subject symbols, TA = T - alpha, TG = T - gamma, H
-        // H lives in uint4 quads (the snapshot stores are 16-byte stores; the spare word after column K-1 takes the tag)
-        unsigned sel[K], TA[K], TG[GAP == GAP_MERGED ? K : 1];
-        uint4 Hq[NCH];
-        auto Hc = [&](int c) -> unsigned& {
-            uint4& q4 = Hq[c >> 2];
-            return (c & 3) == 0 ? q4.x : (c & 3) == 1 ? q4.y : (c & 3) == 2 ? q4.z : q4.w;
-        };
+        // per column: PRMT selector of the two subject symbols, TA = T - alpha (whole quads: the snapshot source), TG = T - gamma,
+        // D = diagonal candidate of the NEXT row (H of the column to the left + sigma of the next row's symbol)
+        unsigned sel[K], TA[NW], TG[GAP == GAP_MERGED ? K : 1], D[K];
+        D[0] = 0u;
         bool flagged_subject = false;
 #pragma unroll
         for (int c = 0; c < K; ++c) {
@@ -186,17 +230,16 @@ __global__ void __launch_bounds__(kThreads, 4) s16_local_short_kernel(const Scor
 #pragma unroll
             for (int v = 0; v < 2; ++v)
                 if (col0 + c < n[v]) {
-                    const unsigned x = sp[v][col0 + c];
+                    const unsigned x = raw[gib][2 * v + 1][ssh[v] + col0 + c];
                     if (x < 4) nib[v] = (x + 4u * v) | ((x + 4u * v) | 8u) << 4;   // value byte, then its sign byte
                     else flagged_subject = true;
                 }
             sel[c] = nib[0] | (nib[1] << 8);
             TA[c] = c_nalpha;
             if (GAP == GAP_MERGED) TG[c] = c_ngamma;
-            Hc(c) = 0u;
         }
 #pragma unroll
-        for (int c = K; c < 4 * NCH; ++c) Hc(c) = 0u;
+        for (int c = K; c < NW; ++c) TA[c] = 0u;
         // a flagged subject symbol cannot be encoded: hand the pair(s) of this unit to the fallback list
         if (__any_sync(gmask, flagged_subject)) {
             if (t == 0) {
@@ -205,26 +248,32 @@ __global__ void __launch_bounds__(kThreads, 4) s16_local_short_kernel(const Scor
                     if (pidx[v] >= 0) { const int at = atomicAdd(prm.redo_count, 1); prm.redo[at] = pidx[v]; }
             }
         }
-        __syncwarp();
+        __syncwarp();   // raw[] and meta[] of this unit are consumed, qbuf is complete
+        {   // candidates of the first row this lane sweeps: H of the row above it is zero
+            const uint2 rw = qbuf[gib][P - t];
+#pragma unroll
+            for (int c = 1; c < K; ++c) asm("prmt.b32 %0, %1, %2, %3;" : "=r"(D[c]) : "r"(rw.x), "r"(rw.y), "r"(sel[c]));
+        }
 
-        unsigned ta_lA = c_nalpha, tg_lA = c_ngamma, h_lA = 0u;   // left border of row A: T - alpha, T - gamma, H
-        unsigned ta_lB = c_nalpha, tg_lB = c_ngamma, h_lB = 0u;   // ... of row B
-        unsigned h_dA = 0u;                                       // H(rA - 1, left column): diagonal of row A, cell 0
+        unsigned ta_l = 0u, tg_l = 0u;     // left border of the coming row: T - alpha, T - gamma
+        unsigned h_l = 0u, h_d = 0u;       // H of the left column in the coming row's row / in the row above it (diagonal)
         unsigned bestvec = 0u;
         const unsigned qbase = (unsigned)__cvta_generic_to_shared(&qbuf[gib][0]);
-        unsigned qaddr = qbase + 8u * (unsigned)(2 * P - 2 * t);    // row r lives at qbuf index r - 1 + 2P
-        const unsigned qend = qaddr + 16u * (unsigned)((mm_w + 1) / 2 + P - 1);
+        unsigned qaddr = qbase + 8u * (unsigned)(P - t);    // row r lives at qbuf index r - 1 + P; lane t runs t rows behind lane 0
 
-        // one row of the strip, in place: H[] holds the previous row on entry and this row on exit
-        auto row = [&](unsigned rwA, unsigned rwB, unsigned h_diag, unsigned& la, unsigned& lg, unsigned& rm) {
+        // one row of the strip.  rw0/rw1: row words of this row (cell 0's candidate), nw0/nw1: of the next row
+        auto row = [&](unsigned rw0, unsigned rw1, unsigned nw0, unsigned nw1, unsigned h_diag, unsigned& la, unsigned& lg,
+                       unsigned& rm, unsigned& h_last) {
             rm = 0u;
-            unsigned hd = h_diag, hprev = 0u;
+            unsigned hprev = 0u;
 #pragma unroll
             for (int c = 0; c < K; ++c) {
-                unsigned sg;
-                asm("prmt.b32 %0, %1, %2, %3;" : "=r"(sg) : "r"(rwA), "r"(rwB), "r"(sel[c]));
-                const unsigned d = __vadd2(hd, sg);
-                hd = Hc(c);
+                unsigned d;
+                if (c == 0) {
+                    unsigned sg;
+                    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(sg) : "r"(rw0), "r"(rw1), "r"(sel[0]));
+                    d = __vadd2(h_diag, sg);
+                } else d = D[c];
                 const unsigned h = __vimax3_s16x2_relu(TA[c], la, d);
                 if (GAP == GAP_MERGED) {
                     const unsigned tn = __vimax3_s16x2_relu(TG[c], lg, d);
@@ -235,48 +284,47 @@ __global__ void __launch_bounds__(kThreads, 4) s16_local_short_kernel(const Scor
                     la = __vadd2(h, c_nalpha);
                 }
                 TA[c] = la;
-                Hc(c) = h;
+                if (c >= 1) {   // this column's candidate for the NEXT row, in place: its old value was consumed just above
+                    unsigned sg;
+                    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(sg) : "r"(nw0), "r"(nw1), "r"(sel[c]));
+                    D[c] = __vadd2(hprev, sg);
+                }
                 if (c & 1) rm = __vimax3_s16x2(rm, hprev, h);
                 else if (c == K - 1) rm = __vmaxs2(rm, h);
                 hprev = h;
             }
+            h_last = hprev;
         };
-        unsigned qa0, qa1, qb0, qb1;  // row words of rows A and B, fetched one trip ahead of their use
-        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(qa0), "=r"(qa1), "=r"(qb0), "=r"(qb1) : "r"(qaddr) : "memory");
+        auto hand_over = [&](unsigned la, unsigned lg, unsigned h_last) {
+            const unsigned s0 = __shfl_up_sync(0xffffffffu, la, 1, P);
+            const unsigned s1 = __shfl_up_sync(0xffffffffu, h_last, 1, P);
+            h_d = h_l;
+            ta_l = s0 * keep;
+            h_l = s1 * keep;
+            if (GAP == GAP_MERGED) tg_l = __shfl_up_sync(0xffffffffu, lg, 1, P) * keep;
+        };
+
+        unsigned qn0, qn1, qc0, qc1;  // row words of the coming row and the one after it
+        asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(qc0), "=r"(qc1) : "r"(qaddr) : "memory");
+        asm volatile("ld.shared.v2.b32 {%0, %1}, [%2+8];" : "=r"(qn0), "=r"(qn1) : "r"(qaddr) : "memory");
+        int done = 0;
+        const int steps = mm_w + P - 1;
+        const int quarter1 = (steps + 3) / 4;
 #pragma unroll 1
-        while (qaddr != qend) {
-            const unsigned a0 = qa0, a1 = qa1, b0 = qb0, b1 = qb1;
-            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4+16];" : "=r"(qa0), "=r"(qa1), "=r"(qb0), "=r"(qb1) : "r"(qaddr) : "memory");
-            unsigned laA = ta_lA, lgA = tg_lA, laB = ta_lB, lgB = tg_lB, rmA, rmB;
-            row(a0, a1, h_dA, laA, lgA, rmA);
-            unsigned nb = __vmaxs2(bestvec, rmA);
-            Hc(K) = qaddr;
-            record16_quads<NCH>(Hq, nb, bestvec, snap_addr);
-            bestvec = nb;
-            const unsigned hA_last = Hc(K - 1);
-            row(b0, b1, h_lA, laB, lgB, rmB);
-            h_dA = h_lB;
-            const unsigned s0 = __shfl_up_sync(0xffffffffu, laA, 1, P);
-            const unsigned s1 = __shfl_up_sync(0xffffffffu, hA_last, 1, P);
-            const unsigned s2 = __shfl_up_sync(0xffffffffu, laB, 1, P);
-            const unsigned s3 = __shfl_up_sync(0xffffffffu, Hc(K - 1), 1, P);
-            unsigned s4 = 0u, s5 = 0u;
-            if (GAP == GAP_MERGED) {
-                s4 = __shfl_up_sync(0xffffffffu, lgA, 1, P);
-                s5 = __shfl_up_sync(0xffffffffu, lgB, 1, P);
-            }
-            nb = __vmaxs2(bestvec, rmB);
-            Hc(K) = qaddr + 8;
-            record16_quads<NCH>(Hq, nb, bestvec, snap_addr);
-            bestvec = nb;
-            qaddr += 16;
-            ta_lA = s0 * keep + edge_ta;
-            h_lA = s1 * keep;
-            ta_lB = s2 * keep + edge_ta;
-            h_lB = s3 * keep;
-            if (GAP == GAP_MERGED) {
-                tg_lA = s4 * keep + edge_tg;
-                tg_lB = s5 * keep + edge_tg;
+        for (int part = 0; part < 4; ++part) {
+            if (rd + 1 < rounds) meta_step(part, u_next);
+            const unsigned qstop = qaddr + 8u * (unsigned)max(0, min(quarter1, steps - done));
+            done += quarter1;
+#pragma unroll 1
+            while (qaddr != qstop) {
+                unsigned la = ta_l, lg = tg_l, rm, h_last;
+                row(qc0, qc1, qn0, qn1, h_d, la, lg, rm, h_last);
+                qc0 = qn0; qc1 = qn1;
+                asm volatile("ld.shared.v2.b32 {%0, %1}, [%2+16];" : "=r"(qn0), "=r"(qn1) : "r"(qaddr) : "memory");
+                TA[K] = qaddr;
+                bestvec = record16<NCH>(TA, bestvec, rm, snap_addr, snap_addr + HS);
+                hand_over(la, lg, h_last);
+                qaddr += 8;
             }
         }
 
@@ -288,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 4) s16_local_short_kernel(const Scor
             if (bv > 0) {  // the tag word after the K columns holds the query-buffer address of the record row
                 const uint4 w = snap[v][K / 4][tid];
                 const unsigned tag = (K % 4 == 0) ? w.x : (K % 4 == 1) ? w.y : (K % 4 == 2) ? w.z : w.w;
-                bi = (int)((tag - qbase) >> 3) - 2 * P + 1;  // buffer index -> matrix row
+                bi = (int)((tag - qbase) >> 3) - P + 1;  // buffer index -> matrix row
                 if (bi > m[v] || bi < 1) bv = 0;       // cannot happen for a real record; keeps pads out defensively
             }
 #pragma unroll
@@ -306,10 +354,10 @@ __global__ void __launch_bounds__(kThreads, 4) s16_local_short_kernel(const Scor
 #pragma unroll
                     for (int ch = (K - 1) / 4; ch >= 0; --ch) {
                         const uint4 w = snap[v][ch][tid];
-                        if (4 * ch + 3 < K && half16(w.w, v) == bv) pos = 4 * ch + 3;
-                        if (4 * ch + 2 < K && half16(w.z, v) == bv) pos = 4 * ch + 2;
-                        if (4 * ch + 1 < K && half16(w.y, v) == bv) pos = 4 * ch + 1;
-                        if (half16(w.x, v) == bv) pos = 4 * ch;
+                        if (4 * ch + 3 < K && half16(w.w, v) == bv - prm.alpha) pos = 4 * ch + 3;
+                        if (4 * ch + 2 < K && half16(w.z, v) == bv - prm.alpha) pos = 4 * ch + 2;
+                        if (4 * ch + 1 < K && half16(w.y, v) == bv - prm.alpha) pos = 4 * ch + 1;
+                        if (half16(w.x, v) == bv - prm.alpha) pos = 4 * ch;
                     }
                     j = bj + pos + 1;
                 } else { bi = 0; }

@@ -481,8 +481,8 @@ static int batch_create_impl(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t
         return e == cudaErrorMemoryAllocation ? WSB_E_NOMEM : WSB_E_CUDA;
     };
     cudaError_t e;
-    if ((e = ctx->alloc((void**)&b->d_qcodes, (size_t)std::max<int64_t>(q_total, 1))) != cudaSuccess) return fail(e);
-    if ((e = ctx->alloc((void**)&b->d_scodes, (size_t)std::max<int64_t>(s_total, 1))) != cudaSuccess) return fail(e);
+    if ((e = ctx->alloc((void**)&b->d_qcodes, (size_t)std::max<int64_t>(q_total, 1) + 64)) != cudaSuccess) return fail(e);
+    if ((e = ctx->alloc((void**)&b->d_scodes, (size_t)std::max<int64_t>(s_total, 1) + 64)) != cudaSuccess) return fail(e);
     // pool slices, address-ordered; a packed pool goes up as packed bytes into a staging area and is expanded per slice
     uint8_t *stage_q = nullptr, *stage_s = nullptr;
     int64_t *dflags_q = nullptr, *dflags_s = nullptr;
@@ -753,8 +753,9 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
     const int ms = max_step(sch);
     const int beta_eff_plan = affine ? sch->gap_extend : sch->gap_open;
     const bool wide_scheme = std::abs(sch->match - sch->mismatch) > 127;
+    // (the snapshot of the packed int16 kernel holds T - alpha: it needs every gap step to cost something)
     const bool s16_ok = want_s16 && atype == AT_LOCAL && f16_scheme_ok && std::abs(sch->match) <= 127 &&
-                        std::abs(sch->mismatch) <= 127;
+                        std::abs(sch->mismatch) <= 127 && sch->gap_open >= 1 && (!affine || sch->gap_extend >= 1);
     plan.status.assign((size_t)np, 0);
 
     if (variant == WSB_VARIANT_F16X2 && !merged_ok) return WSB_E_SCHEME;
@@ -765,7 +766,7 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
         if ((int64_t)ms * ((int64_t)m + n) >= (1ll << 29)) { status = WSB_E_LENGTH; return; }
         const bool fits = f16_scheme_ok && wsb_f16_range_ok(sch, m, n);
         if (variant == WSB_VARIANT_F16X2 && !fits) { status = WSB_E_RANGE; return; }
-        if (variant == WSB_VARIANT_AUTO && fits && s16_ok && n <= 152 && m <= kShort16QRows - 4 * 8 - 2) {
+        if (variant == WSB_VARIANT_AUTO && fits && s16_ok && n <= 152 && m <= kShort16QRows - 2 * 8 - 2) {
             var = WSB_VARIANT_S16X2; shape = n <= 128 ? 0 : 1;   // packed int16 DPX kernel: same pairs as the half2 short kernel
         } else if (variant != WSB_VARIANT_I32 && fits) { var = WSB_VARIANT_F16X2; shape = best_shape(kShapesF16, kNumShapesF16, 5, m, n); }
         else { var = WSB_VARIANT_I32; shape = wide_scheme ? 0 : best_shape(kShapesI32, kNumShapesI32, 4, m, n); }
