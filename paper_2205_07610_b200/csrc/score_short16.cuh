@@ -25,10 +25,10 @@
 // row hand-over (3 SHFL, 3 SEL) + the record (1 VIMNMX.S16x2 with predicates + 10 predicated STS.128) = 155 SASS
 // instructions = 8.2 per packed cell pair (the half2 kernel: 336 per two rows = 8.8, on a ramp twice as long).
 // End-cell snapshot: the record test is the packed maximum itself (VIMNMX.S16x2 returns max(best, rowmax) AND one
-// predicate per half, "best won"); a half whose maximum rose parks the strip's TA row -- whole 16-byte quads that never
+// predicate per half, "best won"); a half whose maximum rose parks the strip's T - gamma row -- whole 16-byte quads that never
 // move -- in shared memory.  T == S <=> H == S for the global maximum S as long as gamma >= 1 (T is max(H, a gap state
 // that lost at least gamma against an earlier T <= S)), so after the sweep the winner finds the first column with
-// TA == S - alpha; schemes with a zero-cost gap step take the half2 kernel.
+// T - gamma == S - gamma; schemes with a zero-cost gap step take the half2 kernel.
 //
 // Unit pipeline: while a lane group sweeps unit u, the sequences of unit u + 1 travel from global to shared memory with
 // cp.async (16-byte chunks of the aligned windows around the four sequences); their metadata chain (unit list -> pair
@@ -46,13 +46,14 @@
 
 namespace wsb {
 
-constexpr int kShort16QRows = 172;   // query rows per lane group (reads up to 154 bp + 2P + 2 pad rows at P = 8)
+constexpr int kShort16MaxM = 154;    // longest query the kernel takes
+template <int P> __host__ __device__ constexpr int short16_qrows() { return (kShort16MaxM + 2 * P + 2 + 1) / 2 * 2; }   // + P pad rows above, P + 2 below
 constexpr int kShort16Raw = 192;     // bytes of one staged sequence window (16-byte aligned start, up to 177 symbols)
 constexpr int kShort16MaxLen = kShort16Raw - 15;
 
 template <int P, int K> constexpr size_t short16_smem_bytes() {
     return (size_t)2 * (K / 4 + 1) * kThreads * 16          // row snapshots, one area per packed half
-           + (size_t)(kThreads / P) * kShort16QRows * 8     // row words of the current unit
+           + (size_t)(kThreads / P) * short16_qrows<P>() * 8     // row words of the current unit
            + (size_t)(kThreads / P) * 4 * kShort16Raw       // staged sequences of the next unit
            + (size_t)(kThreads / P) * 16 * 4;               // metadata of the next unit
 }
@@ -77,8 +78,15 @@ __device__ __forceinline__ int half16(unsigned w, int v) { return (int)(short)(v
 template <int NCH>
 __device__ __forceinline__ unsigned record16(const unsigned (&w)[NCH * 4], unsigned best, unsigned rm, unsigned addr_p,
                                              unsigned addr_q) {
-    static_assert(NCH == 4 || NCH == 5, "instantiated strip widths: K = 12..19");
+    static_assert(NCH >= 3 && NCH <= 5, "instantiated strip widths: K = 8..19");
     unsigned nb;
+    if constexpr (NCH == 3) {
+        asm volatile(WSB_S16_HEAD WSB_S16_ST(0, 5, 6, 7, 8) WSB_S16_ST(2048, 9, 10, 11, 12) WSB_S16_ST(4096, 13, 14, 15, 16) "}\n"
+                     : "=&r"(nb)
+                     : "r"(best), "r"(rm), "r"(addr_p), "r"(addr_q), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]),
+                       "r"(w[5]), "r"(w[6]), "r"(w[7]), "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11])
+                     : "memory");
+    }
     if constexpr (NCH == 4) {
         asm volatile(WSB_S16_HEAD WSB_S16_ST(0, 5, 6, 7, 8) WSB_S16_ST(2048, 9, 10, 11, 12) WSB_S16_ST(4096, 13, 14, 15, 16)
                      WSB_S16_ST(6144, 17, 18, 19, 20) "}\n"
@@ -87,7 +95,8 @@ __device__ __forceinline__ unsigned record16(const unsigned (&w)[NCH * 4], unsig
                        "r"(w[5]), "r"(w[6]), "r"(w[7]), "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]),
                        "r"(w[14]), "r"(w[15])
                      : "memory");
-    } else {
+    }
+    if constexpr (NCH == 5) {
         asm volatile(WSB_S16_HEAD WSB_S16_ST(0, 5, 6, 7, 8) WSB_S16_ST(2048, 9, 10, 11, 12) WSB_S16_ST(4096, 13, 14, 15, 16)
                      WSB_S16_ST(6144, 17, 18, 19, 20) WSB_S16_ST(8192, 21, 22, 23, 24) "}\n"
                      : "=&r"(nb)
@@ -106,15 +115,19 @@ __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
 
-template <int P, int K, int GAP>
-__global__ void __launch_bounds__(kThreads, 4) s16_local_short_kernel(const ScoreParams prm) {
+// AIMM / GIMM > 0: gap costs alpha / gamma baked into the instruction stream as immediates (the host picks such an
+// instantiation when the scheme matches): a VIADD.16x2 with an immediate reads one register instead of two, which the
+// cell-stream microbenchmark (tools/ubench/cell_bench.cu) shows is worth ~6 % of issue rate at four warps per scheduler.
+template <int P, int K, int GAP, int MINB = 4, int AIMM = 0, int GIMM = 0>
+__global__ void __launch_bounds__(kThreads, MINB) s16_local_short_kernel(const ScoreParams prm) {
     constexpr int GPB = kThreads / P;
     constexpr int NCH = K / 4 + 1;   // always at least one spare word after the K columns: it takes the row tag
     constexpr int NW = NCH * 4;
     static_assert(P >= 4, "lanes 0..3 of a group carry the metadata of the four sequences of a unit");
     extern __shared__ uint4 smem_dyn[];
     uint4 (*snap)[NCH][kThreads] = reinterpret_cast<uint4 (*)[NCH][kThreads]>(smem_dyn);
-    uint2 (*qbuf)[kShort16QRows] = reinterpret_cast<uint2 (*)[kShort16QRows]>(smem_dyn + 2 * NCH * kThreads);
+    constexpr int QROWS = short16_qrows<P>();
+    uint2 (*qbuf)[QROWS] = reinterpret_cast<uint2 (*)[QROWS]>(smem_dyn + 2 * NCH * kThreads);
     uint8_t (*raw)[4][kShort16Raw] = reinterpret_cast<uint8_t (*)[4][kShort16Raw]>(&qbuf[GPB][0]);
     int (*meta)[16] = reinterpret_cast<int (*)[16]>(&raw[GPB][0][0]);   // per group: pidx[2], len[4], shift[4]
 
@@ -128,9 +141,9 @@ __global__ void __launch_bounds__(kThreads, 4) s16_local_short_kernel(const Scor
     const unsigned snap_addr = (unsigned)__cvta_generic_to_shared(&snap[0][0][tid]);
     constexpr unsigned HS = NCH * kThreads * 16;  // byte distance between the two halves' snapshot areas
 
-    const int gamma = GAP == GAP_MERGED ? min(prm.alpha, prm.beta) : prm.alpha;
-    const unsigned c_nalpha = pack16(-prm.alpha);
-    const unsigned c_ngamma = pack16(-gamma);
+    const int gamma = GIMM > 0 ? GIMM : (GAP == GAP_MERGED ? min(prm.alpha, prm.beta) : prm.alpha);
+    const unsigned c_nalpha = AIMM > 0 ? ((unsigned)(-AIMM) & 0xffffu) * 0x10001u : pack16(-prm.alpha);
+    const unsigned c_ngamma = GIMM > 0 ? ((unsigned)(-GIMM) & 0xffffu) * 0x10001u : pack16(-gamma);
     const unsigned mism4 = (unsigned)(prm.mismatch & 0xff) * 0x01010101u;
     const unsigned dm1 = (unsigned)((prm.match ^ prm.mismatch) & 0xff);
     // lane 0 sees the matrix' zero left border instead of a neighbour: x * keep (IMAD, FMA pipe).  0 stands for every
@@ -205,23 +218,31 @@ __global__ void __launch_bounds__(kThreads, 4) s16_local_short_kernel(const Scor
             continue;
         }
 
-        // query buffer: P pad rows, the rows of both queries as row words, then pad rows for the ramp-down
+        // query buffer: P pad rows, the rows of both queries as row words, then pad rows for the ramp-down.  The byte
+        // loads of four rows are in flight before the first is used.
         {
+            constexpr int UNR = 4;
             const int total = mm_w + 2 * P + 2;
-            for (int x = t; x < total; x += P) {
-                const int row = x - P;
-                uint2 rw;   // sigma(q, s) for s = 0..3: match in the byte of the query symbol, mismatch elsewhere
-                unsigned c0 = 4, c1 = 4;
-                if (row >= 0 && row < m[0]) c0 = raw[gib][0][qsh[0] + row];
-                if (row >= 0 && row < m[1]) c1 = raw[gib][2][qsh[1] + row];
-                rw.x = c0 < 4 ? mism4 ^ (dm1 << (8 * c0)) : mism4;
-                rw.y = c1 < 4 ? mism4 ^ (dm1 << (8 * c1)) : mism4;
-                qbuf[gib][x] = rw;
+            for (int x0 = t; x0 < total; x0 += P * UNR) {
+                unsigned c0[UNR], c1[UNR];
+#pragma unroll
+                for (int k = 0; k < UNR; ++k) {
+                    const int row = x0 + P * k - P;
+                    c0[k] = (row >= 0 && row < m[0]) ? raw[gib][0][qsh[0] + row] : 4u;
+                    c1[k] = (row >= 0 && row < m[1]) ? raw[gib][2][qsh[1] + row] : 4u;
+                }
+#pragma unroll
+                for (int k = 0; k < UNR; ++k) {
+                    uint2 rw;   // sigma(q, s) for s = 0..3: match in the byte of the query symbol, mismatch elsewhere
+                    rw.x = c0[k] < 4 ? mism4 ^ (dm1 << (8 * c0[k])) : mism4;
+                    rw.y = c1[k] < 4 ? mism4 ^ (dm1 << (8 * c1[k])) : mism4;
+                    if (x0 + P * k < total) qbuf[gib][x0 + P * k] = rw;
+                }
             }
         }
         // per column: PRMT selector of the two subject symbols, TA = T - alpha (whole quads: the snapshot source), TG = T - gamma,
         // D = diagonal candidate of the NEXT row (H of the column to the left + sigma of the next row's symbol)
-        unsigned sel[K], TA[NW], TG[GAP == GAP_MERGED ? K : 1], D[K];
+        unsigned sel[K], TA[GAP == GAP_MERGED ? K : NW], TG[GAP == GAP_MERGED ? NW : 1], D[K];   // the snapshot source holds whole quads
         D[0] = 0u;
         bool flagged_subject = false;
 #pragma unroll
@@ -239,7 +260,7 @@ __global__ void __launch_bounds__(kThreads, 4) s16_local_short_kernel(const Scor
             if (GAP == GAP_MERGED) TG[c] = c_ngamma;
         }
 #pragma unroll
-        for (int c = K; c < NW; ++c) TA[c] = 0u;
+        for (int c = K; c < NW; ++c) { if (GAP == GAP_MERGED) TG[c] = 0u; else TA[c] = 0u; }
         // a flagged subject symbol cannot be encoded: hand the pair(s) of this unit to the fallback list
         if (__any_sync(gmask, flagged_subject)) {
             if (t == 0) {
@@ -295,13 +316,24 @@ __global__ void __launch_bounds__(kThreads, 4) s16_local_short_kernel(const Scor
             }
             h_last = hprev;
         };
-        auto hand_over = [&](unsigned la, unsigned lg, unsigned h_last) {
-            const unsigned s0 = __shfl_up_sync(0xffffffffu, la, 1, P);
-            const unsigned s1 = __shfl_up_sync(0xffffffffu, h_last, 1, P);
+        // The right border leaves for the next lane right after the row's last cell (send) and is taken over at the top
+        // of the NEXT trip (receive): the loop branch keeps the two apart, so the record stores, the row-word loads and the
+        // loop bookkeeping run under the shuffle latency instead of behind it.
+        unsigned s_la = 0u, s_h = 0u, s_lg = 0u;
+        auto send = [&](unsigned la, unsigned lg, unsigned h_last) {
+#ifdef WSB_ABLATE_SHFL     // timing experiment only (wrong results): the lane feeds itself
+            s_la = la; s_h = h_last; s_lg = lg;
+#else
+            s_la = __shfl_up_sync(0xffffffffu, la, 1, P);
+            if (GAP == GAP_MERGED) s_lg = __shfl_up_sync(0xffffffffu, lg, 1, P);
+            s_h = __shfl_up_sync(0xffffffffu, h_last, 1, P);
+#endif
+        };
+        auto receive = [&]() {
             h_d = h_l;
-            ta_l = s0 * keep;
-            h_l = s1 * keep;
-            if (GAP == GAP_MERGED) tg_l = __shfl_up_sync(0xffffffffu, lg, 1, P) * keep;
+            ta_l = s_la * keep;
+            if (GAP == GAP_MERGED) tg_l = s_lg * keep;
+            h_l = s_h * keep;
         };
 
         unsigned qn0, qn1, qc0, qc1;  // row words of the coming row and the one after it
@@ -317,13 +349,20 @@ __global__ void __launch_bounds__(kThreads, 4) s16_local_short_kernel(const Scor
             done += quarter1;
 #pragma unroll 1
             while (qaddr != qstop) {
+                receive();
                 unsigned la = ta_l, lg = tg_l, rm, h_last;
                 row(qc0, qc1, qn0, qn1, h_d, la, lg, rm, h_last);
-                qc0 = qn0; qc1 = qn1;
+                asm volatile("ld.shared.v2.b32 {%0, %1}, [%2+8];" : "=r"(qc0), "=r"(qc1) : "r"(qaddr) : "memory");
                 asm volatile("ld.shared.v2.b32 {%0, %1}, [%2+16];" : "=r"(qn0), "=r"(qn1) : "r"(qaddr) : "memory");
-                TA[K] = qaddr;
-                bestvec = record16<NCH>(TA, bestvec, rm, snap_addr, snap_addr + HS);
-                hand_over(la, lg, h_last);
+                // the row that just finished: T - gamma of the strip (linear gaps: h - alpha, the same thing) plus the row tag
+                if constexpr (GAP == GAP_MERGED) {
+                    TG[K] = qaddr;
+                    bestvec = record16<NCH>(TG, bestvec, rm, snap_addr, snap_addr + HS);
+                } else {
+                    TA[K] = qaddr;
+                    bestvec = record16<NCH>(TA, bestvec, rm, snap_addr, snap_addr + HS);
+                }
+                send(la, lg, h_last);
                 qaddr += 8;
             }
         }
@@ -354,10 +393,10 @@ __global__ void __launch_bounds__(kThreads, 4) s16_local_short_kernel(const Scor
 #pragma unroll
                     for (int ch = (K - 1) / 4; ch >= 0; --ch) {
                         const uint4 w = snap[v][ch][tid];
-                        if (4 * ch + 3 < K && half16(w.w, v) == bv - prm.alpha) pos = 4 * ch + 3;
-                        if (4 * ch + 2 < K && half16(w.z, v) == bv - prm.alpha) pos = 4 * ch + 2;
-                        if (4 * ch + 1 < K && half16(w.y, v) == bv - prm.alpha) pos = 4 * ch + 1;
-                        if (half16(w.x, v) == bv - prm.alpha) pos = 4 * ch;
+                        if (4 * ch + 3 < K && half16(w.w, v) == bv - gamma) pos = 4 * ch + 3;
+                        if (4 * ch + 2 < K && half16(w.z, v) == bv - gamma) pos = 4 * ch + 2;
+                        if (4 * ch + 1 < K && half16(w.y, v) == bv - gamma) pos = 4 * ch + 1;
+                        if (half16(w.x, v) == bv - gamma) pos = 4 * ch;
                     }
                     j = bj + pos + 1;
                 } else { bi = 0; }

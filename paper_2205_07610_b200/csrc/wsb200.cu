@@ -688,9 +688,15 @@ static LongFn pick_long(int atype, int gap, bool cluster) {
     return nullptr;
 }
 
-template <int P, int K> static KernelSel pick_short16(int gap) {
-    if (gap == GAP_LINEAR) return {s16_local_short_kernel<P, K, GAP_LINEAR>, short16_smem_bytes<P, K>()};
-    return {s16_local_short_kernel<P, K, GAP_MERGED>, short16_smem_bytes<P, K>()};
+// alpha / gamma = min(alpha, beta): the schemes of the reference's benchmarks (affine 2/1, linear 1) get instantiations
+// with the gap costs as immediates
+template <int P, int K, int MINB = 4> static KernelSel pick_short16(int gap, int alpha, int gamma) {
+    if (gap == GAP_LINEAR) {
+        if (alpha == 1) return {s16_local_short_kernel<P, K, GAP_LINEAR, MINB, 1, 1>, short16_smem_bytes<P, K>()};
+        return {s16_local_short_kernel<P, K, GAP_LINEAR, MINB>, short16_smem_bytes<P, K>()};
+    }
+    if (alpha == 2 && gamma == 1) return {s16_local_short_kernel<P, K, GAP_MERGED, MINB, 2, 1>, short16_smem_bytes<P, K>()};
+    return {s16_local_short_kernel<P, K, GAP_MERGED, MINB>, short16_smem_bytes<P, K>()};
 }
 
 template <int GAP> static LongFn pick_long16_atype(int atype) {
@@ -707,9 +713,12 @@ static LongFn pick_long16(int atype, int gap) {
 }
 
 // short_ok: every unit of the launch fits one stage and the short kernel's query buffer
-static KernelSel pick_kernel(int variant, int shape, int atype, int gap, bool masked, bool short_ok, bool wide) {
+static KernelSel pick_kernel(int variant, int shape, int atype, int gap, bool masked, bool short_ok, bool wide,
+                             int alpha = 0, int gamma = 0) {
     static const char* no_short = getenv("WSB_NO_SHORT");  // tuning aid: force the general kernel
-    if (variant == WSB_VARIANT_S16X2) return shape == 0 ? pick_short16<8, 16>(gap) : pick_short16<8, 19>(gap);
+    if (variant == WSB_VARIANT_S16X2) {
+        return shape == 0 ? pick_short16<8, 16>(gap, alpha, gamma) : pick_short16<8, 19>(gap, alpha, gamma);
+    }
     if (variant == WSB_VARIANT_F16X2 && atype == AT_LOCAL && short_ok && !(no_short && no_short[0])) {
         switch (shape) {
             case 0: return pick_short<4, 16>(gap);
@@ -766,8 +775,10 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
         if ((int64_t)ms * ((int64_t)m + n) >= (1ll << 29)) { status = WSB_E_LENGTH; return; }
         const bool fits = f16_scheme_ok && wsb_f16_range_ok(sch, m, n);
         if (variant == WSB_VARIANT_F16X2 && !fits) { status = WSB_E_RANGE; return; }
-        if (variant == WSB_VARIANT_AUTO && fits && s16_ok && n <= 152 && m <= kShort16QRows - 2 * 8 - 2) {
-            var = WSB_VARIANT_S16X2; shape = n <= 128 ? 0 : 1;   // packed int16 DPX kernel: same pairs as the half2 short kernel
+        if (variant == WSB_VARIANT_AUTO && fits && s16_ok && n <= 152 && m <= kShort16MaxM) {
+            var = WSB_VARIANT_S16X2; shape = n <= 128 ? 0 : 1;
+            static const char* s16_shape = getenv("WSB_S16_SHAPE");   // tuning aid: lane-group shape / occupancy of the packed int16 kernel
+            if (s16_shape && s16_shape[0]) shape = std::min(1, std::max(0, atoi(s16_shape)));   // packed int16 DPX kernel: same pairs as the half2 short kernel
         } else if (variant != WSB_VARIANT_I32 && fits) { var = WSB_VARIANT_F16X2; shape = best_shape(kShapesF16, kNumShapesF16, 5, m, n); }
         else { var = WSB_VARIANT_I32; shape = wide_scheme ? 0 : best_shape(kShapesI32, kNumShapesI32, 4, m, n); }
     };
@@ -1047,7 +1058,8 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
         const Shape sh = shape_of(g.variant, g.shape);
         const bool short_ok = g.max_n <= sh.P * sh.K && g.max_m <= kShortQRows - 4 * sh.P - 2;
         const KernelSel sel = pick_kernel(g.variant, g.shape, atype, g.gap, sch->mismatch > 0 || sch->match < 0, short_ok,
-                                          std::abs(sch->match - sch->mismatch) > 127);
+                                          std::abs(sch->match - sch->mismatch) > 127, sch->gap_open,
+                                          affine ? std::min(sch->gap_open, sch->gap_extend) : sch->gap_open);
         KernelFn fn = sel.fn;
         if (!fn) return WSB_E_SCHEME;
         CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel.smem));
