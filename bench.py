@@ -31,7 +31,7 @@ WORKLOADS = {
     # BASELINE.json configs.  i_cell = the reference's instrumented score ops per cell; width = cells per
     # thread instruction of the dominant kernel (2 = packed half2, 1 = int32).
     "cfg1": dict(pairs=10_000, length=150, align_type="global", gap_model="linear", scheme=(2, -1, 1, 1), i_cell=5, variant="auto"),
-    "cfg2": dict(pairs=4_000_000, length=150, align_type="local", gap_model="affine", scheme=(2, -1, 2, 1), i_cell=8, variant="f16x2"),
+    "cfg2": dict(pairs=4_000_000, length=150, align_type="local", gap_model="affine", scheme=(2, -1, 2, 1), i_cell=8, variant="auto"),
     "cfg2_i32": dict(pairs=1_000_000, length=150, align_type="local", gap_model="affine", scheme=(2, -1, 2, 1), i_cell=8,
                      variant="i32"),
     "cfg3": dict(pairs=1_000_000, length=250, align_type="semiglobal", gap_model="affine", scheme=(2, -1, 2, 1), i_cell=8,
@@ -347,7 +347,7 @@ def main():
     # cfg3: the direction-code fill of a uniform batch runs packed int16 (two alignments per thread) unless switched off
     tb16 = args.workload == "cfg3" and not os.environ.get("WSB_TB_NO16")
     width = 1 if (variant == "i32" or args.workload == "cfg5" or (args.workload == "cfg3" and not tb16)) else 2
-    dtype = "i32" if width == 1 else ("s16x2" if args.workload in ("cfg3", "cfg4") else "f16x2")
+    dtype = "i32" if width == 1 else ("f16x2" if variant == "f16x2" or args.workload == "cfg1" else "s16x2")
     peak = n_sm * 128 * f_ghz * width / cfg["i_cell"]
     per_gpu = value / world
     traffic = None

@@ -119,8 +119,9 @@ def score_batch(q_codes, q_off, q_len, s_codes, s_off, s_len, pair_q, pair_s, al
 
 
 def traceback_batch(q_codes, q_off, q_len, s_codes, s_off, s_len, pair_q, pair_s, align_type: str, affine: bool,
-                    match: int, mismatch: int, alpha: int, beta: int, threads: int = 0):
-    """Batched ref_traceback; returns dict of int32 arrays plus a list of per-pair op lists."""
+                    match: int, mismatch: int, alpha: int, beta: int, threads: int = 0, unpack: bool = True):
+    """Batched ref_traceback; returns dict of int32 arrays plus a list of per-pair op lists (unpack=False: only the
+    packed run words `ops_packed[n, stride]` with `n_ops[n]`, for array-wise comparison of large batches)."""
     lib = _load()
     q_codes, s_codes = _u8(q_codes), _u8(s_codes)
     q_off = np.ascontiguousarray(q_off, np.int64); s_off = np.ascontiguousarray(s_off, np.int64)
@@ -139,7 +140,8 @@ def traceback_batch(q_codes, q_off, q_len, s_codes, s_off, s_len, pair_q, pair_s
                                        _ptr(outs["s_end"]), _ptr(ops), stride, _ptr(n_ops), threads)
     if rc:
         raise RuntimeError(f"oracle traceback batch failed rc={rc}")
-    outs["ops"] = [unpack_ops(ops[i, :n_ops[i]]) for i in range(n)]
+    if unpack:
+        outs["ops"] = [unpack_ops(ops[i, :n_ops[i]]) for i in range(n)]
     outs["ops_packed"] = ops
     outs["n_ops"] = n_ops
     return outs

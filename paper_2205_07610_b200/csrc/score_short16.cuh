@@ -147,8 +147,8 @@ __global__ void __launch_bounds__(kThreads, MINB) s16_local_short_kernel(const S
     const unsigned mism4 = (unsigned)(prm.mismatch & 0xff) * 0x01010101u;
     const unsigned dm1 = (unsigned)((prm.match ^ prm.mismatch) & 0xff);
     // lane 0 sees the matrix' zero left border instead of a neighbour: x * keep (IMAD, FMA pipe).  0 stands for every
-    // border value: H = 0 exactly, and T - alpha, T - gamma <= 0 never win against the local floor.
-    const unsigned keep = t == 0 ? 0u : 1u;
+    // border value: H = 0 exactly, and T = 0 gives T - alpha, T - gamma <= 0, which never win against the local floor.
+    const unsigned keep = t == 0 ? 0u : (unsigned)prm.one;   // prm.one == 1, opaque: keeps the selects multiplies (FMA pipe)
     const int col0 = t * K;
 
     // ---- metadata chain of a unit, one dependent load per step; lane v (< 4) follows sequence v: 0 = query of pair 0,
@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(kThreads, MINB) s16_local_short_kernel(const S
 
         // one row of the strip.  rw0/rw1: row words of this row (cell 0's candidate), nw0/nw1: of the next row
         auto row = [&](unsigned rw0, unsigned rw1, unsigned nw0, unsigned nw1, unsigned h_diag, unsigned& la, unsigned& lg,
-                       unsigned& rm, unsigned& h_last) {
+                       unsigned& rm, unsigned& h_last, unsigned& t_last) {
             rm = 0u;
             unsigned hprev = 0u;
 #pragma unroll
@@ -298,11 +298,13 @@ __global__ void __launch_bounds__(kThreads, MINB) s16_local_short_kernel(const S
                 const unsigned h = __vimax3_s16x2_relu(TA[c], la, d);
                 if (GAP == GAP_MERGED) {
                     const unsigned tn = __vimax3_s16x2_relu(TG[c], lg, d);
+                    if (c == K - 1) t_last = tn;
                     la = __vadd2(tn, c_nalpha);
                     lg = __vadd2(tn, c_ngamma);
                     TG[c] = lg;
                 } else {
                     la = __vadd2(h, c_nalpha);
+                    if (c == K - 1) t_last = h;
                 }
                 TA[c] = la;
                 if (c >= 1) {   // this column's candidate for the NEXT row, in place: its old value was consumed just above
@@ -319,20 +321,20 @@ __global__ void __launch_bounds__(kThreads, MINB) s16_local_short_kernel(const S
         // The right border leaves for the next lane right after the row's last cell (send) and is taken over at the top
         // of the NEXT trip (receive): the loop branch keeps the two apart, so the record stores, the row-word loads and the
         // loop bookkeeping run under the shuffle latency instead of behind it.
-        unsigned s_la = 0u, s_h = 0u, s_lg = 0u;
-        auto send = [&](unsigned la, unsigned lg, unsigned h_last) {
+        unsigned s_t = 0u, s_h = 0u;
+        auto send = [&](unsigned t_last, unsigned h_last) {
 #ifdef WSB_ABLATE_SHFL     // timing experiment only (wrong results): the lane feeds itself
-            s_la = la; s_h = h_last; s_lg = lg;
+            s_t = t_last; s_h = h_last;
 #else
-            s_la = __shfl_up_sync(0xffffffffu, la, 1, P);
-            if (GAP == GAP_MERGED) s_lg = __shfl_up_sync(0xffffffffu, lg, 1, P);
+            s_t = __shfl_up_sync(0xffffffffu, t_last, 1, P);
             s_h = __shfl_up_sync(0xffffffffu, h_last, 1, P);
 #endif
         };
-        auto receive = [&]() {
+        auto receive = [&]() {   // two multiplies and two packed adds on the FMA pipe; the ALU pipe is the busy one
             h_d = h_l;
-            ta_l = s_la * keep;
-            if (GAP == GAP_MERGED) tg_l = s_lg * keep;
+            const unsigned t_in = s_t * keep;
+            ta_l = __vadd2(t_in, c_nalpha);
+            if (GAP == GAP_MERGED) tg_l = __vadd2(t_in, c_ngamma);
             h_l = s_h * keep;
         };
 
@@ -350,8 +352,8 @@ __global__ void __launch_bounds__(kThreads, MINB) s16_local_short_kernel(const S
 #pragma unroll 1
             while (qaddr != qstop) {
                 receive();
-                unsigned la = ta_l, lg = tg_l, rm, h_last;
-                row(qc0, qc1, qn0, qn1, h_d, la, lg, rm, h_last);
+                unsigned la = ta_l, lg = tg_l, rm, h_last, t_last;
+                row(qc0, qc1, qn0, qn1, h_d, la, lg, rm, h_last, t_last);
                 asm volatile("ld.shared.v2.b32 {%0, %1}, [%2+8];" : "=r"(qc0), "=r"(qc1) : "r"(qaddr) : "memory");
                 asm volatile("ld.shared.v2.b32 {%0, %1}, [%2+16];" : "=r"(qn0), "=r"(qn1) : "r"(qaddr) : "memory");
                 // the row that just finished: T - gamma of the strip (linear gaps: h - alpha, the same thing) plus the row tag
@@ -362,7 +364,7 @@ __global__ void __launch_bounds__(kThreads, MINB) s16_local_short_kernel(const S
                     TA[K] = qaddr;
                     bestvec = record16<NCH>(TA, bestvec, rm, snap_addr, snap_addr + HS);
                 }
-                send(la, lg, h_last);
+                send(t_last, h_last);
                 qaddr += 8;
             }
         }

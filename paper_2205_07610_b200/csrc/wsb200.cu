@@ -997,8 +997,11 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
     int rc = check_scheme(sch, atype);
     if (rc) return rc;
     if (variant < WSB_VARIANT_AUTO || variant > WSB_VARIANT_S16X2) return WSB_E_ARG;
-    const bool want_s16 = variant == WSB_VARIANT_S16X2;   // opt-in: routed like AUTO, short local pairs take the packed int16 kernel
-    if (want_s16) variant = WSB_VARIANT_AUTO;
+    // S16X2 is routed like AUTO; both give short local pairs to the packed int16 kernel (WSB_NO_S16: tuning aid, AUTO then
+    // keeps the half2 short kernel)
+    static const char* no_s16 = getenv("WSB_NO_S16");
+    const bool want_s16 = variant == WSB_VARIANT_S16X2 || (variant == WSB_VARIANT_AUTO && !(no_s16 && no_s16[0]));
+    if (variant == WSB_VARIANT_S16X2) variant = WSB_VARIANT_AUTO;
     wsb_ctx* ctx = b->ctx;
     CUDA_TRY(ctx, cudaSetDevice(ctx->device));
     const bool affine = sch->gap_model == WSB_GAP_AFFINE;

@@ -120,6 +120,96 @@ void run(const char* name, int nsm, unsigned* out, unsigned* in, long long* cyc)
     if (e != cudaSuccess) printf("CUDA error %s\n", cudaGetErrorString(e));
 }
 
+
+// ---- the loop of score_short16.cuh rebuilt element by element (FEAT bits): 1 = row words from shared memory (2 LDS.64
+// per row), 2 = record (VIMNMX with predicates + 10 predicated STS.128 of the T - gamma quads), 4 = hand-over (3 SHFL.UP
+// + 3 SEL into the next row), 8 = record predicates true about a quarter of the time (else almost never)
+template <int FEAT>
+__global__ void __launch_bounds__(128, 4) loop_kernel(unsigned* out, const unsigned* in, long long* cyc) {
+    constexpr int K = 19, NW = 20;
+    extern __shared__ uint4 sm4[];
+    uint2* qb = reinterpret_cast<uint2*>(sm4 + 10 * 128);
+    unsigned sel[K], TA[K], TG[NW], D[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) { sel[c] = in[c] ^ threadIdx.x; TA[c] = in[32 + c]; TG[c] = in[64 + c]; D[c] = in[96 + c]; }
+    TG[K] = 0u;
+    for (int x = threadIdx.x; x < 16 * 172; x += 128) qb[x] = make_uint2(in[x & 127] * 3u, in[(x + 7) & 127]);
+    __syncthreads();
+    const int t = threadIdx.x & 7, gib = threadIdx.x >> 3;
+    const unsigned keep = t == 0 ? 0u : 1u;
+    unsigned qaddr = (unsigned)__cvta_generic_to_shared(qb + gib * 172 + (8 - t));
+    const unsigned snap = (unsigned)__cvta_generic_to_shared(sm4 + threadIdx.x);
+    unsigned rw0 = in[128] + threadIdx.x, rw1 = in[129], nw0 = in[130], nw1 = in[131];
+    unsigned ta_l = in[132], tg_l = in[133], hd = in[134], hl = 0u, best = 0u, s_la = 0u, s_lg = 0u, s_h = 0u;
+    const unsigned c_na = 0xfffefffeu, c_ng = 0xffffffffu;
+    long long t0 = clock64();
+#pragma unroll 1
+    for (int r = 0; r < ROWS; ++r) {
+        if (FEAT & 4) { hd = hl; ta_l = s_la * keep; tg_l = s_lg * keep; hl = s_h * keep; }
+        unsigned la = ta_l, lg = tg_l, rm = 0u, hprev = 0u;
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+            const unsigned d = c == 0 ? __vadd2(hd, prmt(rw0, rw1, sel[0])) : D[c];
+            const unsigned h = __vimax3_s16x2_relu(TA[c], la, d);
+            const unsigned tn = __vimax3_s16x2_relu(TG[c], lg, d);
+            la = __vadd2(tn, c_na); lg = __vadd2(tn, c_ng);
+            TG[c] = lg; TA[c] = la;
+            if (c >= 1) D[c] = __vadd2(hprev, prmt(nw0, nw1, sel[c]));
+            if (c & 1) rm = __vimax3_s16x2(rm, hprev, h);
+            else if (c == K - 1) rm = __vmaxs2(rm, h);
+            hprev = h;
+        }
+        if (FEAT & 1) {
+            const unsigned qa = qaddr + 8u * (unsigned)(r & 127);
+            asm volatile("ld.shared.v2.b32 {%0, %1}, [%2+8];" : "=r"(rw0), "=r"(rw1) : "r"(qa) : "memory");
+            asm volatile("ld.shared.v2.b32 {%0, %1}, [%2+16];" : "=r"(nw0), "=r"(nw1) : "r"(qa) : "memory");
+        } else { const unsigned x = rw0; rw0 = nw0; nw0 = rw1; rw1 = nw1; nw1 = x; }
+        if (FEAT & 2) {
+            TG[K] = qaddr;
+            if ((FEAT & 8) && (r & 3) == 0) best = 0u;   // records become frequent
+            unsigned nb;
+            asm volatile("{\n\t.reg .pred p, q;\n\t.reg .s16 r0, r1, a0, a1;\n\t"
+                "max.s16x2 %0, %1, %2;\n\tmov.b32 {r0, r1}, %0;\n\tmov.b32 {a0, a1}, %1;\n\t"
+                "setp.eq.s16 p, r0, a0;\n\tsetp.eq.s16 q, r1, a1;\n\t"
+                "@!p st.shared.v4.b32 [%3+0], {%4, %5, %6, %7};\n\t@!q st.shared.v4.b32 [%3+10240], {%4, %5, %6, %7};\n\t"
+                "@!p st.shared.v4.b32 [%3+2048], {%8, %9, %10, %11};\n\t@!q st.shared.v4.b32 [%3+12288], {%8, %9, %10, %11};\n\t"
+                "@!p st.shared.v4.b32 [%3+4096], {%12, %13, %14, %15};\n\t@!q st.shared.v4.b32 [%3+14336], {%12, %13, %14, %15};\n\t"
+                "@!p st.shared.v4.b32 [%3+6144], {%16, %17, %18, %19};\n\t@!q st.shared.v4.b32 [%3+16384], {%16, %17, %18, %19};\n\t"
+                "@!p st.shared.v4.b32 [%3+8192], {%20, %21, %22, %23};\n\t@!q st.shared.v4.b32 [%3+18432], {%20, %21, %22, %23};\n\t}"
+                : "=&r"(nb) : "r"(best), "r"(rm), "r"(snap), "r"(TG[0]), "r"(TG[1]), "r"(TG[2]), "r"(TG[3]), "r"(TG[4]), "r"(TG[5]),
+                  "r"(TG[6]), "r"(TG[7]), "r"(TG[8]), "r"(TG[9]), "r"(TG[10]), "r"(TG[11]), "r"(TG[12]), "r"(TG[13]), "r"(TG[14]),
+                  "r"(TG[15]), "r"(TG[16]), "r"(TG[17]), "r"(TG[18]), "r"(TG[19]) : "memory");
+            best = nb;
+        } else best = __vmaxs2(best, rm);
+        if (FEAT & 4) {
+            s_la = __shfl_up_sync(0xffffffffu, la, 1, 8);
+            s_lg = __shfl_up_sync(0xffffffffu, lg, 1, 8);
+            s_h = __shfl_up_sync(0xffffffffu, hprev, 1, 8);
+        } else { ta_l = la; tg_l = lg; hd = hprev; }
+    }
+    long long t1 = clock64();
+    unsigned acc = best ^ ta_l ^ tg_l ^ hd ^ hl;
+#pragma unroll
+    for (int c = 0; c < K; ++c) acc ^= TA[c] ^ TG[c] ^ D[c];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+    if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+template <int FEAT> void run_loop(const char* name, int nsm, unsigned* out, unsigned* in, long long* cyc) {
+    const int smem = 20 * 128 * 16 + 16 * 172 * 8;
+    cudaFuncSetAttribute(loop_kernel<FEAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (int wps = 1; wps <= 4; ++wps) {
+        loop_kernel<FEAT><<<nsm * wps, 128, smem>>>(out, in, cyc); cudaDeviceSynchronize();
+        loop_kernel<FEAT><<<nsm * wps, 128, smem>>>(out, in, cyc); cudaDeviceSynchronize();
+        std::vector<long long> h(nsm * wps);
+        cudaMemcpy(h.data(), cyc, h.size() * 8, cudaMemcpyDeviceToHost);
+        double avg = 0; for (auto c : h) avg += c; avg /= h.size();
+        printf("loop %-46s wps=%d: %7.1f cycles per row per warp, %6.1f scheduler cycles per warp-row\n", name, wps, avg / ROWS, avg / ROWS / wps);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) printf("CUDA error %s\n", cudaGetErrorString(e));
+}
+
 int main() {
     cudaDeviceProp p; cudaGetDeviceProperties(&p, 0);
     const int nsm = p.multiProcessorCount;
@@ -135,5 +225,12 @@ int main() {
     run<4, 19>("2-input max only (4 ALU per cell)", nsm, out, in, cyc);
     run<1, 10>("constants as immediates", nsm, out, in, cyc);
     run<1, 8>("constants as immediates", nsm, out, in, cyc);
+    run_loop<0>("cells only", nsm, out, in, cyc);
+    run_loop<1>("+ row words from shared memory", nsm, out, in, cyc);
+    run_loop<3>("+ record, predicates almost never true", nsm, out, in, cyc);
+    run_loop<11>("+ record, predicates often true", nsm, out, in, cyc);
+    run_loop<5>("+ hand-over (no record)", nsm, out, in, cyc);
+    run_loop<7>("+ record (rare) + hand-over", nsm, out, in, cyc);
+    run_loop<15>("+ record (often) + hand-over", nsm, out, in, cyc);
     return 0;
 }
