@@ -24,7 +24,7 @@ EXPORTED_SYMBOLS = (
     "wsb_ctx_sm_count", "wsb_batch_create", "wsb_batch_create_async", "wsb_batch_create_packed_async", "wsb_batch_create_uniform_async", "wsb_batch_destroy", "wsb_batch_score", "wsb_batch_fetch_scores",
     "wsb_batch_traceback", "wsb_batch_fetch_traceback", "wsb_batch_total_cells", "wsb_score_batch",
     "wsb_traceback_batch", "wsb_merged_state_exact", "wsb_f16_range_ok", "wsb_plan_shards", "wsb_batch_has_faults", "wsb_pinned_alloc",
-    "wsb_pinned_free", "wsb_batch_total_runs", "wsb_batch_h2d_bytes",
+    "wsb_pinned_free", "wsb_batch_total_runs", "wsb_batch_h2d_bytes", "wsb_compact_pool",
 )
 
 
@@ -153,6 +153,21 @@ def plan_shards(q_len, s_len, pair_q, pair_s, n_shards: int):
     if rc:
         raise status_exception(rc)
     return shard_of, cells
+
+
+def compact_pool(codes, off, lengths, ids):
+    """(codes, off) of the pool made of sequences `ids` only, in that order (wsb_compact_pool; host memory, no GPU)."""
+    codes = np.ascontiguousarray(codes, np.uint8); off = np.ascontiguousarray(off, np.int64)
+    lengths = np.ascontiguousarray(lengths, np.int32); ids = np.ascontiguousarray(ids, np.int64)
+    total = int(lengths[ids].astype(np.int64).sum()) if len(ids) else 0
+    out_codes = np.empty(max(total, 1), np.uint8)
+    out_off = np.zeros(len(ids), np.int64)
+    lib = load()
+    lib.wsb_compact_pool.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
+    rc = lib.wsb_compact_pool(_ptr(codes), _ptr(off), _ptr(lengths), _ptr(ids), len(ids), _ptr(out_codes), _ptr(out_off))
+    if rc:
+        raise status_exception(rc)
+    return out_codes, out_off
 
 
 class Context:

@@ -214,6 +214,32 @@ def _run_shard(device: int, queries: SequencePool, subjects: SequencePool, pair_
         out["error"] = exc
 
 
+def _run_sliced_shard(device: int, queries: SequencePool, subjects: SequencePool, pair_q: np.ndarray, pair_s: np.ndarray,
+                      idx: np.ndarray, regular: bool, cfg: AlignConfig, scheme: ScoringScheme, variant: str, out: dict):
+    """One GPU's share of a multi-GPU job: the pools are cut down to what the shard's pairs reference before anything is
+    uploaded (a contiguous block of a reads matrix is a zero-copy slice; an arbitrary pair list is gathered into compact
+    pools with remapped indices; a shard that references most of a pool anyway takes it whole)."""
+    try:
+        if regular:
+            lo, hi = int(idx[0]), int(idx[-1]) + 1
+            q_sub, s_sub = queries.slice_uniform(lo, hi), subjects.slice_uniform(lo, hi)
+            ident = np.arange(hi - lo, dtype=np.int32)
+            return _run_shard(device, q_sub, s_sub, ident, ident, cfg, scheme, variant, out, True)
+        pq, ps = pair_q[idx], pair_s[idx]
+
+        def cut(pool, col):
+            used, inv = np.unique(col, return_inverse=True)
+            if len(used) * 4 > len(pool) * 3:
+                return pool, col
+            return pool.subset(used), inv.astype(np.int32)
+        q_sub, pq = cut(queries, pq)
+        s_sub, ps = cut(subjects, ps)
+        _run_shard(device, q_sub, s_sub, np.ascontiguousarray(pq, np.int32), np.ascontiguousarray(ps, np.int32), cfg, scheme,
+                   variant, out, False)
+    except BaseException as exc:
+        out["error"] = exc
+
+
 def run_batch(job: BatchJob) -> BatchReport:
     """Align every pair of the job on the GPU(s); results keep the pairs' order.
 
@@ -237,9 +263,15 @@ def run_batch(job: BatchJob) -> BatchReport:
         return lens["m"], lens["n"]
 
     t0 = time.perf_counter()
+    regular = (job._identity and queries.uniform_len is not None and subjects.uniform_len is not None and
+               n <= len(queries) and n <= len(subjects))
     if len(devices) == 1:
         shard_index = [np.arange(n) if cfg.result_mode == "traceback" else range(n)]
         shard_cells = []
+    elif regular:   # a reads matrix: contiguous blocks (whole packed units, whole 2-bit bytes), no planner pass
+        cuts = [min(n, (n * k // len(devices) + 2047) // 2048 * 2048) for k in range(len(devices))] + [n]
+        shard_index = [np.arange(cuts[k], cuts[k + 1]) for k in range(len(devices))]
+        shard_cells = [int(len(ix)) * queries.uniform_len * subjects.uniform_len for ix in shard_index]
     else:
         shard_of, sc = N.plan_shards(queries.len, subjects.len, pair_q, pair_s, len(devices))
         shard_index = [np.nonzero(shard_of == k)[0] for k in range(len(devices))]
@@ -250,12 +282,10 @@ def run_batch(job: BatchJob) -> BatchReport:
         if len(idx) == 0:
             continue
         if len(devices) == 1:  # no thread hop for the common single-GPU case
-            regular = (job._identity and queries.uniform_len is not None and subjects.uniform_len is not None and
-                       n <= len(queries) and n <= len(subjects))
             _run_shard(dev, queries, subjects, pair_q, pair_s, cfg, job.scheme, variant, out, regular)
             continue
-        th = threading.Thread(target=_run_shard, name=f"waveseq-gpu-{dev}",
-                              args=(dev, queries, subjects, pair_q[idx], pair_s[idx], cfg, job.scheme, variant, out))
+        th = threading.Thread(target=_run_sliced_shard, name=f"waveseq-gpu-{dev}",
+                              args=(dev, queries, subjects, pair_q, pair_s, idx, regular, cfg, job.scheme, variant, out))
         threads.append(th)
         th.start()
     for th in threads:
@@ -298,11 +328,10 @@ def run_batch(job: BatchJob) -> BatchReport:
             if len(idx) == 0:
                 continue
             tb = out["tb"]
-            if len(devices) == 1:
-                runs[:] = tb["cigar"]
-            else:
-                for k, p in enumerate(idx):
-                    runs[run_off[p]:run_off[p + 1]] = tb["cigar"][tb["cigar_off"][k]:tb["cigar_off"][k + 1]]
+            # shard run k of pair idx[j] goes to run_off[idx[j]] + (k - shard offset of that pair): one fancy-index store
+            src_off = tb["cigar_off"]
+            shift = np.repeat(run_off[idx] - src_off[:-1], np.diff(src_off))
+            runs[shift + np.arange(len(shift), dtype=np.int64)] = tb["cigar"][:len(shift)]
     else:
         for idx, out in zip(shard_index, outs):
             if len(idx) == 0:

@@ -60,6 +60,7 @@ template <int PASS> static void tb_launch_walk(int atype, const TbParams& prm, c
 
 extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atype, float* kernel_ms, int32_t* n_launches) {
     if (!b) return WSB_E_ARG;
+    std::lock_guard<std::recursive_mutex> lock_(b->ctx->mu);
     int rc = check_scheme(sch, atype);
     if (rc) return rc;
     wsb_ctx* ctx = b->ctx;
@@ -298,6 +299,7 @@ extern "C" int wsb_batch_fetch_traceback(wsb_batch* b, int32_t* out_score, int32
     if (!b || !out_score || !q_start || !q_end || !s_start || !s_end || !cigar_off) return WSB_E_ARG;
     if (!b->tb.valid) return WSB_E_ARG;
     wsb_ctx* ctx = b->ctx;
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     CUDA_TRY(ctx, cudaSetDevice(ctx->device));
     const int64_t np = b->n_pairs;
     const size_t bytes = sizeof(int32_t) * (size_t)np;
@@ -325,6 +327,8 @@ extern "C" int wsb_traceback_batch(wsb_ctx* ctx, const wsb_scheme* scheme, int a
                                    const int32_t* pair_s, int64_t n_pairs, int32_t* out_score, int32_t* q_start,
                                    int32_t* q_end, int32_t* s_start, int32_t* s_end, uint32_t* cigar, int64_t cigar_cap,
                                    int64_t* cigar_off, int32_t* status) {
+    if (!ctx) return WSB_E_ARG;
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     wsb_batch* b = nullptr;
     int rc = wsb_batch_create(ctx, q_codes, q_off, q_len, n_q, s_codes, s_off, s_len, n_s, pair_q, pair_s, n_pairs, &b);
     if (rc) return rc;

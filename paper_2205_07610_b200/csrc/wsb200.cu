@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <new>
 #include <numeric>
 #include <string>
@@ -40,6 +41,10 @@ struct wsb_ctx {
     unsigned int* d_queues = nullptr;  // work-queue heads of the long-read launches
     int32_t* d_cflags = nullptr;       // cluster launches of the long-read kernel: 160 ints per cluster
     std::string last_error;
+    // One context serves every host thread that aligns on its GPU (the reference runs independent alignments
+    // concurrently, batch.py:213-240): each entry point that touches the context's streams, events, queues or block
+    // cache holds this lock for its whole duration.  Recursive: the one-shot calls nest the batch calls.
+    std::recursive_mutex mu;
     // Device-memory cache: batches come and go with every run_batch call, and cudaMalloc/cudaFree of GB-sized pools
     // cost tens of milliseconds each, so freed blocks are kept (size-bucketed, 2 MiB granularity) and reused.
     std::multimap<size_t, void*> free_blocks;
@@ -218,6 +223,32 @@ extern "C" int wsb_plan_shards(const int32_t* q_len, const int32_t* s_len, const
 }
 
 // ------------------------------------------------------------------------------------------------ context
+// Gather sequences ids[0 .. n_ids) of a pool into a compact pool (host only): the per-GPU shards of run_batch upload
+// only the sequences their pairs reference ("sliced to the referenced subset"; the reference's workers share
+// one read-only copy, batch.py:213-240).
+extern "C" int wsb_compact_pool(const uint8_t* codes, const int64_t* off, const int32_t* len, const int64_t* ids,
+                                int64_t n_ids, uint8_t* out_codes, int64_t* out_off) {
+    if (!codes || !off || !len || !ids || !out_off || n_ids < 0) return WSB_E_ARG;
+    int64_t at = 0;
+    for (int64_t k = 0; k < n_ids; ++k) {
+        if (ids[k] < 0 || len[ids[k]] < 0) return WSB_E_ARG;
+        out_off[k] = at; at += len[ids[k]];
+    }
+    if (at > 0 && !out_codes) return WSB_E_ARG;
+    const int nthr = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<unsigned>(8u, std::max(1u, std::thread::hardware_concurrency())), at / (4 << 20) + 1));
+    auto work = [&](int t) {
+        for (int64_t k = n_ids * t / nthr, hi = n_ids * (t + 1) / nthr; k < hi; ++k)
+            std::memcpy(out_codes + out_off[k], codes + off[ids[k]], (size_t)len[ids[k]]);
+    };
+    if (nthr == 1) work(0);
+    else {
+        std::vector<std::thread> th;
+        for (int t = 0; t < nthr; ++t) th.emplace_back(work, t);
+        for (auto& x : th) x.join();
+    }
+    return WSB_OK;
+}
+
 extern "C" int wsb_ctx_create(int device, wsb_ctx** out) {
     if (!out) return WSB_E_ARG;
     *out = nullptr;
@@ -301,6 +332,7 @@ template <class T> static int generate(wsb_ctx* ctx, T** dst, T a0, T d, int64_t
 
 extern "C" void wsb_batch_destroy(wsb_batch* b) {
     if (!b) return;
+    std::lock_guard<std::recursive_mutex> lock_(b->ctx->mu);
     cudaSetDevice(b->ctx->device);
     cudaStreamSynchronize(b->ctx->copy_stream);
     cudaStreamSynchronize(b->ctx->stream);
@@ -357,6 +389,7 @@ static int batch_create_impl(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t
         n_q <= 0 || n_s <= 0 || n_pairs <= 0 || n_pairs > (int64_t)0x7fffffff || (vouched && (n_pairs > n_q || n_pairs > n_s)))
         return WSB_E_ARG;
     *out = nullptr;
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     CUDA_TRY(ctx, cudaSetDevice(ctx->device));
     wsb_batch* b = new (std::nothrow) wsb_batch();
     if (!b) return WSB_E_NOMEM;
@@ -453,8 +486,11 @@ static int batch_create_impl(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t
         };
         for (int k = 0; k < n_pieces; ++k)   // boundaries on multiples of 2048 pairs (packed units never straddle pieces)
             b->piece_end[k] = k + 1 == n_pieces ? n_pairs : std::min<int64_t>(n_pairs, (n_pairs * (k + 1) / n_pieces + 2047) / 2048 * 2048);
+        // the arithmetic shortcut holds only for reads stored back to back from offset 0 (always true for the vouched
+        // uniform entry); strided or prefixed pools with an identity pair list take the scan below
+        const bool back_to_back = regular && ap_off[0] && o0[0] == 0 && od[0] == l0[0] && ap_off[1] && o0[1] == 0 && od[1] == l0[1];
         if (n_pieces == 1) { need_q[0] = q_total; need_s[0] = s_total; }
-        else if (regular) {   // pair p needs the pool bytes up to (p + 1) * length
+        else if (back_to_back) {   // pair p needs the pool bytes up to (p + 1) * length
             for (int k = 0; k < n_pieces; ++k) { need_q[k] = b->piece_end[k] * l0[0]; need_s[k] = b->piece_end[k] * l0[1]; }
             need_q[n_pieces - 1] = q_total; need_s[n_pieces - 1] = s_total;
         } else {
@@ -566,6 +602,8 @@ extern "C" int wsb_batch_create(wsb_ctx* ctx, const uint8_t* q_codes, const int6
                                 int64_t n_q, const uint8_t* s_codes, const int64_t* s_off, const int32_t* s_len,
                                 int64_t n_s, const int32_t* pair_q, const int32_t* pair_s, int64_t n_pairs,
                                 wsb_batch** out) {
+    if (!ctx) return WSB_E_ARG;
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     int rc = wsb_batch_create_async(ctx, q_codes, q_off, q_len, n_q, s_codes, s_off, s_len, n_s, pair_q, pair_s, n_pairs, out);
     if (rc) return rc;
     cudaError_t e = cudaStreamSynchronize(ctx->copy_stream);  // host arrays may be reused by the caller after return
@@ -994,6 +1032,7 @@ static int check_scheme(const wsb_scheme* s, int atype) {
 static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int variant, float* kernel_ms,
                             int32_t* n_launches, bool plan_only) {
     if (!b) return WSB_E_ARG;
+    std::lock_guard<std::recursive_mutex> lock_(b->ctx->mu);
     int rc = check_scheme(sch, atype);
     if (rc) return rc;
     if (variant < WSB_VARIANT_AUTO || variant > WSB_VARIANT_S16X2) return WSB_E_ARG;
@@ -1226,6 +1265,9 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
         if (b->uniform) any_empty = b->m[0] == 0 || b->n[0] == 0;
         else for (int64_t p = 0; p < b->n_pairs && !any_empty; ++p) any_empty = b->m[p] == 0 || b->n[p] == 0;
         if (any_empty) {
+            // deferred upload (traceback of a large global / semiglobal batch): the metadata this kernel reads travels on
+            // the copy stream; piece 0's event is recorded behind all of it
+            if (defer_upload && b->n_pieces > 0) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, b->piece_ev[0], 0));
             const int thr = 256;
             empty_side_kernel<<<(unsigned)((b->n_pairs + thr - 1) / thr), thr, 0, ctx->stream>>>(
                 b->d_pq, b->d_ps, b->d_qlen, b->d_slen, b->n_pairs, atype, affine ? 1 : 0, sch->gap_open, beta_eff,
@@ -1251,6 +1293,7 @@ extern "C" int wsb_batch_score(wsb_batch* b, const wsb_scheme* sch, int atype, i
 extern "C" int wsb_batch_fetch_scores(wsb_batch* b, int32_t* out_score, int32_t* out_i, int32_t* out_j, int32_t* status) {
     if (!b || !out_score || !out_i || !out_j) return WSB_E_ARG;
     wsb_ctx* ctx = b->ctx;
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     CUDA_TRY(ctx, cudaSetDevice(ctx->device));
     const size_t bytes = sizeof(int32_t) * (size_t)b->n_pairs;
     CUDA_TRY(ctx, cudaMemcpyAsync(out_score, b->d_score, bytes, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1269,6 +1312,8 @@ extern "C" int wsb_score_batch(wsb_ctx* ctx, const wsb_scheme* scheme, int align
                                const uint8_t* s_codes, const int64_t* s_off, const int32_t* s_len, int64_t n_s,
                                const int32_t* pair_q, const int32_t* pair_s, int64_t n_pairs, int32_t* out_score,
                                int32_t* out_i, int32_t* out_j, int32_t* status) {
+    if (!ctx) return WSB_E_ARG;
+    std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     wsb_batch* b = nullptr;
     int rc = wsb_batch_create(ctx, q_codes, q_off, q_len, n_q, s_codes, s_off, s_len, n_s, pair_q, pair_s, n_pairs, &b);
     if (rc) return rc;

@@ -64,6 +64,38 @@ class SequencePool:
         out.uniform_len = self.uniform_len
         return out
 
+    def subset(self, ids: np.ndarray) -> "SequencePool":
+        """Compact pool of the sequences `ids` (in that order): what one GPU shard uploads when its pairs reference only a
+        part of the pool.  Uniform pools keep their shape, so a contiguous id range of one is a zero-copy slice."""
+        from . import _native as N
+        ids = np.asarray(ids, np.int64)
+        if self.uniform_len is not None and len(ids) and int(ids[-1]) - int(ids[0]) + 1 == len(ids) and \
+                (len(ids) == 1 or bool((np.diff(ids) == 1).all())):
+            return self.slice_uniform(int(ids[0]), int(ids[-1]) + 1)
+        codes, off = N.compact_pool(self.codes, self.off, self.len, ids)
+        out = SequencePool(codes, off, self.len[ids], None if self.ids is None else [self.ids[int(k)] for k in ids])
+        if self.uniform_len is not None:
+            out.uniform_len = self.uniform_len
+        return out
+
+    def slice_uniform(self, lo: int, hi: int) -> "SequencePool":
+        """Reads lo .. hi-1 of a uniform pool without copying (2-bit pools: lo * length must be a multiple of four symbols,
+        else the slice falls back to the byte form)."""
+        L = self.uniform_len
+        if L is None:
+            raise ValueError("slice_uniform needs a pool built by from_uniform")
+        n = hi - lo
+        off = np.arange(n, dtype=np.int64) * L
+        lens = np.full(n, L, np.int32)
+        ids = None if self.ids is None else self.ids[lo:hi]
+        no_flags = self.flag_pos is None or len(self.flag_pos) == 0
+        if self.packed is not None and (lo * L) % 4 == 0 and no_flags:
+            out = SequencePool.from_packed(self.packed[lo * L // 4:(hi * L + 3) // 4], off, lens, None, ids)
+        else:
+            out = SequencePool(self.codes[lo * L:hi * L], off, lens, ids)
+        out.uniform_len = L
+        return out
+
     def __getitem__(self, k: int) -> Sequence:
         """Materialise one Sequence (reference type) on demand."""
         o, n = int(self.off[k]), int(self.len[k])

@@ -173,3 +173,65 @@ def test_multi_shard_assembly_on_one_gpu(monkeypatch, result_mode):
     assert list(one.results) == list(three.results)
     for c in made:
         c.close()
+
+
+def _contexts_per_shard(monkeypatch):
+    from paper_2205_07610_b200 import _native as N, batch as B
+    made = []
+    monkeypatch.setattr(B, "get_context", lambda device: made.append(N.Context(0)) or made[-1])
+    return made
+
+
+@pytest.mark.parametrize("result_mode", ["score_only", "traceback"])
+def test_sharded_run_uploads_every_pool_byte_once(monkeypatch, result_mode):
+    """a shard uploads only what its pairs reference.  Arbitrary pair lists over pools four times larger than
+    any shard needs: the four shards together move about as many bytes as one shard would, results identical."""
+    rng = np.random.default_rng(44)
+    n_seq, n = 4000, 1000
+    lens = rng.integers(60, 300, n_seq)
+    qs = [rng.integers(0, 4, int(L)).astype(np.uint8) for L in lens]
+    ss = [rng.integers(0, 4, int(L)).astype(np.uint8) for L in lens]
+
+    def pool(seqs):
+        ln = np.array([len(s) for s in seqs], np.int32)
+        off = np.zeros(len(seqs), np.int64); off[1:] = np.cumsum(ln[:-1])
+        return W.SequencePool(np.concatenate(seqs), off, ln)
+
+    used = rng.choice(n_seq, n, replace=False)
+    pairs = np.stack([used, rng.permutation(used)], 1).astype(np.int32)      # a quarter of either pool is referenced
+    cfg = W.AlignConfig("local" if result_mode == "score_only" else "global", "affine", result_mode)
+    one = W.run_batch(W.BatchJob(pool(qs), pool(ss), pairs, cfg, W.ScoringScheme(), devices=[0]))
+    made = _contexts_per_shard(monkeypatch)
+    four = W.run_batch(W.BatchJob(pool(qs), pool(ss), pairs, cfg, W.ScoringScheme(), devices=[0, 0, 0, 0]))
+    assert len(made) == 4 and list(one.results) == list(four.results)
+    referenced = int(lens[pairs[:, 0]].sum() + lens[pairs[:, 1]].sum())
+    metadata = 4 * (8 + 4) * n // 2 + 2 * 4 * n          # offsets + lengths of the compact pools, pair columns
+    assert four.h2d_bytes <= referenced + 2 * metadata + 4096, (four.h2d_bytes, referenced)
+    assert four.h2d_bytes * 3 < one.h2d_bytes            # the single shard sends the whole pools
+    for c in made:
+        c.close()
+
+
+def test_sharded_reads_matrix_takes_the_metadata_free_path_per_shard(monkeypatch):
+    """Uniform pools with the identity pair list: contiguous blocks, zero-copy slices, every shard on the regular upload
+    (no offset / length / pair arrays), bytes and 2-bit pools alike."""
+    rng = np.random.default_rng(45)
+    n, L = 140_000, 64
+    q = rng.integers(0, 4, (n, L), dtype=np.uint8); s = rng.integers(0, 4, (n, L), dtype=np.uint8)
+    s[::3] = q[::3]
+    pairs = np.stack([np.arange(n), np.arange(n)], 1).astype(np.int32)
+    cfg = W.AlignConfig("local", "affine", "score_only")
+    one = W.run_batch(W.BatchJob(W.SequencePool.from_uniform(q), W.SequencePool.from_uniform(s), pairs, cfg,
+                                 W.ScoringScheme(), devices=[0]))
+    made = _contexts_per_shard(monkeypatch)
+    for packed in (False, True):
+        pq, ps = W.SequencePool.from_uniform(q), W.SequencePool.from_uniform(s)
+        if packed:
+            pq, ps = pq.to_packed(), ps.to_packed()
+        two = W.run_batch(W.BatchJob(pq, ps, pairs, cfg, W.ScoringScheme(), devices=[0, 0]))
+        assert (two.results.score == one.results.score).all() and (two.results.q_end == one.results.q_end).all()
+        assert (two.results.s_end == one.results.s_end).all()
+        assert two.h2d_bytes == (2 * n * L // 4 if packed else 2 * n * L)      # pool bytes only, each once
+        assert len(two.shard_cells) == 2 and sum(two.shard_cells) == n * L * L
+    for c in made:
+        c.close()

@@ -159,8 +159,9 @@ def test_cfg5_pareto_lengths_swap_symmetry_and_every_giant_against_the_oracle(ct
     others = np.setdiff1d(giant, capped)
     rng = np.random.default_rng(5)
     assert len(capped) >= 50 and int(cells[capped].max()) == 10_000_000_000
-    sel = np.concatenate([rng.choice(small, 10_000, replace=False), rng.choice(mid, 48, replace=False),
-                          rng.choice(others, 40, replace=False), capped]).astype(np.int32)
+    # giants first: the oracle hands small lists out pair by pair, largest work at the front keeps its threads level
+    sel = np.concatenate([capped, rng.choice(others, 40, replace=False), rng.choice(mid, 48, replace=False),
+                          rng.choice(small, 10_000, replace=False)]).astype(np.int32)
     want = _oracle(qp, sp, sel, "local", AFF)    # rolling-row oracle: ~1.2e12 cells, two to three minutes on 16 cores
     for name, g, w in zip(("score", "end_i", "end_j"), a[:3], want):
         bad = np.nonzero(g[sel] != w)[0]
