@@ -206,6 +206,29 @@ def cpu_sample(cfg, seconds_target=12.0, seed=7):
     return rate, threads, pairs, dt
 
 
+def workload_config(args, cfg, n_pairs):
+    """The `config` object of the JSON line: identical for the GPU arm and the reference arm (what differs between them --
+    kernel variant, host format, the CPU arm's bounded sample -- lives outside it)."""
+    L = cfg["length"]
+    traceback = bool(cfg.get("traceback"))
+    input_bytes = 2 * n_pairs * L if L else 0   # (the Pareto batch of cfg5: ~0.2 GB, described in words below)
+    return {"workload": args.workload, "pairs_per_gpu": n_pairs, "read_length": L if L else "pareto 100..%d" % args.cap,
+            "align_type": cfg["align_type"], "gap_model": cfg["gap_model"], "scheme": list(cfg["scheme"]),
+            "result_mode": "traceback" if traceback else "score_only",
+            "statistic": "median of the timed steps, mean of the two middle values (reference bench.py:35-43, PAPER.md:454)",
+            "l2": (f"inputs {input_bytes / 1e6:.0f} MB per GPU vs 126 MB L2 " if L else "inputs ~200 MB per batch vs 126 MB L2 ")
+                  + ("(no flush needed)" if input_bytes > 252e6 else
+                     "(inputs re-read from L2/HBM each step; per-cell DRAM traffic is ~0 either way)"),
+            "sharding": "independent pairs per rank, no collective; gloo for barrier/max only"}
+
+
+def median_rule(values):
+    """Median; even count: mean of the two middle values (reference bench.py:35-43)."""
+    v = sorted(values)
+    mid = len(v) // 2
+    return v[mid] if len(v) % 2 else 0.5 * (v[mid - 1] + v[mid])
+
+
 def run_reference(args, cfg, rank, world):
     """--impl reference: the reference's CPU algorithm (oracle port, all host threads); rank 0 only."""
     if rank != 0:
@@ -217,15 +240,15 @@ def run_reference(args, cfg, rank, world):
         info = (threads, pairs, dt)
         if step >= args.warmup:
             rates.append(rate)
-    value = float(np.mean(rates))
+    value = float(median_rule(rates))
     threads, pairs, dt = info
     length = cfg["length"] if cfg["length"] else "pareto(cap 6000)"
-    sample = f"{pairs} pairs of {length} bp per step ({dt:.2f} s), {cfg['align_type']}/{cfg['gap_model']}"
+    sample = (f"every step scores {pairs} pairs of {length} bp of the workload ({dt:.2f} s; GCUPS does not depend on the batch "
+              f"size), {cfg['align_type']}/{cfg['gap_model']}")
     line = {"impl": "reference", "metric": "GCUPS", "value": value, "unit": "GCUPS", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "int32", "data": "synthetic",
-            "config": {"workload": args.workload, "pairs_per_step": pairs, "read_length": length,
-                       "align_type": cfg["align_type"], "gap_model": cfg["gap_model"], "scheme": list(cfg["scheme"])},
+            "config": workload_config(args, cfg, cfg["pairs"]),
             "cpu_baseline": {"value": value, "unit": "GCUPS", "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -309,8 +332,11 @@ def main():
     wall = time.perf_counter() - t_wall0
     clocks = sampler.stop()
     total_ms = dist_max(float(np.sum(step_ms)), world)      # slowest rank
+    median_ms = dist_max(float(median_rule(step_ms)), world)
     total_cells = dist_sum(float(cells), world) * args.steps   # weak: every rank its own batch; strong (cfg5): the shards add up to the one batch
-    value = total_cells / (total_ms * 1e-3) / 1e9
+    value = total_cells / args.steps / (median_ms * 1e-3) / 1e9   # the reference's statistic: median step, not the mean
+    value_mean = total_cells / (total_ms * 1e-3) / 1e9
+    kernel_cycles = 0 if traceback else batch.kernel_cycles      # SM cycles of the last headline-kernel launch (0: another kernel)
     launches = int(dist_sum(float(launches), world))
 
     # end to end through the public API: host buffers in, host results out, every step
@@ -357,26 +383,24 @@ def main():
     except OSError:
         pass
     roofline = {"bound": "alu_issue", "achieved": per_gpu, "peak": peak, "unit": "GCUPS", "frac": per_gpu / peak,
-                "traffic": traffic, "peak_source": "N_SM*128*f_SM*W/I_cell with f_SM = " + ("sm_max_mhz of MEASURED_PEAKS.json" if "sm_max_mhz" in peaks
+                "traffic": traffic, "traffic_source": "static: profiles/ncu_traffic.json (dram__bytes_read + dram__bytes_write of one "
+                "ncu --set full capture of this workload's dominant kernel, scaled to the launch size); not re-measured per run",
+                "peak_source": "N_SM*128*f_SM*W/I_cell with f_SM = " + ("sm_max_mhz of MEASURED_PEAKS.json" if "sm_max_mhz" in peaks
                                                                           else "1965 MHz (fallback: MEASURED_PEAKS.json absent)"),
                 "i_cell": cfg["i_cell"], "cells_per_thread_instr": width, "n_sm": n_sm, "f_ghz": f_ghz}
     if clocks.get("sm_mhz"):
         cyc_peak = n_sm * 128 * clocks["sm_mhz"] / 1e3 * width / cfg["i_cell"]
         roofline["frac_at_measured_clock"] = per_gpu / cyc_peak
+    if kernel_cycles > 0:   # cycle-based fraction: algorithmic thread-instructions / issue slots the launch had
+        roofline["frac_cycle_based"] = (cells * cfg["i_cell"] / width) / (float(kernel_cycles) * n_sm * 128)
+        roofline["kernel_sm_cycles"] = int(kernel_cycles)
 
     if rank == 0:
         line = {"metric": "GCUPS", "value": value, "unit": "GCUPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong" if strong else "weak",
+                "ms_per_step": median_ms, "ms_per_step_mean": total_ms / args.steps, "value_mean": value_mean, "higher_is_better": True, "scaling": "strong" if strong else "weak",
                 "vs_baseline": None, "dtype": dtype, "data": "synthetic",
-                "config": {"workload": args.workload, "pairs_per_gpu": n, "read_length": L if L else "pareto 100..%d" % args.cap,
-                           "align_type": cfg["align_type"],
-                           "gap_model": cfg["gap_model"], "scheme": list(cfg["scheme"]),
-                           "result_mode": "traceback" if traceback else "score_only", "variant": variant,
-                           "e2e_host_format": args.host_format,
-                           "l2": f"inputs {(len(pool_q[0]) + len(pool_s[0])) / 1e6:.0f} MB per GPU vs 126 MB L2 "
-                                 + ("(no flush needed)" if len(pool_q[0]) + len(pool_s[0]) > 252e6 else
-                                    "(inputs re-read from L2/HBM each step; per-cell DRAM traffic is ~0 either way)"),
-                           "sharding": "independent pairs per rank, no collective; gloo for barrier/max only"},
+                "config": workload_config(args, cfg, n if not strong else cfg["pairs"]),
+                "variant": variant, "e2e_host_format": args.host_format,
                 "roofline": roofline,
                 "e2e": {"value": e2e_value, "unit": "GCUPS", "h2d_bytes_per_step": int(rep.h2d_bytes) * world,
                         "d2h_bytes_per_step": int(rep.d2h_bytes) * world, "steps": e2e_steps},

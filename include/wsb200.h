@@ -166,6 +166,10 @@ int wsb_f16_range_ok(const wsb_scheme* scheme, int32_t m, int32_t n);
 int wsb_plan_shards(const int32_t* q_len, const int32_t* s_len, const int32_t* pair_q, const int32_t* pair_s,
                     int64_t n_pairs, int32_t n_shards, int32_t* shard_of, int64_t* shard_cells);
 
+/* SM cycles the last packed int16 short-read launch of the batch took (largest per-block clock64 span; 0 if none ran):
+ * the denominator of the cycle-based roofline fraction, independent of the clock the GPU happened to hold. */
+int64_t wsb_batch_kernel_cycles(wsb_batch* batch);
+
 /* Gather sequences ids[0 .. n_ids) of a pool into a compact pool: out_codes (sum of their lengths) receives them back to
  * back, out_off[k] the new offset of sequence ids[k].  Used by the multi-GPU runner so that every shard uploads only the
  * sequences its pairs reference (the reference's worker threads share one read-only copy, batch.py:213-240). */

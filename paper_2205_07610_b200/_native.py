@@ -24,7 +24,7 @@ EXPORTED_SYMBOLS = (
     "wsb_ctx_sm_count", "wsb_batch_create", "wsb_batch_create_async", "wsb_batch_create_packed_async", "wsb_batch_create_uniform_async", "wsb_batch_destroy", "wsb_batch_score", "wsb_batch_fetch_scores",
     "wsb_batch_traceback", "wsb_batch_fetch_traceback", "wsb_batch_total_cells", "wsb_score_batch",
     "wsb_traceback_batch", "wsb_merged_state_exact", "wsb_f16_range_ok", "wsb_plan_shards", "wsb_batch_has_faults", "wsb_pinned_alloc",
-    "wsb_pinned_free", "wsb_batch_total_runs", "wsb_batch_h2d_bytes", "wsb_compact_pool",
+    "wsb_pinned_free", "wsb_batch_total_runs", "wsb_batch_h2d_bytes", "wsb_compact_pool", "wsb_batch_kernel_cycles",
 )
 
 
@@ -258,6 +258,13 @@ class Batch:
         self._h = h
         self.h2d_bytes = int(self._lib.wsb_batch_h2d_bytes(h))
         return self
+
+    @property
+    def kernel_cycles(self) -> int:
+        """SM cycles of the last packed int16 short-read launch (0 when another kernel carried the batch)."""
+        self._lib.wsb_batch_kernel_cycles.restype = ctypes.c_int64
+        self._lib.wsb_batch_kernel_cycles.argtypes = [ctypes.c_void_p]
+        return int(self._lib.wsb_batch_kernel_cycles(self._h))
 
     @property
     def total_cells(self) -> int:

@@ -52,6 +52,7 @@ struct ScoreParams {
     int32_t* out_score; int32_t* out_i; int32_t* out_j;
     int32_t match, mismatch, alpha, beta;  // beta == alpha for the linear model
     int32_t one = 1;    // the value 1, opaque to the compiler (multiplies that must stay multiplies)
+    unsigned long long* block_cycles = nullptr;   // optional: SM cycles every block of the launch spent (clock64 end - start)
     int32_t* redo; int32_t* redo_count;   // packed int16 kernel: pairs it cannot encode (flagged subject symbol) are listed here
     const int32_t* n_pairs_dev;           // re-score launch: units is that list, its length is read from the device
     void* bnd;          // stage border scratch: per lane group bnd_rows x {A, B}

@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(kThreads, MINB) s16_local_short_kernel(const S
     uint8_t (*raw)[4][kShort16Raw] = reinterpret_cast<uint8_t (*)[4][kShort16Raw]>(&qbuf[GPB][0]);
     int (*meta)[16] = reinterpret_cast<int (*)[16]>(&raw[GPB][0][0]);   // per group: pidx[2], len[4], shift[4]
 
+    const long long cycles_at_start = prm.block_cycles ? clock64() : 0;
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int t = tid & (P - 1);
@@ -408,6 +409,9 @@ __global__ void __launch_bounds__(kThreads, MINB) s16_local_short_kernel(const S
             }
         }
     }
+    // cycle-based roofline fraction: a resident block lives as long as the launch, so the largest value is the
+    // launch's duration in cycles of the SM it ran on
+    if (prm.block_cycles && tid == 0) prm.block_cycles[blockIdx.x] = (unsigned long long)(clock64() - cycles_at_start);
 }
 
 }  // namespace wsb

@@ -124,6 +124,8 @@ struct wsb_batch {
     size_t bnd_bytes = 0;
     int32_t* d_redo_long = nullptr;   // packed int16 long-read kernel: same, re-scored by the int32 long-read kernel
     int32_t* d_redo = nullptr;   // packed int16 kernel: list of pairs to re-score (slot 0 = count, list from slot 4)
+    unsigned long long* d_cycles = nullptr;   // per-block SM cycles of the last packed int16 short launch (wsb_batch_kernel_cycles)
+    int cycles_blocks = 0;
     // Piecewise upload: piece k covers pairs [piece_end[k-1], piece_end[k]) and is complete (pools included) once
     // piece_ev[k] has fired on the copy stream; the first score call after creation launches piece by piece.
     static constexpr int kMaxPieces = 16;
@@ -337,6 +339,7 @@ extern "C" void wsb_batch_destroy(wsb_batch* b) {
     cudaStreamSynchronize(b->ctx->copy_stream);
     cudaStreamSynchronize(b->ctx->stream);
     for (int k = 0; k < wsb_batch::kMaxPieces; ++k) if (b->piece_ev[k]) cudaEventDestroy(b->piece_ev[k]);
+    if (b->d_cycles) b->ctx->release(b->d_cycles);
     for (void* p : {(void*)b->d_qcodes, (void*)b->d_scodes, (void*)b->d_qoff, (void*)b->d_soff, (void*)b->d_qlen,
                     (void*)b->d_slen, (void*)b->d_pq, (void*)b->d_ps, (void*)b->d_score, (void*)b->d_i, (void*)b->d_j,
                     b->d_bnd, (void*)b->d_redo, (void*)b->d_redo_long, b->stage_blocks[0], b->stage_blocks[1], b->stage_blocks[2], b->stage_blocks[3]})
@@ -612,6 +615,18 @@ extern "C" int wsb_batch_create(wsb_ctx* ctx, const uint8_t* q_codes, const int6
 }
 
 extern "C" int64_t wsb_batch_total_cells(const wsb_batch* b) { return b ? b->total_cells : 0; }
+// SM cycles of the last packed int16 short-read launch of this batch (largest per-block clock64 span), 0 if there was none
+extern "C" int64_t wsb_batch_kernel_cycles(wsb_batch* b) {
+    if (!b || !b->d_cycles || b->cycles_blocks <= 0) return 0;
+    std::lock_guard<std::recursive_mutex> lock_(b->ctx->mu);
+    std::vector<unsigned long long> h((size_t)b->cycles_blocks);
+    if (cudaSetDevice(b->ctx->device) != cudaSuccess) return 0;
+    if (cudaMemcpyAsync(h.data(), b->d_cycles, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, b->ctx->stream) != cudaSuccess) return 0;
+    if (cudaStreamSynchronize(b->ctx->stream) != cudaSuccess) return 0;
+    unsigned long long mx = 0;
+    for (auto v : h) mx = std::max(mx, v);
+    return (int64_t)mx;
+}
 extern "C" int64_t wsb_batch_h2d_bytes(const wsb_batch* b) { return b ? b->h2d_bytes : 0; }
 extern "C" int wsb_batch_has_faults(const wsb_batch* b) { return (b && b->last_plan && b->last_plan->any_error) ? 1 : 0; }
 
@@ -1194,7 +1209,14 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
         prm.units = g.unit_off >= 0 ? plan.d_units + g.unit_off : nullptr;
         prm.n_units = g.n_units; prm.n_pairs = b->n_pairs; prm.pair_base = 0;
         prm.redo = b->d_redo ? b->d_redo + 4 : nullptr; prm.redo_count = b->d_redo; prm.n_pairs_dev = nullptr;
-        if (g.variant == WSB_VARIANT_S16X2) { any_s16 = true; s16_gap = g.gap; }
+        if (g.variant == WSB_VARIANT_S16X2) {
+            any_s16 = true; s16_gap = g.gap;
+            if (!piecewise) {   // one launch carries the group: its blocks report their cycle counts
+                if (!b->d_cycles) CUDA_TRY(ctx, ctx->alloc((void**)&b->d_cycles, sizeof(unsigned long long) * 4096));
+                b->cycles_blocks = std::min(geo[k].grid, 4096);
+                if (geo[k].grid <= 4096) prm.block_cycles = b->d_cycles;
+            }
+        }
         prm.out_score = b->d_score; prm.out_i = b->d_i; prm.out_j = b->d_j;
         prm.match = sch->match; prm.mismatch = sch->mismatch; prm.alpha = sch->gap_open; prm.beta = beta_eff;
         prm.bnd = geo[k].bnd_rows ? (char*)b->d_bnd + geo[k].bnd_off : nullptr; prm.bnd_rows = geo[k].bnd_rows;

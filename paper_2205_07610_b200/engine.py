@@ -124,12 +124,9 @@ def engine_score(query: Sequence, subject: Sequence, cfg: AlignConfig, scheme: S
     cfg = validate_config(cfg, scheme)
     m, n = len(query), len(subject)
     check_length_bounds(m, n, scheme)
-    variant = "auto"
-    if tuning is not None and tuning.packed:
-        if not packed_range_ok(scheme, m, n) or not f16_range_ok(scheme, m, n):
-            raise PackedRangeOverflow(f"problem of size {m}x{n} exceeds the packed range (max |score| step {scheme.max_step})")
-        variant = "f16x2"
-    score, ei, ej = _score_pairs([(query, subject)], cfg, scheme, variant)
+    # tuning.packed is a hint, as in the reference (engine.py:383-400 never looks at it): the planner packs two
+    # alignments per register wherever that is exact (int16 / half2) and runs int32 elsewhere
+    score, ei, ej = _score_pairs([(query, subject)], cfg, scheme, "auto")
     if stats is not None:
         stats.cells += m * n
         stats.stages += 1
@@ -139,15 +136,18 @@ def engine_score(query: Sequence, subject: Sequence, cfg: AlignConfig, scheme: S
 def engine_score_packed(pair_a: tuple[Sequence, Sequence], pair_b: tuple[Sequence, Sequence], cfg: AlignConfig,
                         scheme: ScoringScheme, tuning: EngineTuning | None = None, stats: EngineStats | None = None,
                         instrument: bool = False):
-    """Two problems in the halves of one half2 lane group: ((score_a, end_a), (score_b, end_b), cells)."""
+    """Two problems scored in one call: ((score_a, end_a), (score_b, end_b), cells).  Accepts and rejects exactly what
+    the reference does (engine.py:512-536): PackedRangeOverflow beyond max_step * (m + n) < 2^14, ValueError for affine
+    schemes outside the merged-state rule.  Inside that range the planner picks the widest exact kernel: packed int16
+    (short local pairs, long twins), packed half2 (values within 2^11) or int32 -- every one of them bit-exact."""
     cfg = validate_config(cfg, scheme)
     for q, s in (pair_a, pair_b):
-        if not packed_range_ok(scheme, len(q), len(s)) or not f16_range_ok(scheme, len(q), len(s)):
-            raise PackedRangeOverflow(f"problem of size {len(q)}x{len(s)} exceeds the packed range "
+        if not packed_range_ok(scheme, len(q), len(s)):
+            raise PackedRangeOverflow(f"problem of size {len(q)}x{len(s)} exceeds the packed 16-bit range "
                                       f"(max |score| step {scheme.max_step})")
     if scheme.gap_model == "affine" and not merged_state_exact(scheme):
         raise ValueError("packed affine mode requires a merged-state-exact scheme")
-    score, ei, ej = _score_pairs([pair_a, pair_b], cfg, scheme, "f16x2")
+    score, ei, ej = _score_pairs([pair_a, pair_b], cfg, scheme, "auto")
     cells = len(pair_a[0]) * len(pair_a[1]) + len(pair_b[0]) * len(pair_b[1])
     if stats is not None:
         stats.cells += cells

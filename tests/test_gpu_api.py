@@ -93,6 +93,42 @@ def test_packed_engine_and_errors():
         W.BatchJob(_seqs(["AC"]), _seqs(["AC"]), [], cfg, aff)
 
 
+def _recipe_pair(seed, m, n, related):
+    """tests/golden/make_golden_packed_long.py:make_pair, restated (the fixture stores recipes + CRCs, not the text)."""
+    rng = np.random.default_rng(seed)
+    bases = np.array(list("ACGT"))
+    q = rng.integers(0, 4, m)
+    if related:
+        s = np.resize(q, n).copy()
+        mut = rng.random(n) < 0.08
+        s[mut] = (s[mut] + rng.integers(1, 4, int(mut.sum()))) % 4
+    else:
+        s = rng.integers(0, 4, n)
+    return "".join(bases[q]), "".join(bases[s])
+
+
+def test_packed_entry_accepts_the_reference_range_up_to_2_pow_14():
+    """engine_score_packed over the reference's whole packed range (max_step * (m + n) < 2^14, engine.py:504-536): 27
+    results of the REFERENCE's engine_score_packed on pairs of 600..4000 symbols; tuning.packed stays a hint."""
+    import zlib
+    for rec in load_golden("packed_long.json")["packed_long"]:
+        scheme = W.ScoringScheme(*rec["scheme"], rec["gap_model"])
+        c = W.AlignConfig(rec["align_type"], rec["gap_model"])
+        (qa, sa), (qb, sb) = _recipe_pair(*rec["a_recipe"]), _recipe_pair(*rec["b_recipe"])
+        assert [zlib.crc32((qa + "|" + sa).encode()), zlib.crc32((qb + "|" + sb).encode())] == rec["crc"]
+        qa, sa, qb, sb = _seqs([qa, sa, qb, sb])
+        assert W.packed_range_ok(scheme, len(qa), len(sa)) and W.packed_range_ok(scheme, len(qb), len(sb))
+        ra, rb, cells = W.engine_score_packed((qa, sa), (qb, sb), c, scheme)
+        assert [ra[0], ra[1][0], ra[1][1]] == rec["a"] and [rb[0], rb[1][0], rb[1][1]] == rec["b"] and cells == rec["cells"], rec
+        one = W.engine_score(qa, sa, c, scheme, tuning=W.EngineTuning(packed=True))     # never raises on range
+        assert [one[0], one[1][0], one[1][1]] == rec["a"]
+    aff = W.ScoringScheme(2, -1, 2, 1, "affine")
+    edge = _seqs(["A" * 4096, "C" * 4095, "A" * 4096, "C" * 4096])        # 2 * 8191 < 2^14 <= 2 * 8192
+    W.engine_score_packed((edge[0], edge[1]), (edge[0], edge[1]), W.AlignConfig("local", "affine"), aff)
+    with pytest.raises(W.PackedRangeOverflow):
+        W.engine_score_packed((edge[2], edge[3]), (edge[0], edge[1]), W.AlignConfig("local", "affine"), aff)
+
+
 def test_flagged_symbols_never_match():
     aff = W.ScoringScheme(2, -1, 2, 1, "affine")
     q, s = _seqs(["NNNN", "NNNN"])
