@@ -130,6 +130,15 @@ int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* scheme, int align_type, 
 int wsb_batch_fetch_traceback(wsb_batch* b, int32_t* out_score, int32_t* q_start, int32_t* q_end, int32_t* s_start,
                               int32_t* s_end, uint32_t* cigar, int64_t cigar_cap, int64_t* cigar_off, int32_t* status);
 
+/* Bounded-memory traceback (the reference's linear-space path: traceback.py:208-344 hirschberg, :312-344
+ * locate_endpoints).  A pair whose direction codes (0.5 byte per cell) exceed the scratch budget is traced through
+ * checkpointed tiles instead: same path as the full-matrix walk, 8/R + 8/512 bytes per cell.  wsb_batch_set_tb_scratch
+ * overrides the budget of this batch (bytes; 0 = library default 16 GiB or WSB_TB_SCRATCH_MB); wsb_batch_tb_info
+ * reports the last traceback call: out4 = {pairs that took the bounded path, cells they computed, tiles re-filled by
+ * their walks, peak scratch bytes of one such pair}. */
+int wsb_batch_set_tb_scratch(wsb_batch* b, int64_t bytes);
+int wsb_batch_tb_info(const wsb_batch* b, int64_t* out4);
+
 /* 1 when the last plan of the batch holds per-pair faults (then fetch the status array), else 0 */
 int wsb_batch_has_faults(const wsb_batch* b);
 /* Page-locked host memory for result buffers, recycled by the library (a fetch into such a block runs at PCIe speed;

@@ -25,6 +25,7 @@ EXPORTED_SYMBOLS = (
     "wsb_batch_traceback", "wsb_batch_fetch_traceback", "wsb_batch_total_cells", "wsb_score_batch",
     "wsb_traceback_batch", "wsb_merged_state_exact", "wsb_f16_range_ok", "wsb_plan_shards", "wsb_batch_has_faults", "wsb_pinned_alloc",
     "wsb_pinned_free", "wsb_batch_total_runs", "wsb_batch_h2d_bytes", "wsb_compact_pool", "wsb_batch_kernel_cycles",
+    "wsb_batch_set_tb_scratch", "wsb_batch_tb_info",
 )
 
 
@@ -76,6 +77,8 @@ def load():
     lib.wsb_batch_h2d_bytes.restype = i64
     lib.wsb_batch_total_runs.argtypes = [p]
     lib.wsb_batch_total_runs.restype = i64
+    lib.wsb_batch_set_tb_scratch.argtypes = [p, i64]
+    lib.wsb_batch_tb_info.argtypes = [p, p]
     lib.wsb_pinned_alloc.argtypes = [ctypes.c_size_t, p]
     lib.wsb_pinned_free.argtypes = [p]
     lib.wsb_pinned_free.restype = None
@@ -294,6 +297,20 @@ class Batch:
         if status is None:
             status = np.zeros(n, np.int32)  # calloc: costs nothing until somebody reads it
         return score, ei, ej, status
+
+    def set_tb_scratch(self, nbytes: int) -> None:
+        """Direction-code scratch budget of this batch; pairs whose codes exceed it take the bounded-memory path."""
+        rc = self._lib.wsb_batch_set_tb_scratch(self._h, int(nbytes))
+        if rc:
+            raise status_exception(rc, self.ctx.last_error())
+
+    def tb_info(self) -> dict:
+        """Counters of the bounded-memory path in the last traceback call."""
+        out = (ctypes.c_int64 * 4)()
+        rc = self._lib.wsb_batch_tb_info(self._h, out)
+        if rc:
+            raise status_exception(rc, self.ctx.last_error())
+        return {"pairs": int(out[0]), "cells": int(out[1]), "tiles": int(out[2]), "peak_bytes": int(out[3])}
 
     def traceback(self, scheme, align_type: str, timed: bool = True):
         s = scheme_struct(scheme)

@@ -7,6 +7,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include "traceback_fill16.cuh"
+#include "traceback_band_host.inl"
 
 struct TbShape { int P, K; };
 static const TbShape kTbShapes[] = {{8, 16}, {8, 32}, {32, 16}, {16, 16}, {8, 24}};   // index 4: packed int16 fill only
@@ -76,12 +77,26 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
     TracebackState& tb = b->tb;
     tb.valid = false;
 
+    size_t budget_words = (size_t)16384 << 18;  // 16 GiB in 32-bit words (a B200 carries 180 GB)
+    if (const char* e = getenv("WSB_TB_SCRATCH_MB")) { const long mb = atol(e); if (mb > 0) budget_words = (size_t)mb << 18; }
+    if (b->tb_scratch_bytes > 0) budget_words = (size_t)std::max<int64_t>(b->tb_scratch_bytes / 4, 1);
+    // pairs whose direction codes alone exceed the budget take the checkpointed-tile path (traceback_band.cuh)
+    auto is_giant = [&](int64_t p) {
+        const int m_ = b->m[p], n_ = b->n[p];
+        return m_ > 0 && n_ > 0 && (size_t)tb_code_words(m_, n_, kBandP, kBandK) > budget_words;
+    };
+    bool any_giant = false;
+    if (b->uniform) any_giant = is_giant(0);
+    else for (int64_t p = 0; p < np && !any_giant; ++p) any_giant = is_giant(p);
+    b->tb_band_pairs = b->tb_band_cells = b->tb_band_tiles = b->tb_band_peak = 0;
+
     // 1. end cells with the score kernels (identical tie-break); per-pair length faults surface here
     float score_ms = 0.f;
     int32_t score_launches = 0;
-    // (global / semiglobal: the fill kernel finds them itself, only the plan and the empty-side pairs are needed)
+    // (global / semiglobal: the fill kernel finds them itself, only the plan and the empty-side pairs are needed -- unless
+    // a giant pair needs its end cell before any code is written)
     rc = batch_score_impl(b, sch, atype, WSB_VARIANT_AUTO, kernel_ms ? &score_ms : nullptr, &score_launches,
-                          /*plan_only=*/atype != AT_LOCAL);
+                          /*plan_only=*/atype == AT_GLOBAL || (atype == AT_SEMI && !any_giant));
     if (rc) return rc;
     const Plan* score_plan = b->last_plan;
 
@@ -106,8 +121,6 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
                   : shape == 2 ? tb_pick_fill<32, 16>(atype, affine)
                   : shape == 3 ? tb_pick_fill<16, 16>(atype, affine) : tb_pick_fill<8, 32>(atype, affine);   // 4: never launched
     TbFillFn fill16 = (can16 && max_n <= P * K) ? tb_pick_fill16(shape, atype, ragged16, affine) : nullptr;
-    size_t budget_words = (size_t)16384 << 18;  // 16 GiB in 32-bit words (a B200 carries 180 GB)
-    if (const char* e = getenv("WSB_TB_SCRATCH_MB")) { const long mb = atol(e); if (mb > 0) budget_words = (size_t)mb << 18; }
 
     int per_sm = 0;
     CUDA_TRY(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fill, kThreads, 0));
@@ -167,6 +180,16 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
     int piece = 0;
     int64_t first = 0;
     while (first < np) {
+        if (any_giant && is_giant(first) && !(score_plan && !score_plan->status.empty() && score_plan->status[first] != 0)) {
+            int band_launches = 0;
+            float band_ms = 0.f;
+            const int brc = tb_band_pair(b, sch, atype, first, budget_words * 4, &band_ms, &band_launches);
+            if (brc) { cleanup(); return brc; }
+            total_ms += band_ms;
+            launches += band_launches;
+            ++first;
+            continue;
+        }
         // grow the chunk until the code budget is reached
         code_off.clear();
         int64_t words = 0, count = 0;
@@ -183,7 +206,7 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
             const int64_t p = first + count;
             const bool faulty = score_plan && score_plan->status[p] != 0;
             const int64_t w = (b->m[p] > 0 && b->n[p] > 0 && !faulty) ? tb_code_words(b->m[p], b->n[p], P, K) : 0;
-            if (count > 0 && words + w > (int64_t)budget_words) break;
+            if (count > 0 && (words + w > (int64_t)budget_words || (any_giant && !faulty && is_giant(p)))) break;
             code_off.push_back(faulty ? -1 : words);
             words += w;
             ++count;
@@ -254,15 +277,9 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
         TB_TRY(cudaMemcpyAsync(&chunk_runs, d_chunk_off + count, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
         TB_TRY(cudaStreamSynchronize(ctx->stream));
         if (tb.total_runs + chunk_runs > tb.runs_cap) {  // grow the run buffer, keeping what earlier chunks wrote
-            const int64_t want = std::max<int64_t>((tb.total_runs + chunk_runs) * 3 / 2 + 1024,
-                                                   (int64_t)((double)(tb.total_runs + chunk_runs) * np / (first + count)) + 1024);
-            uint32_t* bigger = nullptr;
-            TB_TRY(ctx->alloc((void**)&bigger, sizeof(uint32_t) * (size_t)want));
-            if (tb.d_runs && tb.total_runs)
-                TB_TRY(cudaMemcpyAsync(bigger, tb.d_runs, sizeof(uint32_t) * (size_t)tb.total_runs, cudaMemcpyDeviceToDevice, ctx->stream));
-            TB_TRY(cudaStreamSynchronize(ctx->stream));
-            if (tb.d_runs) ctx->release(tb.d_runs);
-            tb.d_runs = bigger; tb.runs_cap = want;
+            const int grc = tb_reserve_runs(ctx, tb, tb.total_runs + chunk_runs,
+                                            (int64_t)((double)(tb.total_runs + chunk_runs) * np / (first + count)) + 1024);
+            if (grc) { cleanup(); return grc; }
         }
         prm.runs = tb.d_runs + tb.total_runs;
         tb_launch_walk<2>(atype, prm, ctx->stream);
@@ -289,6 +306,18 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
     if (kernel_ms) *kernel_ms = total_ms;
     if (n_launches) *n_launches = launches;
     return status;
+}
+
+extern "C" int wsb_batch_set_tb_scratch(wsb_batch* b, int64_t bytes) {
+    if (!b || bytes < 0) return WSB_E_ARG;
+    b->tb_scratch_bytes = bytes;
+    return WSB_OK;
+}
+
+extern "C" int wsb_batch_tb_info(const wsb_batch* b, int64_t* out4) {
+    if (!b || !out4) return WSB_E_ARG;
+    out4[0] = b->tb_band_pairs; out4[1] = b->tb_band_cells; out4[2] = b->tb_band_tiles; out4[3] = b->tb_band_peak;
+    return WSB_OK;
 }
 
 extern "C" int64_t wsb_batch_total_runs(const wsb_batch* b) { return (b && b->tb.valid) ? b->tb.total_runs : -1; }

@@ -137,6 +137,9 @@ struct wsb_batch {
     bool upload_pending = false;
     int64_t h2d_bytes = 0;               // bytes that actually crossed the bus at creation (generated arrays excluded)
     TracebackState tb;  // traceback_kernels.cuh
+    // bounded-memory traceback of giant pairs (traceback_band.cuh): scratch budget override and counters of the last call
+    int64_t tb_scratch_bytes = 0;
+    int64_t tb_band_pairs = 0, tb_band_cells = 0, tb_band_tiles = 0, tb_band_peak = 0;
 };
 
 #define CUDA_TRY(ctx, expr)                                                                        \
