@@ -373,7 +373,7 @@ def main():
     # cfg3: the direction-code fill of a uniform batch runs packed int16 (two alignments per thread) unless switched off
     tb16 = args.workload == "cfg3" and not os.environ.get("WSB_TB_NO16")
     width = 1 if (variant == "i32" or args.workload == "cfg5" or (args.workload == "cfg3" and not tb16)) else 2
-    dtype = "i32" if width == 1 else ("f16x2" if variant == "f16x2" or args.workload == "cfg1" else "s16x2")
+    dtype = "i32" if width == 1 else ("f16x2" if variant == "f16x2" else "s16x2")
     peak = n_sm * 128 * f_ghz * width / cfg["i_cell"]
     per_gpu = value / world
     traffic = None

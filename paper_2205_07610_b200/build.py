@@ -8,7 +8,7 @@ PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG_DIR, "csrc")
 LIB_PATH = os.path.join(PKG_DIR, "libwsb200.so")
 SOURCES = ["wsb200.cu"]
-DEPS = ["wsb200.cu", "score_kernels.cuh", "score_short.cuh", "score_short16.cuh", "score_long.cuh", "score_long16.cuh", "traceback_kernels.cuh", "traceback_fill16.cuh", "traceback_host.inl", "traceback_band.cuh", "traceback_band_host.inl",
+DEPS = ["wsb200.cu", "score_kernels.cuh", "score_short.cuh", "score_short16.cuh", "score_short16g.cuh", "score_long.cuh", "score_long16.cuh", "traceback_kernels.cuh", "traceback_fill16.cuh", "traceback_host.inl", "traceback_band.cuh", "traceback_band_host.inl",
         os.path.join("..", "..", "include", "wsb200.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]

@@ -212,7 +212,10 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const ScoreParams prm) 
     const V c_nbeta = AR::splat(-beta);
     const V c_open_from_hm = AR::splat(-mism - alpha);  // A = H - alpha = HM - mismatch - alpha (exact model)
 
-    const int64_t rounds = (prm.n_units + n_groups - 1) / n_groups;
+    // re-score launch of pairs a packed kernel handed back: the unit count sits in device memory
+    const int64_t n_units = prm.n_pairs_dev ? (int64_t)((*prm.n_pairs_dev + NV - 1) / NV) : prm.n_units;
+    const int64_t n_listed = prm.n_pairs_dev ? (int64_t)*prm.n_pairs_dev : 0;
+    const int64_t rounds = (n_units + n_groups - 1) / n_groups;
     for (int64_t rd = 0; rd < rounds; ++rd) {
         const int64_t u = rd * n_groups + group_global;
         int pidx[NV], m[NV], n[NV];
@@ -222,8 +225,9 @@ __global__ void __launch_bounds__(kThreads) score_kernel(const ScoreParams prm) 
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
             int p = -1;
-            if (u < prm.n_units) {
-                if (prm.units) p = prm.units[u * NV + v];
+            if (u < n_units) {
+                if (prm.n_pairs_dev) p = u * NV + v < n_listed ? prm.units[u * NV + v] : -1;
+                else if (prm.units) p = prm.units[u * NV + v];
                 else { const int64_t pp = prm.pair_base + u * NV + v; p = pp < prm.n_pairs ? (int)pp : -1; }
             }
             pidx[v] = p; m[v] = 0; n[v] = 0; qp[v] = nullptr; sp[v] = nullptr;

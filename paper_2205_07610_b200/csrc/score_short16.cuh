@@ -350,14 +350,24 @@ __global__ void __launch_bounds__(kThreads, MINB) s16_local_short_kernel(const S
             if (rd + 1 < rounds) meta_step(part, u_next);
             const unsigned qstop = qaddr + 8u * (unsigned)max(0, min(quarter1, steps - done));
             done += quarter1;
+#ifdef WSB_S16_UNROLL2
+#pragma unroll 2
+#else
 #pragma unroll 1
+#endif
             while (qaddr != qstop) {
                 receive();
                 unsigned la = ta_l, lg = tg_l, rm, h_last, t_last;
                 row(qc0, qc1, qn0, qn1, h_d, la, lg, rm, h_last, t_last);
                 asm volatile("ld.shared.v2.b32 {%0, %1}, [%2+8];" : "=r"(qc0), "=r"(qc1) : "r"(qaddr) : "memory");
                 asm volatile("ld.shared.v2.b32 {%0, %1}, [%2+16];" : "=r"(qn0), "=r"(qn1) : "r"(qaddr) : "memory");
+#ifdef WSB_S16_SEND_FIRST
+                send(t_last, h_last);
+#endif
                 // the row that just finished: T - gamma of the strip (linear gaps: h - alpha, the same thing) plus the row tag
+#ifdef WSB_S16_NOREC      // timing experiment only (end cells wrong)
+                bestvec = __vmaxs2(bestvec, rm);
+#else
                 if constexpr (GAP == GAP_MERGED) {
                     TG[K] = qaddr;
                     bestvec = record16<NCH>(TG, bestvec, rm, snap_addr, snap_addr + HS);
@@ -365,7 +375,10 @@ __global__ void __launch_bounds__(kThreads, MINB) s16_local_short_kernel(const S
                     TA[K] = qaddr;
                     bestvec = record16<NCH>(TA, bestvec, rm, snap_addr, snap_addr + HS);
                 }
+#endif
+#ifndef WSB_S16_SEND_FIRST
                 send(t_last, h_last);
+#endif
                 qaddr += 8;
             }
         }

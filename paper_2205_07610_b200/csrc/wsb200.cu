@@ -5,6 +5,7 @@
 #include "score_kernels.cuh"
 #include "score_short.cuh"
 #include "score_short16.cuh"
+#include "score_short16g.cuh"
 #include "score_long.cuh"
 #include "score_long16.cuh"
 #include "traceback_kernels.cuh"
@@ -755,6 +756,19 @@ template <int P, int K, int MINB = 4> static KernelSel pick_short16(int gap, int
     return {s16_local_short_kernel<P, K, GAP_MERGED, MINB>, short16_smem_bytes<P, K>()};
 }
 
+// global alignment of short reads (score_short16g.cuh); ragged = units of unequal pairs (row m is captured in every trip)
+template <int P, int K> static KernelSel pick_short16g(int gap, int alpha, int gamma, bool ragged) {
+    const size_t smem = short16g_smem_bytes<P, K>();
+    if (gap == GAP_LINEAR) {
+        if (ragged) return {s16_global_short_kernel<P, K, GAP_LINEAR, true>, smem};
+        if (alpha == 1) return {s16_global_short_kernel<P, K, GAP_LINEAR, false, 1, 1>, smem};
+        return {s16_global_short_kernel<P, K, GAP_LINEAR, false>, smem};
+    }
+    if (ragged) return {s16_global_short_kernel<P, K, GAP_MERGED, true>, smem};
+    if (alpha == 2 && gamma == 1) return {s16_global_short_kernel<P, K, GAP_MERGED, false, 2, 1>, smem};
+    return {s16_global_short_kernel<P, K, GAP_MERGED, false>, smem};
+}
+
 template <int GAP> static LongFn pick_long16_atype(int atype) {
     switch (atype) {
         case AT_GLOBAL: return score_long16_kernel<AT_GLOBAL, GAP>;
@@ -770,8 +784,11 @@ static LongFn pick_long16(int atype, int gap) {
 
 // short_ok: every unit of the launch fits one stage and the short kernel's query buffer
 static KernelSel pick_kernel(int variant, int shape, int atype, int gap, bool masked, bool short_ok, bool wide,
-                             int alpha = 0, int gamma = 0) {
+                             int alpha = 0, int gamma = 0, bool ragged = true) {
     static const char* no_short = getenv("WSB_NO_SHORT");  // tuning aid: force the general kernel
+    if (variant == WSB_VARIANT_S16X2 && atype == AT_GLOBAL) {
+        return shape == 0 ? pick_short16g<8, 16>(gap, alpha, gamma, ragged) : pick_short16g<8, 19>(gap, alpha, gamma, ragged);
+    }
     if (variant == WSB_VARIANT_S16X2) {
         return shape == 0 ? pick_short16<8, 16>(gap, alpha, gamma) : pick_short16<8, 19>(gap, alpha, gamma);
     }
@@ -821,6 +838,9 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
     // (the snapshot of the packed int16 kernel holds T - alpha: it needs every gap step to cost something)
     const bool s16_ok = want_s16 && atype == AT_LOCAL && f16_scheme_ok && std::abs(sch->match) <= 127 &&
                         std::abs(sch->mismatch) <= 127 && sch->gap_open >= 1 && (!affine || sch->gap_extend >= 1);
+    // global alignment of short reads: no pad argument needed (pads sit right of / below every real cell), values in 16 bits
+    const bool s16g_ok = want_s16 && atype == AT_GLOBAL && merged_ok && !wide_scheme && std::abs(sch->match) <= 127 &&
+                         std::abs(sch->mismatch) <= 127;
     plan.status.assign((size_t)np, 0);
 
     if (variant == WSB_VARIANT_F16X2 && !merged_ok) return WSB_E_SCHEME;
@@ -835,6 +855,10 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
             var = WSB_VARIANT_S16X2; shape = n <= 128 ? 0 : 1;
             static const char* s16_shape = getenv("WSB_S16_SHAPE");   // tuning aid: lane-group shape / occupancy of the packed int16 kernel
             if (s16_shape && s16_shape[0]) shape = std::min(1, std::max(0, atoi(s16_shape)));   // packed int16 DPX kernel: same pairs as the half2 short kernel
+        } else if (variant == WSB_VARIANT_AUTO && s16g_ok && n <= 152 && m <= kShort16MaxM &&
+                   (int64_t)std::abs(sch->match) * std::min(m, n) + std::abs(sch->mismatch) <= 16000 &&
+                   3ll * sch->gap_open + (int64_t)beta_eff_plan * (m + n) + std::abs(sch->mismatch) <= 16000) {
+            var = WSB_VARIANT_S16X2; shape = n <= 128 ? 0 : 1;
         } else if (variant != WSB_VARIANT_I32 && fits) { var = WSB_VARIANT_F16X2; shape = best_shape(kShapesF16, kNumShapesF16, 5, m, n); }
         else { var = WSB_VARIANT_I32; shape = wide_scheme ? 0 : best_shape(kShapesI32, kNumShapesI32, 4, m, n); }
     };
@@ -1119,7 +1143,8 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
         const bool short_ok = g.max_n <= sh.P * sh.K && g.max_m <= kShortQRows - 4 * sh.P - 2;
         const KernelSel sel = pick_kernel(g.variant, g.shape, atype, g.gap, sch->mismatch > 0 || sch->match < 0, short_ok,
                                           std::abs(sch->match - sch->mismatch) > 127, sch->gap_open,
-                                          affine ? std::min(sch->gap_open, sch->gap_extend) : sch->gap_open);
+                                          affine ? std::min(sch->gap_open, sch->gap_extend) : sch->gap_open,
+                                          /*ragged=*/g.unit_off >= 0 || g.max_m < 16);
         KernelFn fn = sel.fn;
         if (!fn) return WSB_E_SCHEME;
         CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel.smem));
@@ -1246,7 +1271,25 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
         CUDA_TRY(ctx, cudaGetLastError());
         ++launches;
     }
-    if (any_s16) {   // re-score what the packed int16 kernel could not encode, with the half2 short kernel
+    if (any_s16 && atype == AT_GLOBAL) {   // global: the general int32 kernel takes the listed pairs (one pair per unit)
+        const int gap32 = !affine ? GAP_LINEAR : (wsb_merged_state_exact(sch) ? GAP_MERGED : GAP_EXACT);
+        const bool wide32 = std::abs(sch->match - sch->mismatch) > 127;
+        const KernelSel sel = pick_kernel(WSB_VARIANT_I32, wide32 ? 0 : 3, atype, gap32, false, false, wide32);
+        if (!sel.fn) return WSB_E_SCHEME;
+        CUDA_TRY(ctx, cudaFuncSetAttribute(sel.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel.smem));
+        ScoreParams prm = {};
+        prm.q_codes = b->d_qcodes; prm.q_off = b->d_qoff; prm.q_len = b->d_qlen;
+        prm.s_codes = b->d_scodes; prm.s_off = b->d_soff; prm.s_len = b->d_slen;
+        prm.pair_q = b->d_pq; prm.pair_s = b->d_ps;
+        prm.units = b->d_redo + 4; prm.n_pairs_dev = b->d_redo; prm.n_units = 0; prm.n_pairs = b->n_pairs;
+        prm.out_score = b->d_score; prm.out_i = b->d_i; prm.out_j = b->d_j;
+        prm.match = sch->match; prm.mismatch = sch->mismatch; prm.alpha = sch->gap_open; prm.beta = beta_eff;
+        prm.bnd = nullptr; prm.bnd_rows = 0;   // one stage: n <= 152 = 8 x 19 (the wide kernel's 8 x 16 would need borders)
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((b->n_pairs + 15) / 16, (int64_t)ctx->sm_count * 2));
+        sel.fn<<<grid, kThreads, sel.smem, ctx->stream>>>(prm);
+        CUDA_TRY(ctx, cudaGetLastError());
+        ++launches;
+    } else if (any_s16) {   // re-score what the packed int16 kernel could not encode, with the half2 short kernel
         const KernelSel sel = s16_gap == GAP_LINEAR
             ? KernelSel{f16_local_short_kernel<8, 19, GAP_LINEAR, true>, short_smem_bytes<8, 19>()}
             : KernelSel{f16_local_short_kernel<8, 19, GAP_MERGED, true>, short_smem_bytes<8, 19>()};

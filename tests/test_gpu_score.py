@@ -252,3 +252,39 @@ def test_packed_int16_long_read_kernel_twins_and_hand_backs(ctx, align_type, gap
     assert_scores_equal(got, want, f"long16 {align_type}/{gap_model}")
     i32 = gpu_scores(ctx, qs, ss, pairs, scheme, align_type, "i32")
     assert_scores_equal(i32, want, f"long int32 {align_type}/{gap_model}")
+
+
+@pytest.mark.parametrize("gap_model", ["linear", "affine"])
+def test_packed_int16_global_short_kernel(ctx, gap_model):
+    """AUTO sends short global pairs to score_short16g.cuh: uniform batches (row m captured in the last P trips), ragged
+    ones (captured in every trip), reads shorter than the lane group, flagged symbols on both sides (a flagged subject
+    symbol hands the pair to the int32 kernel inside the same call), schemes with positive mismatch / beta > alpha."""
+    rng = np.random.default_rng(1601)
+    schemes = [(2, -1, 2, 1), (3, -2, 4, 1), (1, -3, 2, 2), (5, -4, 10, 1), (2, 1, 3, 1), (2, -1, 1, 3), (1, -1, 0, 0)] \
+        if gap_model == "affine" else [(2, -1, 1, 1), (2, -1, 2, 2), (3, -2, 5, 5), (1, 1, 1, 1), (2, -1, 0, 0)]
+    for sch in schemes:
+        scheme = scheme_of(sch, gap_model)
+        if gap_model == "affine" and not N.merged_state_exact(scheme):
+            continue
+        # uniform 150 x 150 (and 150 x 140), odd pair count
+        for L, Ls in ((150, 150), (150, 140), (17, 152), (154, 9)):
+            n = 1001
+            qs = [random_codes(rng, L) for _ in range(n)]
+            ss = [mutate_codes(rng, q, 0.1, 0.05, 0.05)[:Ls] if i % 2 else random_codes(rng, Ls) for i, q in enumerate(qs)]
+            ss = [np.concatenate([s, random_codes(rng, Ls - len(s))]) for s in ss]
+            for i in range(0, n, 11):
+                if i % 3 != 1:
+                    s = ss[i].copy(); s[rng.integers(0, len(s))] = 4; ss[i] = s
+                if i % 3 != 0:
+                    q = qs[i].copy(); q[rng.integers(0, len(q))] = 4; qs[i] = q
+            pairs = [(i, i) for i in range(n)]
+            assert_scores_equal(gpu_scores(ctx, qs, ss, pairs, scheme, "global", "auto"),
+                                oracle_scores(qs, ss, pairs, scheme, "global"), f"uniform {L}x{Ls} {gap_model} {sch}")
+        # ragged: 1 .. 154 x 1 .. 152, plus pairs too long for the kernel
+        qs, ss, pairs = _random_batch(rng, 1500, 1, 152, flagged=0.1)
+        qs.append(random_codes(rng, 154)); ss.append(random_codes(rng, 1))
+        qs.append(random_codes(rng, 400)); ss.append(random_codes(rng, 90))
+        qs.append(random_codes(rng, 3)); ss.append(random_codes(rng, 3))
+        pairs = [(i, i) for i in range(len(qs))]
+        assert_scores_equal(gpu_scores(ctx, qs, ss, pairs, scheme, "global", "auto"),
+                            oracle_scores(qs, ss, pairs, scheme, "global"), f"ragged {gap_model} {sch}")
