@@ -3,15 +3,17 @@ from __future__ import annotations
 
 import os
 import subprocess
+from concurrent.futures import ThreadPoolExecutor
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG_DIR, "csrc")
 LIB_PATH = os.path.join(PKG_DIR, "libwsb200.so")
-SOURCES = ["wsb200.cu"]
-DEPS = ["wsb200.cu", "score_kernels.cuh", "score_short.cuh", "score_short16.cuh", "score_short16g.cuh", "score_long.cuh", "score_long16.cuh", "traceback_kernels.cuh", "traceback_fill16.cuh", "traceback_host.inl", "traceback_band.cuh", "traceback_band_host.inl",
-        os.path.join("..", "..", "include", "wsb200.h")]
-NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared"]
+# translation units and their extra flags: the packed int16 short-read kernels are built with ptxas -O1 (see wsb200_s16.cu)
+SOURCES = {"wsb200.cu": [], "wsb200_s16.cu": ["-Xptxas", "-O1"]}
+DEPS = ["wsb200.cu", "wsb200_s16.cu", "score_kernels.cuh", "score_short.cuh", "score_short16.cuh", "score_short16g.cuh",
+        "score_long.cuh", "score_long16.cuh", "traceback_kernels.cuh", "traceback_fill16.cuh", "traceback_host.inl",
+        "traceback_band.cuh", "traceback_band_host.inl", os.path.join("..", "..", "include", "wsb200.h")]
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC"]
 
 
 def needs_build() -> bool:
@@ -21,17 +23,27 @@ def needs_build() -> bool:
     return any(os.path.getmtime(os.path.join(CSRC, d)) > built for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if force or needs_build():
+def build(force: bool = False, verbose: bool = False, out: str | None = None) -> str:
+    out = out or LIB_PATH
+    if force or needs_build() or out != LIB_PATH:
         nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-        cmd = [nvcc, *NVCC_FLAGS, "-o", LIB_PATH, *[os.path.join(CSRC, s) for s in SOURCES]]
-        if verbose:
-            cmd.insert(1, "-Xptxas=-v")
         extra = os.environ.get("WSB_NVCC_EXTRA", "").split()   # tuning aid, e.g. -DWSB_TG_ONLY
-        cmd[1:1] = extra
-        subprocess.check_call(cmd, cwd=CSRC)
-    return LIB_PATH
+        objdir = os.path.join(PKG_DIR, "csrc", "_obj" + ("" if out == LIB_PATH else "_" + os.path.basename(out)))
+        os.makedirs(objdir, exist_ok=True)
+
+        def compile_one(item):
+            src, flags = item
+            obj = os.path.join(objdir, src.replace(".cu", ".o"))
+            cmd = [nvcc, *extra, *NVCC_FLAGS, *flags, *(["-Xptxas=-v"] if verbose else []), "-c", "-o", obj, os.path.join(CSRC, src)]
+            subprocess.check_call(cmd, cwd=CSRC)
+            return obj
+
+        with ThreadPoolExecutor(len(SOURCES)) as pool:
+            objs = list(pool.map(compile_one, SOURCES.items()))
+        subprocess.check_call([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, *objs], cwd=CSRC)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose=True))
+    import sys
+    print(build(force=True, verbose="-v" in sys.argv, out=sys.argv[sys.argv.index("-o") + 1] if "-o" in sys.argv else None))

@@ -59,6 +59,11 @@ struct ScoreParams {
     int64_t bnd_rows;
 };
 
+constexpr int kShort16MaxM = 154;    // longest query the packed int16 short-read kernels take (score_short16*.cuh)
+
+using KernelFn = void (*)(const ScoreParams);
+struct KernelSel { KernelFn fn; size_t smem; };   // a kernel instantiation and the dynamic shared memory it needs
+
 // ---------------------------------------------------------------- arithmetic policies
 // int32 with the substitution score looked up by one IDP.4A: the subject symbol is kept as a profile word (delta =
 // match - mismatch in the byte of its code, 0 elsewhere or everywhere for flagged / pad symbols), the query symbol as a

@@ -46,7 +46,6 @@
 
 namespace wsb {
 
-constexpr int kShort16MaxM = 154;    // longest query the kernel takes
 template <int P> __host__ __device__ constexpr int short16_qrows() { return (kShort16MaxM + 2 * P + 2 + 1) / 2 * 2; }   // + P pad rows above, P + 2 below
 constexpr int kShort16Raw = 192;     // bytes of one staged sequence window (16-byte aligned start, up to 177 symbols)
 constexpr int kShort16MaxLen = kShort16Raw - 15;

@@ -4,8 +4,6 @@
 #include "../../include/wsb200.h"
 #include "score_kernels.cuh"
 #include "score_short.cuh"
-#include "score_short16.cuh"
-#include "score_short16g.cuh"
 #include "score_long.cuh"
 #include "score_long16.cuh"
 #include "traceback_kernels.cuh"
@@ -704,8 +702,6 @@ static int best_shape(const Shape* shapes, int count, int table_size, int m, int
     return best;
 }
 
-using KernelFn = void (*)(const ScoreParams);
-struct KernelSel { KernelFn fn; size_t smem; };
 
 template <class AR, int P, int K, int GAP> static KernelSel pick_atype(int atype, bool masked) {
     switch (atype) {
@@ -745,28 +741,11 @@ static LongFn pick_long(int atype, int gap, bool cluster) {
     return nullptr;
 }
 
-// alpha / gamma = min(alpha, beta): the schemes of the reference's benchmarks (affine 2/1, linear 1) get instantiations
-// with the gap costs as immediates
-template <int P, int K, int MINB = 4> static KernelSel pick_short16(int gap, int alpha, int gamma) {
-    if (gap == GAP_LINEAR) {
-        if (alpha == 1) return {s16_local_short_kernel<P, K, GAP_LINEAR, MINB, 1, 1>, short16_smem_bytes<P, K>()};
-        return {s16_local_short_kernel<P, K, GAP_LINEAR, MINB>, short16_smem_bytes<P, K>()};
-    }
-    if (alpha == 2 && gamma == 1) return {s16_local_short_kernel<P, K, GAP_MERGED, MINB, 2, 1>, short16_smem_bytes<P, K>()};
-    return {s16_local_short_kernel<P, K, GAP_MERGED, MINB>, short16_smem_bytes<P, K>()};
-}
-
-// global alignment of short reads (score_short16g.cuh); ragged = units of unequal pairs (row m is captured in every trip)
-template <int P, int K> static KernelSel pick_short16g(int gap, int alpha, int gamma, bool ragged) {
-    const size_t smem = short16g_smem_bytes<P, K>();
-    if (gap == GAP_LINEAR) {
-        if (ragged) return {s16_global_short_kernel<P, K, GAP_LINEAR, true>, smem};
-        if (alpha == 1) return {s16_global_short_kernel<P, K, GAP_LINEAR, false, 1, 1>, smem};
-        return {s16_global_short_kernel<P, K, GAP_LINEAR, false>, smem};
-    }
-    if (ragged) return {s16_global_short_kernel<P, K, GAP_MERGED, true>, smem};
-    if (alpha == 2 && gamma == 1) return {s16_global_short_kernel<P, K, GAP_MERGED, false, 2, 1>, smem};
-    return {s16_global_short_kernel<P, K, GAP_MERGED, false>, smem};
+// The packed int16 short-read kernels live in their own translation unit (wsb200_s16.cu, built with -Xptxas -O1: ptxas'
+// default scheduling costs those two kernels 3-4 %, every other kernel is at its best with the default).
+namespace wsb {
+KernelSel pick_short16_local(int shape, int gap, int alpha, int gamma);
+KernelSel pick_short16_global(int shape, int gap, int alpha, int gamma, bool ragged);
 }
 
 template <int GAP> static LongFn pick_long16_atype(int atype) {
@@ -787,10 +766,10 @@ static KernelSel pick_kernel(int variant, int shape, int atype, int gap, bool ma
                              int alpha = 0, int gamma = 0, bool ragged = true) {
     static const char* no_short = getenv("WSB_NO_SHORT");  // tuning aid: force the general kernel
     if (variant == WSB_VARIANT_S16X2 && atype == AT_GLOBAL) {
-        return shape == 0 ? pick_short16g<8, 16>(gap, alpha, gamma, ragged) : pick_short16g<8, 19>(gap, alpha, gamma, ragged);
+        return pick_short16_global(shape, gap, alpha, gamma, ragged);
     }
     if (variant == WSB_VARIANT_S16X2) {
-        return shape == 0 ? pick_short16<8, 16>(gap, alpha, gamma) : pick_short16<8, 19>(gap, alpha, gamma);
+        return pick_short16_local(shape, gap, alpha, gamma);
     }
     if (variant == WSB_VARIANT_F16X2 && atype == AT_LOCAL && short_ok && !(no_short && no_short[0])) {
         switch (shape) {

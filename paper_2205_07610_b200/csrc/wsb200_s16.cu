@@ -1,0 +1,42 @@
+// wsb200_s16.cu -- the packed int16 short-read kernels (score_short16.cuh: local, score_short16g.cuh: global) in their own
+// translation unit, compiled with -Xptxas -O1.  Their loops are hand-scheduled straight-line code whose strip state is
+// updated in place; ptxas' default optimisation level reorders them and pays with register moves and earlier stalls
+// (1 M x 150 bp on a B200: local affine 5.24 -> 5.38 TCUPS, global linear 8.11 -> 8.45 at -O1), while every other kernel
+// of the library is faster at the default level (half2 short kernel -13 %, long-read kernel -14 % at -O1).
+#include "score_short16.cuh"
+#include "score_short16g.cuh"
+
+namespace wsb {
+
+// alpha / gamma = min(alpha, beta): the schemes of the reference's benchmarks (affine 2/1, linear 1) get instantiations
+// with the gap costs as immediates
+template <int P, int K, int MINB = 4> static KernelSel pick_local(int gap, int alpha, int gamma) {
+    if (gap == GAP_LINEAR) {
+        if (alpha == 1) return {s16_local_short_kernel<P, K, GAP_LINEAR, MINB, 1, 1>, short16_smem_bytes<P, K>()};
+        return {s16_local_short_kernel<P, K, GAP_LINEAR, MINB>, short16_smem_bytes<P, K>()};
+    }
+    if (alpha == 2 && gamma == 1) return {s16_local_short_kernel<P, K, GAP_MERGED, MINB, 2, 1>, short16_smem_bytes<P, K>()};
+    return {s16_local_short_kernel<P, K, GAP_MERGED, MINB>, short16_smem_bytes<P, K>()};
+}
+
+// global alignment; ragged = units of unequal pairs or reads shorter than two lane groups (row m is captured in every trip)
+template <int P, int K> static KernelSel pick_global(int gap, int alpha, int gamma, bool ragged) {
+    const size_t smem = short16g_smem_bytes<P, K>();
+    if (gap == GAP_LINEAR) {
+        if (ragged) return {s16_global_short_kernel<P, K, GAP_LINEAR, true>, smem};
+        if (alpha == 1) return {s16_global_short_kernel<P, K, GAP_LINEAR, false, 1, 1>, smem};
+        return {s16_global_short_kernel<P, K, GAP_LINEAR, false>, smem};
+    }
+    if (ragged) return {s16_global_short_kernel<P, K, GAP_MERGED, true>, smem};
+    if (alpha == 2 && gamma == 1) return {s16_global_short_kernel<P, K, GAP_MERGED, false, 2, 1>, smem};
+    return {s16_global_short_kernel<P, K, GAP_MERGED, false>, smem};
+}
+
+KernelSel pick_short16_local(int shape, int gap, int alpha, int gamma) {
+    return shape == 0 ? pick_local<8, 16>(gap, alpha, gamma) : pick_local<8, 19>(gap, alpha, gamma);
+}
+KernelSel pick_short16_global(int shape, int gap, int alpha, int gamma, bool ragged) {
+    return shape == 0 ? pick_global<8, 16>(gap, alpha, gamma, ragged) : pick_global<8, 19>(gap, alpha, gamma, ragged);
+}
+
+}  // namespace wsb

@@ -5,7 +5,6 @@ cd "$(dirname "$0")/.." || exit 1
 mkdir -p build
 for spec in "$@"; do
   name="${spec%%=*}"; flags="${spec#*=}"
-  ( /usr/local/cuda/bin/nvcc $flags -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared \
-      -o build/lib_$name.so paper_2205_07610_b200/csrc/wsb200.cu 2> build/lib_$name.log && echo "built $name" || echo "FAILED $name" ) &
+  ( WSB_NVCC_EXTRA="$flags" python -m paper_2205_07610_b200.build -o "$PWD/build/lib_$name.so" > build/lib_$name.log 2>&1 && echo "built $name" || echo "FAILED $name" ) &
 done
 wait
