@@ -82,6 +82,23 @@ __device__ __forceinline__ unsigned pick_reg(const unsigned (&a)[K], int idx) {
     return v[0];
 }
 
+// a[idx] with an index that is the same in every lane of the warp (uniform batches: column n sits in the same register of
+// every lane group): a jump table instead of a select tree
+template <int K>
+__device__ __forceinline__ unsigned pick_reg_uniform(const unsigned (&a)[K], int idx) {
+    unsigned v = a[K - 1];
+    switch (idx) {
+#define WSB_PICK(i) case i: if (i < K) v = a[i < K ? i : 0]; break;
+        WSB_PICK(0) WSB_PICK(1) WSB_PICK(2) WSB_PICK(3) WSB_PICK(4) WSB_PICK(5) WSB_PICK(6) WSB_PICK(7)
+        WSB_PICK(8) WSB_PICK(9) WSB_PICK(10) WSB_PICK(11) WSB_PICK(12) WSB_PICK(13) WSB_PICK(14) WSB_PICK(15)
+        WSB_PICK(16) WSB_PICK(17) WSB_PICK(18) WSB_PICK(19) WSB_PICK(20) WSB_PICK(21) WSB_PICK(22) WSB_PICK(23)
+        WSB_PICK(24) WSB_PICK(25) WSB_PICK(26) WSB_PICK(27) WSB_PICK(28) WSB_PICK(29) WSB_PICK(30) WSB_PICK(31)
+#undef WSB_PICK
+        default: break;
+    }
+    return v;
+}
+
 template <bool ON_ALU>
 __device__ __forceinline__ unsigned max_mark2(unsigned a, unsigned b, uint32_t& wlo, uint32_t& whi, uint32_t bit, int one) {
     unsigned r;
@@ -183,6 +200,11 @@ __global__ void __launch_bounds__(kThreads, K <= 16 ? 4 : 1) tb_fill16_kernel(co
         const bool has_cap_a = cap_a >= 0 && cap_a < K, has_cap_b = cap_b >= 0 && cap_b < K;
         int bv_a = GLOBAL_EDGES ? kNeg32 : 0, bi_a = 0, bj_a = ATYPE == AT_SEMI ? n_a : 0;
         int bv_b = bv_a, bi_b = 0, bj_b = ATYPE == AT_SEMI ? n_b : 0;
+        // uniform semiglobal batches: the last matrix column is followed in packed form (both halves at once, biased
+        // H - alpha values; the earliest row keeps ties), one VIMNMX.S16x2 + two selects per row
+        const int cap_u = (n_a - 1) % K;
+        unsigned col_best = pk16b(0 - alpha);   // H(0, n) = 0
+        int col_i_a = 0, col_i_b = 0;
 
         // row m of a half: semiglobal scans it, global reads H(m, n)
         auto last_row = [&](bool second, int m, int n, bool has_cap, int cap_rel, int& bv, int& bi, int& bj) {
@@ -261,7 +283,20 @@ __global__ void __launch_bounds__(kThreads, K <= 16 ? 4 : 1) tb_fill16_kernel(co
                 }
                 out_al = al;
                 out_fp = fl;
-                if (ATYPE == AT_SEMI) {   // last matrix column, rows above the last one
+                if (ATYPE == AT_SEMI && !RAGGED) {   // last matrix column, rows above the last one (only the owner lane's result counts)
+                    const unsigned hv = r < mm ? pick_reg<K>(AL, cap_u) : col_best;
+                    unsigned nb;
+                    asm("{\n\t.reg .pred pl, ph;\n\t.reg .s16 r0, r1, a0, a1;\n\t"
+                        "max.s16x2 %0, %3, %4;\n\t"
+                        "mov.b32 {r0, r1}, %0;\n\t"
+                        "mov.b32 {a0, a1}, %3;\n\t"
+                        "setp.eq.s16 pl, r0, a0;\n\t"
+                        "setp.eq.s16 ph, r1, a1;\n\t"
+                        "@!pl mov.b32 %1, %5;\n\t"
+                        "@!ph mov.b32 %2, %5;\n\t"
+                        "}" : "=&r"(nb), "+r"(col_i_a), "+r"(col_i_b) : "r"(col_best), "r"(hv), "r"(r));
+                    col_best = nb;
+                } else if (ATYPE == AT_SEMI) {
                     if (has_cap_a && r < m_a) {
                         const int v = lo16(pick_reg<K>(AL, cap_a)) + alpha;
                         if (better_cell(v, r, n_a, bv_a, bi_a, bj_a)) { bv_a = v; bi_a = r; bj_a = n_a; }
@@ -289,6 +324,10 @@ __global__ void __launch_bounds__(kThreads, K <= 16 ? 4 : 1) tb_fill16_kernel(co
         }
         // every lane's registers now hold row max(m) of its strip
         if (LOCAL) { __syncwarp(); continue; }
+        if (ATYPE == AT_SEMI && !RAGGED) {
+            if (has_cap_a) { const int v = lo16(col_best) + alpha; if (better_cell(v, col_i_a, n_a, bv_a, bi_a, bj_a)) { bv_a = v; bi_a = col_i_a; bj_a = n_a; } }
+            if (has_cap_b) { const int v = hi16(col_best) + alpha; if (better_cell(v, col_i_b, n_b, bv_b, bi_b, bj_b)) { bv_b = v; bi_b = col_i_b; bj_b = n_b; } }
+        }
         if (m_a == mm && m_a > 0) last_row(false, m_a, n_a, has_cap_a, cap_a, bv_a, bi_a, bj_a);
         if (m_b == mm && m_b > 0) last_row(true, m_b, n_b, has_cap_b, cap_b, bv_b, bi_b, bj_b);
         const unsigned gmask = group_mask<P>(tid & 31);

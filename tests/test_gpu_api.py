@@ -271,3 +271,33 @@ def test_sharded_reads_matrix_takes_the_metadata_free_path_per_shard(monkeypatch
         assert len(two.shard_cells) == 2 and sum(two.shard_cells) == n * L * L
     for c in made:
         c.close()
+
+
+def test_selftest_draws_the_reference_cases_and_agrees_with_the_oracle():
+    """selftest() mirrors cli.cmd_selftest (cli.py:264-301): same random cases per seed, AUTO kernels vs the int32 kernel on
+    the GPU, here with the CPU oracle as a third voice; a planted wrong answer must come back as a JSON-able repro blob."""
+    import json
+    import oracle
+    from helpers import make_pool
+    import paper_2205_07610_b200 as W
+
+    def checker(queries, subjects, scheme, align_type):
+        qc, qo, ql = make_pool([np.where(q.flags, 4, q.codes).astype(np.uint8) for q in queries])
+        sc, so, sl = make_pool([np.where(s.flags, 4, s.codes).astype(np.uint8) for s in subjects])
+        idx = np.arange(len(queries), dtype=np.int32)
+        return oracle.score_batch(qc, qo, ql, sc, so, sl, idx, idx, align_type, scheme.gap_model == "affine",
+                                  scheme.match_score, scheme.mismatch_score, scheme.gap_open, scheme.gap_extend)
+
+    rep = W.selftest(cases=600, seed=11, checker=checker)
+    assert rep == {"ok": True, "cases": 600, "failure": None}
+
+    def liar(queries, subjects, scheme, align_type):
+        sc, ei, ej = (np.array(a) for a in checker(queries, subjects, scheme, align_type))
+        sc[-1] += 1
+        return sc, ei, ej
+
+    rep = W.selftest(cases=40, seed=3, checker=liar)
+    assert not rep["ok"]
+    blob = json.loads(json.dumps(rep["failure"]))
+    assert set(blob) >= {"case", "seed", "query", "subject", "align_type", "gap_model", "scheme", "engine", "reference"}
+    assert blob["reference"][0] == blob["engine"][0] + 1 and set(blob["query"]) <= set("ACGT")
