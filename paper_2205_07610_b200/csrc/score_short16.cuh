@@ -358,8 +358,12 @@ __global__ void __launch_bounds__(kThreads, MINB) s16_local_short_kernel(const S
                 receive();
                 unsigned la = ta_l, lg = tg_l, rm, h_last, t_last;
                 row(qc0, qc1, qn0, qn1, h_d, la, lg, rm, h_last, t_last);
-                asm volatile("ld.shared.v2.b32 {%0, %1}, [%2+8];" : "=r"(qc0), "=r"(qc1) : "r"(qaddr) : "memory");
-                asm volatile("ld.shared.v2.b32 {%0, %1}, [%2+16];" : "=r"(qn0), "=r"(qn1) : "r"(qaddr) : "memory");
+                // The address register is bumped BEFORE the loads that read it: bumped behind them (at the loop end) the add
+                // has to wait until the loads, queued in the memory pipe behind other warps' stores, have read the register
+                // -- 14 % of all stall samples of the kernel sat on that add (profiles/r02_ncu_s16_local_short_before.md).
+                qaddr += 8;
+                asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(qc0), "=r"(qc1) : "r"(qaddr) : "memory");
+                asm volatile("ld.shared.v2.b32 {%0, %1}, [%2+8];" : "=r"(qn0), "=r"(qn1) : "r"(qaddr) : "memory");
 #ifdef WSB_S16_SEND_FIRST
                 send(t_last, h_last);
 #endif
@@ -378,7 +382,6 @@ __global__ void __launch_bounds__(kThreads, MINB) s16_local_short_kernel(const S
 #ifndef WSB_S16_SEND_FIRST
                 send(t_last, h_last);
 #endif
-                qaddr += 8;
             }
         }
 
@@ -390,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, MINB) s16_local_short_kernel(const S
             if (bv > 0) {  // the tag word after the K columns holds the query-buffer address of the record row
                 const uint4 w = snap[v][K / 4][tid];
                 const unsigned tag = (K % 4 == 0) ? w.x : (K % 4 == 1) ? w.y : (K % 4 == 2) ? w.z : w.w;
-                bi = (int)((tag - qbase) >> 3) - P + 1;  // buffer index -> matrix row
+                bi = (int)((tag - qbase) >> 3) - P;      // the tag is the buffer address of the row AFTER the recorded one
                 if (bi > m[v] || bi < 1) bv = 0;       // cannot happen for a real record; keeps pads out defensively
             }
 #pragma unroll
