@@ -266,6 +266,9 @@ def main():
     ap.add_argument("--host-format", default="bytes", choices=["bytes", "packed2"],
                     help="e2e leg: host pools as one byte per symbol, or in the reference's 2-bit Sequence.data layout")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard-api", type=int, default=0,
+                    help="also time ONE process calling run_batch(devices=[0..N-1]) (the product's own multi-GPU path; devices wrap "
+                         "around the GPUs present, so N > 1 works on a one-GPU box and then measures the sharding overhead)")
     args = ap.parse_args()
     cfg = dict(WORKLOADS[args.workload])
     if args.pairs:
@@ -336,7 +339,8 @@ def main():
     total_cells = dist_sum(float(cells), world) * args.steps   # weak: every rank its own batch; strong (cfg5): the shards add up to the one batch
     value = total_cells / args.steps / (median_ms * 1e-3) / 1e9   # the reference's statistic: median step, not the mean
     value_mean = total_cells / (total_ms * 1e-3) / 1e9
-    kernel_cycles = 0 if traceback else batch.kernel_cycles      # SM cycles of the last headline-kernel launch (0: another kernel)
+    # SM cycles of the last packed int16 short-read launch: only where that kernel IS the step (cfg1 / cfg2 under AUTO)
+    kernel_cycles = batch.kernel_cycles if (args.workload in ("cfg1", "cfg2") and variant == "auto" and not traceback) else 0
     launches = int(dist_sum(float(launches), world))
 
     # end to end through the public API: host buffers in, host results out, every step
@@ -364,6 +368,21 @@ def main():
         _ = int(rep.results.score[0]) if isinstance(rep.results, W.ResultArray) else rep.results[0].score
     e2e_time = dist_max(time.perf_counter() - t0, world)
     e2e_value = total_cells / args.steps * e2e_steps / e2e_time / 1e9
+
+    sharded = None
+    if args.shard_api > 0 and world == 1:   # the product's own sharding: one process, one host thread + context + stream per shard
+        devs = [d % ndev for d in range(args.shard_api)]
+        job_s = W.BatchJob(host_q, host_s, pair_arr, job.cfg, scheme, tuning=job.tuning, devices=devs)
+        W.run_batch(job_s); W.run_batch(job_s)
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            rep_s = W.run_batch(job_s)
+            _ = int(rep_s.results.score[0]) if isinstance(rep_s.results, W.ResultArray) else rep_s.results[0].score
+        dt = time.perf_counter() - t0
+        same = bool(np.array_equal(np.asarray(rep_s.results.score), np.asarray(rep.results.score))) if isinstance(rep.results, W.ResultArray) else None
+        sharded = {"value": cells * e2e_steps / dt / 1e9, "unit": "GCUPS", "shards": args.shard_api, "devices": sorted(set(devs)),
+                   "h2d_bytes_per_step": int(rep_s.h2d_bytes), "d2h_bytes_per_step": int(rep_s.d2h_bytes),
+                   "scores_equal_single_device": same}
 
     # roofline: ALU-issue bound of the dominant kernel
     peaks = measured_peaks()
@@ -405,6 +424,8 @@ def main():
                 "e2e": {"value": e2e_value, "unit": "GCUPS", "h2d_bytes_per_step": int(rep.h2d_bytes) * world,
                         "d2h_bytes_per_step": int(rep.d2h_bytes) * world, "steps": e2e_steps},
                 "gpu_launches": launches, "clocks": clocks, "wall_s_timed_region": wall}
+        if sharded:
+            line["e2e_shard_api"] = sharded
         if not args.no_cpu_baseline and world == 1:   # the CPU baseline is timed on rank 0 at N = 1 only
             rate, threads, pairs, dt = cpu_sample(cfg)
             line["cpu_baseline"] = {"value": rate, "unit": "GCUPS", "cores": threads, "kind": "port",
