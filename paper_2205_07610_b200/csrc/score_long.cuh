@@ -62,6 +62,8 @@ __device__ __forceinline__ int fma_add(int a, int one, int b) {
     return d;
 }
 
+using LongFn = void (*)(const LongParams);
+
 template <int ATYPE, int GAP, bool CLUSTER = false>
 __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long_kernel(const LongParams prm) {
     constexpr int K = kLongK, W = kLongW;

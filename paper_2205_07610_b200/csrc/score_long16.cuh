@@ -147,16 +147,25 @@ __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long16_kernel(const 
                 const int r = it - t;
                 unsigned out_tg = tg_l, out_h = h_l;
                 if (!CHECK || (unsigned)(r - 1) < (unsigned)m) {
-                    unsigned hd = hdiag;
                     unsigned la = MERGED ? __vadd2(tg_l, c_gma) : __vadd2(h_l, c_nalpha);
                     unsigned lg = tg_l;
                     unsigned rm = 0u, hprev = 0u;
+                    // the diagonal candidate runs one column ahead of the cell: it reads H(r - 1, c) BEFORE the cell of column c
+                    // overwrites that register with H(r, c), so H[] is updated in place (no register rotation at the loop end)
+                    unsigned dn;
+                    {
+                        unsigned sg;
+                        asm("prmt.b32 %0, %1, %2, %3;" : "=r"(sg) : "r"(rwA), "r"(rwB), "r"(sel[0]));
+                        dn = __vadd2(hdiag, sg);
+                    }
 #pragma unroll
                     for (int c = 0; c < K; ++c) {
-                        unsigned sg;
-                        asm("prmt.b32 %0, %1, %2, %3;" : "=r"(sg) : "r"(rwA), "r"(rwB), "r"(sel[c]));
-                        const unsigned d = __vadd2(hd, sg);
-                        hd = H[c];
+                        const unsigned d = dn;
+                        if (c + 1 < K) {
+                            unsigned sg;
+                            asm("prmt.b32 %0, %1, %2, %3;" : "=r"(sg) : "r"(rwA), "r"(rwB), "r"(sel[c + 1]));
+                            dn = __vadd2(H[c], sg);
+                        }
                         const unsigned h = LOCAL ? __vimax3_s16x2_relu(TA[c], la, d) : __vimax3_s16x2(TA[c], la, d);
                         if (MERGED) {
                             const unsigned tn = LOCAL ? __vimax3_s16x2_relu(TG[c], lg, d) : __vimax3_s16x2(TG[c], lg, d);

@@ -5,7 +5,6 @@
 #include "score_kernels.cuh"
 #include "score_short.cuh"
 #include "score_long.cuh"
-#include "score_long16.cuh"
 #include "traceback_kernels.cuh"
 
 #include <cuda_runtime.h>
@@ -727,7 +726,6 @@ template <int P, int K> static KernelSel pick_short(int gap) {
     return {f16_local_short_kernel<P, K, GAP_MERGED>, short_smem_bytes<P, K>()};
 }
 
-using LongFn = void (*)(const LongParams);
 template <int GAP, bool CLUSTER> static LongFn pick_long_atype(int atype) {
     switch (atype) {
         case AT_GLOBAL: return score_long_kernel<AT_GLOBAL, GAP, CLUSTER>;
@@ -748,18 +746,7 @@ KernelSel pick_short16_local(int shape, int gap, int alpha, int gamma);
 KernelSel pick_short16_global(int shape, int gap, int alpha, int gamma, bool ragged);
 }
 
-template <int GAP> static LongFn pick_long16_atype(int atype) {
-    switch (atype) {
-        case AT_GLOBAL: return score_long16_kernel<AT_GLOBAL, GAP>;
-        case AT_LOCAL: return score_long16_kernel<AT_LOCAL, GAP>;
-        default: return score_long16_kernel<AT_SEMI, GAP>;
-    }
-}
-static LongFn pick_long16(int atype, int gap) {
-    if (gap == GAP_LINEAR) return pick_long16_atype<GAP_LINEAR>(atype);
-    if (gap == GAP_MERGED) return pick_long16_atype<GAP_MERGED>(atype);
-    return nullptr;
-}
+namespace wsb { LongFn pick_long16(int atype, int gap); }   // score_long16.cuh, compiled in wsb200_s16.cu
 
 // short_ok: every unit of the launch fits one stage and the short kernel's query buffer
 static KernelSel pick_kernel(int variant, int shape, int atype, int gap, bool masked, bool short_ok, bool wide,

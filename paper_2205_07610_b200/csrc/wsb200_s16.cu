@@ -1,10 +1,12 @@
-// wsb200_s16.cu -- the packed int16 short-read kernels (score_short16.cuh: local, score_short16g.cuh: global) in their own
-// translation unit, compiled with -Xptxas -O1.  Their loops are hand-scheduled straight-line code whose strip state is
+// wsb200_s16.cu -- the packed int16 kernels (score_short16.cuh: short local reads, score_short16g.cuh: short global reads,
+// score_long16.cuh: long reads, two pairs per block) in their own translation unit, compiled with -Xptxas -O1.  Their loops are hand-scheduled straight-line code whose strip state is
 // updated in place; ptxas' default optimisation level reorders them and pays with register moves and earlier stalls
 // (1 M x 150 bp on a B200: local affine 5.24 -> 5.38 TCUPS, global linear 8.11 -> 8.45 at -O1), while every other kernel
-// of the library is faster at the default level (half2 short kernel -13 %, long-read kernel -14 % at -O1).
+// of the library is faster at the default level (half2 short kernel -13 %, int32 long-read kernel -14 % at -O1).  The packed
+// long-read kernel's row loop shrinks from 162 to 151 instructions at -O1.
 #include "score_short16.cuh"
 #include "score_short16g.cuh"
+#include "score_long16.cuh"
 
 namespace wsb {
 
@@ -37,6 +39,19 @@ KernelSel pick_short16_local(int shape, int gap, int alpha, int gamma) {
 }
 KernelSel pick_short16_global(int shape, int gap, int alpha, int gamma, bool ragged) {
     return shape == 0 ? pick_global<8, 16>(gap, alpha, gamma, ragged) : pick_global<8, 19>(gap, alpha, gamma, ragged);
+}
+
+template <int GAP> static LongFn pick_long16_atype(int atype) {
+    switch (atype) {
+        case AT_GLOBAL: return score_long16_kernel<AT_GLOBAL, GAP>;
+        case AT_LOCAL: return score_long16_kernel<AT_LOCAL, GAP>;
+        default: return score_long16_kernel<AT_SEMI, GAP>;
+    }
+}
+LongFn pick_long16(int atype, int gap) {
+    if (gap == GAP_LINEAR) return pick_long16_atype<GAP_LINEAR>(atype);
+    if (gap == GAP_MERGED) return pick_long16_atype<GAP_MERGED>(atype);
+    return nullptr;
 }
 
 }  // namespace wsb
