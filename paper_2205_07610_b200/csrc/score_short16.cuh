@@ -114,6 +114,45 @@ __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
 
+// PRMT selectors of a strip of K columns for the two alignments of a unit, four columns at a time: the subject bytes come
+// in as aligned 32-bit words of the staged windows (funnel-shifted to the strip's first column), every byte x < 4 becomes
+// the selector byte x' * 0x11 + 0x80 (low nibble: value byte x' of the row words, high nibble: its sign fill; x' = x for
+// the first alignment, x + 4 for the second) with ONE multiply-add per word; columns beyond the subject get 0x88 (sign
+// fill of byte 0 in both nibbles: sigma in {0, -1}, never improving).  Returns true when a column inside a subject holds a
+// flagged symbol (no selector encoding).  ~150 instructions per strip where the byte-by-byte form took ~520, most of them
+// waiting for one-byte shared-memory loads.
+template <int K>
+__device__ __forceinline__ bool build_selectors16(const uint8_t* win_a, const uint8_t* win_b, int pos_a, int pos_b, int left_a,
+                                                  int left_b, unsigned (&sel)[K]) {
+    constexpr int NWD = (K + 3) / 4;
+    unsigned nibs[2][NWD];
+    unsigned fl = 0u;
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+        const uint8_t* win = v ? win_b : win_a;
+        const int pos = v ? pos_b : pos_a, left = v ? left_b : left_a;   // window byte of the strip's first column; columns left in the subject
+        const unsigned* words = reinterpret_cast<const unsigned*>(win) + (pos >> 2);
+        const unsigned sh = 8u * (unsigned)(pos & 3);
+        unsigned w[NWD + 1];
+#pragma unroll
+        for (int k = 0; k <= NWD; ++k) w[k] = words[k];
+#pragma unroll
+        for (int k = 0; k < NWD; ++k) {
+            const unsigned x = __funnelshift_r(w[k], w[k + 1], sh);
+            const int valid = min(max(left - 4 * k, 0), 4);
+            const unsigned mask = valid >= 4 ? 0xffffffffu : ((1u << (8 * valid)) - 1u);
+            fl |= x & mask;
+            const unsigned xm = x & mask & 0x03030303u;
+            const unsigned base = 0x80808080u | (~mask & 0x08080808u) | (v ? (mask & 0x04040404u) * 0x11u : 0u);
+            nibs[v][k] = xm * 0x11u + base;
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < K; ++c)   // byte c of either word; the consumer PRMT reads the low 16 bits only
+        sel[c] = __byte_perm(nibs[0][c >> 2], nibs[1][c >> 2], (unsigned)(c & 3) | ((4u + (unsigned)(c & 3)) << 4));
+    return (fl & 0xfcfcfcfcu) != 0u;
+}
+
 // AIMM / GIMM > 0: gap costs alpha / gamma baked into the instruction stream as immediates (the host picks such an
 // instantiation when the scheme matches): a VIADD.16x2 with an immediate reads one register instead of two, which the
 // cell-stream microbenchmark (tools/ubench/cell_bench.cu) shows is worth ~6 % of issue rate at four warps per scheduler.
@@ -244,18 +283,10 @@ __global__ void __launch_bounds__(kThreads, MINB) s16_local_short_kernel(const S
         // D = diagonal candidate of the NEXT row (H of the column to the left + sigma of the next row's symbol)
         unsigned sel[K], TA[GAP == GAP_MERGED ? K : NW], TG[GAP == GAP_MERGED ? NW : 1], D[K];   // the snapshot source holds whole quads
         D[0] = 0u;
-        bool flagged_subject = false;
+        const bool flagged_subject = build_selectors16<K>(raw[gib][1], raw[gib][3], ssh[0] + col0, ssh[1] + col0, n[0] - col0,
+                                                          n[1] - col0, sel);
 #pragma unroll
         for (int c = 0; c < K; ++c) {
-            unsigned nib[2] = {0x88u, 0x88u};   // pad column: sign fill of byte 0 in both bytes -> sigma in {0, -1}
-#pragma unroll
-            for (int v = 0; v < 2; ++v)
-                if (col0 + c < n[v]) {
-                    const unsigned x = raw[gib][2 * v + 1][ssh[v] + col0 + c];
-                    if (x < 4) nib[v] = (x + 4u * v) | ((x + 4u * v) | 8u) << 4;   // value byte, then its sign byte
-                    else flagged_subject = true;
-                }
-            sel[c] = nib[0] | (nib[1] << 8);
             TA[c] = c_nalpha;
             if (GAP == GAP_MERGED) TG[c] = c_ngamma;
         }

@@ -185,18 +185,10 @@ __global__ void __launch_bounds__(kThreads, 4) s16_global_short_kernel(const Sco
         // strip state at row 0: T(0, j) = H(0, j) = edge; D[c] = H(0, c - 1) + sigma(row 1, c)
         unsigned sel[K], TA[K], TG[MERGED ? K : 1], D[K];
         D[0] = 0u;
-        bool flagged_subject = false;
+        const bool flagged_subject = build_selectors16<K>(raw[gib][1], raw[gib][3], ssh[0] + col0, ssh[1] + col0, n[0] - col0,
+                                                          n[1] - col0, sel);
 #pragma unroll
         for (int c = 0; c < K; ++c) {
-            unsigned nib[2] = {0x88u, 0x88u};
-#pragma unroll
-            for (int v = 0; v < 2; ++v)
-                if (col0 + c < n[v]) {
-                    const unsigned x = raw[gib][2 * v + 1][ssh[v] + col0 + c];
-                    if (x < 4) nib[v] = (x + 4u * v) | ((x + 4u * v) | 8u) << 4;
-                    else flagged_subject = true;
-                }
-            sel[c] = nib[0] | (nib[1] << 8);
             const int e = edge_h(true, col0 + c + 1, prm.alpha, beta);
             TA[c] = pack16(e - alpha);
             if (MERGED) TG[c] = pack16(e - gamma);
