@@ -138,6 +138,11 @@ __global__ void __launch_bounds__(kThreads, K <= 16 ? 4 : 1) tb_fill16_kernel(co
     constexpr bool LOCAL = ATYPE == AT_LOCAL;   // end cells come from the score pass; H == 0 is stored as a stop code
     static_assert(K % 8 == 0, "K must pack into whole code words");
 
+    // code words of four iterations per lane and half, read back by the thread that wrote them (no synchronisation); one
+    // vector per (half, iteration, thread) keeps the 8- / 16-byte accesses of a warp contiguous
+    using StageVec = typename std::conditional<NW == 2, uint2, typename std::conditional<NW == 4, uint4, uint3>::type>::type;
+    static_assert(NW >= 2 && NW <= 4, "strip widths 16, 24, 32");
+    __shared__ StageVec stage[2][4][kThreads];
     const int tid = threadIdx.x;
     const int t = tid & (P - 1);
     const int gib = tid / P;
@@ -181,6 +186,7 @@ __global__ void __launch_bounds__(kThreads, K <= 16 ? 4 : 1) tb_fill16_kernel(co
         uint32_t* code_a = prm.codes + ((!RAGGED || keep_a) ? prm.code_off[ua] : 0);
         uint32_t* code_b = prm.codes + ((!RAGGED || keep_b) ? prm.code_off[ub] : 0);
         const int col0 = t * K;
+        const int rows4_a = tb_rows4(m_a, P), rows4_b = tb_rows4(m_b, P);
 
         unsigned ss[K], AL[K], EP[AFFINE ? K : 1];
 #pragma unroll
@@ -267,19 +273,17 @@ __global__ void __launch_bounds__(kThreads, K <= 16 ? 4 : 1) tb_fill16_kernel(co
                     wa[w8] = (wd_a | wm_a) | (we_a | wf_a);
                     wb[w8] = (wd_b | wm_b) | (we_b | wf_b);
                 }
-                const int64_t at = ((int64_t)(it - 1) * P + t) * NW;   // wavefront-major, one stage
-                // equal-sized pairs: no guards -- an odd tail's second half and a group without a unit of its own recompute an
-                // existing alignment and store the same words to the same place
-                const bool st_a = !RAGGED || (keep_a && r <= m_a), st_b = !RAGGED || (keep_b && r <= m_b);
-                if (NW == 2) {
-                    if (st_a) *reinterpret_cast<uint2*>(code_a + at) = make_uint2(wa[0], wa[1]);
-                    if (st_b) *reinterpret_cast<uint2*>(code_b + at) = make_uint2(wb[0], wb[1]);
-                } else if (NW == 4) {
-                    if (st_a) *reinterpret_cast<uint4*>(code_a + at) = make_uint4(wa[0], wa[1], wa[2], wa[NW - 1]);
-                    if (st_b) *reinterpret_cast<uint4*>(code_b + at) = make_uint4(wb[0], wb[1], wb[2], wb[NW - 1]);
+                // lane-major layout (tb_code_index): the words of four consecutive iterations are parked in shared memory and
+                // leave as one granule (see the flush at the loop bottom)
+                if constexpr (NW == 2) {
+                    stage[0][(it - 1) & 3][tid] = make_uint2(wa[0], wa[1]);
+                    stage[1][(it - 1) & 3][tid] = make_uint2(wb[0], wb[1]);
+                } else if constexpr (NW == 4) {
+                    stage[0][(it - 1) & 3][tid] = make_uint4(wa[0], wa[1], wa[2], wa[NW - 1]);
+                    stage[1][(it - 1) & 3][tid] = make_uint4(wb[0], wb[1], wb[2], wb[NW - 1]);
                 } else {
-#pragma unroll
-                    for (int w8 = 0; w8 < NW; ++w8) { if (st_a) code_a[at + w8] = wa[w8]; if (st_b) code_b[at + w8] = wb[w8]; }
+                    stage[0][(it - 1) & 3][tid] = make_uint3(wa[0], wa[1], wa[NW - 1]);
+                    stage[1][(it - 1) & 3][tid] = make_uint3(wb[0], wb[1], wb[NW - 1]);
                 }
                 out_al = al;
                 out_fp = fl;
@@ -321,6 +325,30 @@ __global__ void __launch_bounds__(kThreads, K <= 16 ? 4 : 1) tb_fill16_kernel(co
             all = nal; fpl = nfp;
             if (r == 0) al_diag = al_top;
             q_cur = q_nxt; q_nxt = q_nn;
+            if (((it - 1) & 3) == 3 || it == it_end) {   // a granule of four iterations is complete (or the sweep ends)
+                const int g4 = (it - 1) & ~3;
+                // equal-sized pairs: no guards -- an odd tail's second half and a group without a unit of its own recompute an
+                // existing alignment and store the same words to the same place; rows outside the matrix leave stale words
+                // that no walk reads
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                    const bool keep = v ? keep_b : keep_a;
+                    const int rows4 = v ? rows4_b : rows4_a;
+                    if (RAGGED && (!keep || g4 >= rows4)) continue;
+                    uint32_t* dst = (v ? code_b : code_a) + ((int64_t)t * rows4 + g4) * NW;
+                    uint32_t g[4 * NW];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const StageVec sv = stage[v][k][tid];
+                        g[k * NW] = sv.x; g[k * NW + 1] = sv.y;
+                        if constexpr (NW >= 3) g[k * NW + 2] = sv.z;
+                        if constexpr (NW == 4) g[k * NW + 3] = reinterpret_cast<const uint4&>(sv).w;
+                    }
+#pragma unroll
+                    for (int x = 0; x < NW; ++x)
+                        reinterpret_cast<uint4*>(dst)[x] = make_uint4(g[4 * x], g[4 * x + 1], g[4 * x + 2], g[4 * x + 3]);
+                }
+            }
         }
         // every lane's registers now hold row max(m) of its strip
         if (LOCAL) { __syncwarp(); continue; }

@@ -256,6 +256,7 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
         prm.w_score = b->d_score; prm.w_i = b->d_i; prm.w_j = b->d_j;
         prm.n_runs = d_cnt; prm.run_off = d_chunk_off; prm.runs = nullptr;
         prm.tb_p = P; prm.tb_k = K; prm.one = 1; prm.run_tmp = d_run_tmp;
+        prm.lane_major = fill16 ? 1 : 0;
 
         if (by_piece) TB_TRY(cudaStreamWaitEvent(ctx->stream, b->piece_ev[piece], 0));
         TB_TRY(cudaEventRecord(e0, ctx->stream));

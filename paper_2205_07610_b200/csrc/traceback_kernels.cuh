@@ -47,13 +47,22 @@ struct TbParams {
     int32_t one;                                  // 1, opaque to the compiler (keeps plane-bit adds on the FMA pipe)
     uint32_t* run_tmp;                            // pass 1 parks up to kTbTmpRuns runs per pair here (reverse order), so
                                                   // that pass 2 is a copy for all but the most fragmented alignments
+    int32_t lane_major = 0;                       // code layout (tb_code_index): 1 = written by the packed int16 fill
 };
 
-// code block geometry shared by fill and walk
+// Code block geometry shared by fill and walk.  A pair's block holds, per stage, one K/8-word entry per (iteration, lane);
+// iteration it = i + t computes row i in lane t.  Two orders:
+//   wavefront-major (int32 fill, bounded-memory tiles): entry (it, t) at (it - 1) * P + t -- what a lane group writes per
+//     iteration is contiguous;
+//   lane-major (packed int16 fill): entry (it, t) at t * rows4 + (it - 1), rows4 = iterations rounded up to a multiple of 4
+//     -- four consecutive iterations of a lane share one 32-byte sector, so a walk that moves up or diagonally stays in a
+//     sector for four steps instead of touching a new one every step (the walk's first pass was 15 % of cfg3, bound by one
+//     DRAM sector per step); the fill collects four iterations per lane in shared memory and stores whole granules.
+__host__ __device__ inline int tb_rows4(int m, int P) { return (m + P - 1 + 3) & ~3; }
 __host__ __device__ inline int64_t tb_code_words(int m, int n, int P, int K) {
     const int W = P * K;
     const int stages = (n + W - 1) / W;
-    return (int64_t)stages * (m + P - 1) * P * (K / 8);
+    return (int64_t)stages * tb_rows4(m, P) * P * (K / 8);
 }
 
 // max(a, b) with "a wins ties", and the plane bit added to w when a wins: compare, select, predicated add
@@ -271,13 +280,15 @@ __global__ void __launch_bounds__(kThreads) tb_fill_kernel(const TbParams prm) {
 // code of cell (i, j), 1 <= i <= m, 1 <= j <= n, translated from the fill's bit planes to
 //   bits 1:0 origin of H (0 stop, 1 diagonal, 2 E, 3 F), bit 2 "E extends", bit 3 "F extends"
 template <bool LOCAL>
-__device__ __forceinline__ uint32_t tb_code_at(const uint32_t* code, int i, int j, int m, int P, int K) {
+__device__ __forceinline__ uint32_t tb_code_at(const uint32_t* code, int i, int j, int m, int P, int K, bool lane_major = false) {
     const int W = P * K;
     const int st = (j - 1) / W;
     const int col = (j - 1) - st * W;
     const int t = col / K, c = col - t * K;
     const int it = i + t;
-    const int64_t word = (((int64_t)st * (m + P - 1) + (it - 1)) * P + t) * (K / 8) + c / 8;
+    const int64_t entry = lane_major ? ((int64_t)st * P + t) * tb_rows4(m, P) + (it - 1)
+                                     : ((int64_t)st * (m + P - 1) + (it - 1)) * P + t;
+    const int64_t word = entry * (K / 8) + c / 8;
     const uint32_t bits = __ldcg(code + word) >> (c % 8);   // L2 only: random 4-byte reads
     const bool pd = bits & 1u, pm = bits & 0x100u;
     const uint32_t origin = pm ? (pd ? 1u : 2u) : ((LOCAL && pd) ? 0u : 3u);   // local: "F wins" + diagonal bit = stop
@@ -292,6 +303,7 @@ template <int ATYPE, int PASS>
 __device__ __forceinline__ void tb_walk_pair(const TbParams& prm, int64_t u, int64_t p, int m, int n, const uint32_t* code,
                                              int i, int j) {
     const int P = prm.tb_p, K = prm.tb_k;
+    const bool lane_major = prm.lane_major != 0;
     uint32_t* out = nullptr;
     int64_t w = 0;
     if (PASS == 2) { out = prm.runs + prm.run_off[u]; w = prm.n_runs[u]; }
@@ -323,14 +335,14 @@ __device__ __forceinline__ void tb_walk_pair(const TbParams& prm, int64_t u, int
                     if (i == 0) { emit(2, j); j = 0; break; }
                     if (j == 0) { emit(1, i); i = 0; break; }
                 } else if (i == 0 || j == 0) break;  // local: H == 0 on the edges; semiglobal: free edges
-                const uint32_t cd = tb_code_at<ATYPE == AT_LOCAL>(code, i, j, m, P, K);
+                const uint32_t cd = tb_code_at<ATYPE == AT_LOCAL>(code, i, j, m, P, K, lane_major);
                 const uint32_t origin = cd & 3u;
                 if (origin == 0u) break;                        // local stop: H(i, j) == 0
                 if (origin == 1u) { emit(0, 1); --i; --j; continue; }
                 state = origin == 2u ? 1 : 2;
                 continue;
             }
-            const uint32_t cd = tb_code_at<ATYPE == AT_LOCAL>(code, i, j, m, P, K);
+            const uint32_t cd = tb_code_at<ATYPE == AT_LOCAL>(code, i, j, m, P, K, lane_major);
             if (state == 1) { emit(1, 1); const bool ext = cd & 4u; --i; if (!ext) state = 0; }
             else { emit(2, 1); const bool ext = cd & 8u; --j; if (!ext) state = 0; }
         }
