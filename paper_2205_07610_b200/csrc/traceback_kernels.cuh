@@ -297,13 +297,39 @@ __device__ __forceinline__ uint32_t tb_code_at(const uint32_t* code, int i, int 
 
 constexpr int kTbTmpRuns = 128;   // unrelated 250 bp reads average 77 runs, 99th percentile 99
 
+// Position of the walk inside a pair's code block, kept incrementally: a step changes the row by one and / or the column by
+// one, so the lane (t), the column inside the lane's strip (c) and the stage are carried along instead of being re-derived
+// from (i, j) with two integer divisions by run-time lane-group shapes per step.
+template <bool LOCAL>
+struct TbCursor {
+    const uint32_t* code;
+    int P, K, NW, m, rows4, st, t, c;
+    bool lane_major;
+    __device__ __forceinline__ void init(const uint32_t* code_, int m_, int P_, int K_, bool lane_major_, int j) {
+        code = code_; m = m_; P = P_; K = K_; NW = K_ / 8; lane_major = lane_major_; rows4 = tb_rows4(m_, P_);
+        const int W = P * K;
+        st = (j - 1) / W;
+        const int col = (j - 1) - st * W;
+        t = col / K; c = col - t * K;
+    }
+    __device__ __forceinline__ void left() {   // j -> j - 1
+        if (--c < 0) { c = K - 1; if (--t < 0) { t = P - 1; --st; } }
+    }
+    __device__ __forceinline__ uint32_t at(int i) const {   // code of cell (i, current column), as tb_code_at returns it
+        const int it = i + t;
+        const int64_t entry = lane_major ? ((int64_t)st * P + t) * rows4 + (it - 1) : ((int64_t)st * (m + P - 1) + (it - 1)) * P + t;
+        const uint32_t bits = __ldcg(code + entry * NW + (c >> 3)) >> (c & 7);
+        const bool pd = bits & 1u, pm = bits & 0x100u;
+        const uint32_t origin = pm ? (pd ? 1u : 2u) : ((LOCAL && pd) ? 0u : 3u);
+        return origin | ((bits >> 14) & 4u) | ((bits >> 21) & 8u);
+    }
+};
+
 // PASS 1 counts the runs, records the start cell and parks the first kTbTmpRuns runs (in walk order); PASS 2 writes the
 // runs in forward order: a reversed copy of the parked runs, or a second walk for alignments with more runs than that.
 template <int ATYPE, int PASS>
 __device__ __forceinline__ void tb_walk_pair(const TbParams& prm, int64_t u, int64_t p, int m, int n, const uint32_t* code,
                                              int i, int j) {
-    const int P = prm.tb_p, K = prm.tb_k;
-    const bool lane_major = prm.lane_major != 0;
     uint32_t* out = nullptr;
     int64_t w = 0;
     if (PASS == 2) { out = prm.runs + prm.run_off[u]; w = prm.n_runs[u]; }
@@ -328,6 +354,8 @@ __device__ __forceinline__ void tb_walk_pair(const TbParams& prm, int64_t u, int
     };
     int state = 0;  // 0: at H, 1: inside a vertical run (E), 2: inside a horizontal run (F)
     if (m > 0 && n > 0) {
+        TbCursor<ATYPE == AT_LOCAL> cur;
+        cur.init(code, m, prm.tb_p, prm.tb_k, prm.lane_major != 0, max(j, 1));
         for (;;) {
             if (state == 0) {
                 if (i == 0 && j == 0) break;
@@ -335,16 +363,16 @@ __device__ __forceinline__ void tb_walk_pair(const TbParams& prm, int64_t u, int
                     if (i == 0) { emit(2, j); j = 0; break; }
                     if (j == 0) { emit(1, i); i = 0; break; }
                 } else if (i == 0 || j == 0) break;  // local: H == 0 on the edges; semiglobal: free edges
-                const uint32_t cd = tb_code_at<ATYPE == AT_LOCAL>(code, i, j, m, P, K, lane_major);
+                const uint32_t cd = cur.at(i);
                 const uint32_t origin = cd & 3u;
                 if (origin == 0u) break;                        // local stop: H(i, j) == 0
-                if (origin == 1u) { emit(0, 1); --i; --j; continue; }
+                if (origin == 1u) { emit(0, 1); --i; --j; cur.left(); continue; }
                 state = origin == 2u ? 1 : 2;
                 continue;
             }
-            const uint32_t cd = tb_code_at<ATYPE == AT_LOCAL>(code, i, j, m, P, K, lane_major);
+            const uint32_t cd = cur.at(i);
             if (state == 1) { emit(1, 1); const bool ext = cd & 4u; --i; if (!ext) state = 0; }
-            else { emit(2, 1); const bool ext = cd & 8u; --j; if (!ext) state = 0; }
+            else { emit(2, 1); const bool ext = cd & 8u; --j; cur.left(); if (!ext) state = 0; }
         }
     } else if (ATYPE == AT_GLOBAL) {  // an empty side: one gap run (ref_traceback walks the edge)
         if (i == 0 && j > 0) { emit(2, j); j = 0; }
