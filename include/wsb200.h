@@ -175,6 +175,12 @@ int wsb_f16_range_ok(const wsb_scheme* scheme, int32_t m, int32_t n);
 int wsb_plan_shards(const int32_t* q_len, const int32_t* s_len, const int32_t* pair_q, const int32_t* pair_s,
                     int64_t n_pairs, int32_t n_shards, int32_t* shard_of, int64_t* shard_cells);
 
+/* Geometry counters of the batch's last plan -- the GPU counterpart of the reference's EngineStats (engine.py:109-146,
+ * pinned by tests/test_engine.py:187-245): out8 = {stages, wavefront iterations, cell updates executed (padding included,
+ * stages * m * stage width per alignment), max instructions, add / sub instructions, substitution lookups (thread-instruction
+ * counts of the kernels' cell bodies: packed kernels advance two cells per instruction), launch groups, pairs launched}. */
+int wsb_batch_plan_stats(const wsb_batch* b, int64_t* out8);
+
 /* SM cycles the last packed int16 short-read launch of the batch took (largest per-block clock64 span; 0 if none ran):
  * the denominator of the cycle-based roofline fraction, independent of the clock the GPU happened to hold. */
 int64_t wsb_batch_kernel_cycles(wsb_batch* batch);

@@ -25,7 +25,7 @@ EXPORTED_SYMBOLS = (
     "wsb_batch_traceback", "wsb_batch_fetch_traceback", "wsb_batch_total_cells", "wsb_score_batch",
     "wsb_traceback_batch", "wsb_merged_state_exact", "wsb_f16_range_ok", "wsb_plan_shards", "wsb_batch_has_faults", "wsb_pinned_alloc",
     "wsb_pinned_free", "wsb_batch_total_runs", "wsb_batch_h2d_bytes", "wsb_compact_pool", "wsb_batch_kernel_cycles",
-    "wsb_batch_set_tb_scratch", "wsb_batch_tb_info",
+    "wsb_batch_set_tb_scratch", "wsb_batch_tb_info", "wsb_batch_plan_stats",
 )
 
 
@@ -79,6 +79,7 @@ def load():
     lib.wsb_batch_total_runs.restype = i64
     lib.wsb_batch_set_tb_scratch.argtypes = [p, i64]
     lib.wsb_batch_tb_info.argtypes = [p, p]
+    lib.wsb_batch_plan_stats.argtypes = [p, p]
     lib.wsb_pinned_alloc.argtypes = [ctypes.c_size_t, p]
     lib.wsb_pinned_free.argtypes = [p]
     lib.wsb_pinned_free.restype = None
@@ -284,10 +285,16 @@ class Batch:
             raise status_exception(rc, self.ctx.last_error())
         return float(ms.value), int(nl.value)
 
-    def fetch_scores(self):
+    def fetch_scores(self, dest=None):
+        """(score, end_i, end_j, status).  dest: three preallocated int32 arrays of n_pairs elements to download into (the
+        multi-GPU runner passes slices of the job-wide result arrays, so shard results land in place)."""
         n = self.n_pairs
         big = n >= 65536
-        score, ei, ej = (pinned_empty(n) for _ in range(3)) if big else (np.empty(n, np.int32) for _ in range(3))
+        if dest is not None:
+            score, ei, ej = dest
+            assert all(a.dtype == np.int32 and a.flags.c_contiguous and len(a) == n for a in dest)
+        else:
+            score, ei, ej = (pinned_empty(n) for _ in range(3)) if big else (np.empty(n, np.int32) for _ in range(3))
         # the per-pair status array only carries information when the plan recorded a fault
         self.has_faults = bool(self._lib.wsb_batch_has_faults(self._h))
         status = np.empty(n, np.int32) if self.has_faults else None
@@ -297,6 +304,15 @@ class Batch:
         if status is None:
             status = np.zeros(n, np.int32)  # calloc: costs nothing until somebody reads it
         return score, ei, ej, status
+
+    def plan_stats(self) -> dict:
+        """Geometry counters of the last plan (stages, wavefront iterations, executed cell updates, instruction counts)."""
+        out = (ctypes.c_int64 * 8)()
+        rc = self._lib.wsb_batch_plan_stats(self._h, out)
+        if rc:
+            raise status_exception(rc, self.ctx.last_error())
+        keys = ("stages", "iterations", "updates", "ops_max", "ops_addsub", "ops_lookup", "groups", "pairs")
+        return {k: int(v) for k, v in zip(keys, out)}
 
     def set_tb_scratch(self, nbytes: int) -> None:
         """Direction-code scratch budget of this batch; pairs whose codes exceed it take the bounded-memory path."""

@@ -180,7 +180,7 @@ def _variant_for(job: BatchJob, cfg: AlignConfig) -> str:
 
 
 def _run_shard(device: int, queries: SequencePool, subjects: SequencePool, pair_q: np.ndarray, pair_s: np.ndarray,
-               cfg: AlignConfig, scheme: ScoringScheme, variant: str, out: dict, regular: bool = False):
+               cfg: AlignConfig, scheme: ScoringScheme, variant: str, out: dict, regular: bool = False, dest=None):
     try:
         ctx = get_context(device)
         both_packed = queries.packed is not None and subjects.packed is not None
@@ -206,7 +206,7 @@ def _run_shard(device: int, queries: SequencePool, subjects: SequencePool, pair_
                 out["faults"] = batch.has_faults
             else:
                 out["ms"], out["launches"] = batch.score(scheme, cfg.align_type, variant)
-                out["scores"] = batch.fetch_scores()
+                out["scores"] = batch.fetch_scores(dest)
                 out["faults"] = batch.has_faults
         finally:
             batch.close()
@@ -215,7 +215,8 @@ def _run_shard(device: int, queries: SequencePool, subjects: SequencePool, pair_
 
 
 def _run_sliced_shard(device: int, queries: SequencePool, subjects: SequencePool, pair_q: np.ndarray, pair_s: np.ndarray,
-                      idx: np.ndarray, regular: bool, cfg: AlignConfig, scheme: ScoringScheme, variant: str, out: dict):
+                      idx: np.ndarray, regular: bool, cfg: AlignConfig, scheme: ScoringScheme, variant: str, out: dict,
+                      dest=None):
     """One GPU's share of a multi-GPU job: the pools are cut down to what the shard's pairs reference before anything is
     uploaded (a contiguous block of a reads matrix is a zero-copy slice; an arbitrary pair list is gathered into compact
     pools with remapped indices; a shard that references most of a pool anyway takes it whole)."""
@@ -224,7 +225,7 @@ def _run_sliced_shard(device: int, queries: SequencePool, subjects: SequencePool
             lo, hi = int(idx[0]), int(idx[-1]) + 1
             q_sub, s_sub = queries.slice_uniform(lo, hi), subjects.slice_uniform(lo, hi)
             ident = np.arange(hi - lo, dtype=np.int32)
-            return _run_shard(device, q_sub, s_sub, ident, ident, cfg, scheme, variant, out, True)
+            return _run_shard(device, q_sub, s_sub, ident, ident, cfg, scheme, variant, out, True, dest)
         pq, ps = pair_q[idx], pair_s[idx]
 
         def cut(pool, col):
@@ -278,14 +279,18 @@ def run_batch(job: BatchJob) -> BatchReport:
         shard_cells = [int(x) for x in sc]
     outs = [dict() for _ in devices]
     threads = []
+    # contiguous shards of a score-only job download straight into their block of the job-wide (page-locked) result arrays
+    in_place = len(devices) > 1 and regular and cfg.result_mode != "traceback" and n >= 65536
+    whole = tuple(N.pinned_empty(n) for _ in range(3)) if in_place else None
     for dev, idx, out in zip(devices, shard_index, outs):
         if len(idx) == 0:
             continue
         if len(devices) == 1:  # no thread hop for the common single-GPU case
             _run_shard(dev, queries, subjects, pair_q, pair_s, cfg, job.scheme, variant, out, regular)
             continue
+        dest = tuple(a[int(idx[0]):int(idx[-1]) + 1] for a in whole) if in_place else None
         th = threading.Thread(target=_run_sliced_shard, name=f"waveseq-gpu-{dev}",
-                              args=(dev, queries, subjects, pair_q, pair_s, idx, regular, cfg, job.scheme, variant, out))
+                              args=(dev, queries, subjects, pair_q, pair_s, idx, regular, cfg, job.scheme, variant, out, dest))
         threads.append(th)
         th.start()
     for th in threads:
@@ -303,6 +308,10 @@ def run_batch(job: BatchJob) -> BatchReport:
             qs = np.zeros(n, np.int32); ss = qs
         else:
             qs, ss = qe, se
+    elif in_place:
+        score, qe, se = whole
+        qs = ss = None
+        status = None
     else:
         score = np.empty(n, np.int32); qs = np.zeros(n, np.int32); qe = np.empty(n, np.int32)
         ss = np.zeros(n, np.int32); se = np.empty(n, np.int32); status = np.zeros(n, np.int32)
@@ -332,14 +341,28 @@ def run_batch(job: BatchJob) -> BatchReport:
             src_off = tb["cigar_off"]
             shift = np.repeat(run_off[idx] - src_off[:-1], np.diff(src_off))
             runs[shift + np.arange(len(shift), dtype=np.int64)] = tb["cigar"][:len(shift)]
+    elif in_place:   # the shards wrote their blocks themselves; the status array exists only if a shard reported faults
+        if any(o.get("faults", False) for o in outs if o):
+            status = np.zeros(n, np.int32)
+            for idx, out in zip(shard_index, outs):
+                if len(idx):
+                    status[int(idx[0]):int(idx[-1]) + 1] = out["scores"][3]
+        else:
+            status = np.zeros(n, np.int32)   # calloc: costs nothing until somebody reads it
+        if cfg.align_type == "global":
+            qs = np.zeros(n, np.int32); ss = qs
+        else:
+            qs, ss = qe, se
     else:
         for idx, out in zip(shard_index, outs):
             if len(idx) == 0:
                 continue
             sc_, ei, ej, st = out["scores"]
-            score[idx], qe[idx], se[idx], status[idx] = sc_, ei, ej, st
+            # contiguous shards (reads matrices) land with four block copies; index arrays only for planner-made shards
+            at = slice(int(idx[0]), int(idx[-1]) + 1) if int(idx[-1]) - int(idx[0]) + 1 == len(idx) else idx
+            score[at], qe[at], se[at], status[at] = sc_, ei, ej, st
         if cfg.align_type != "global":  # start is unknown without a traceback pass: both span ends carry the argmax cell (batch.py:111-115)
-            qs[:] = qe; ss[:] = se
+            qs, ss = qe, se
     any_fault = any(o.get("faults", True) for o in outs if o)
     bad = np.nonzero(status)[0] if any_fault else ()
     if len(bad):

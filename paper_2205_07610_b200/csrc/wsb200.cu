@@ -96,6 +96,9 @@ struct Plan {
     int32_t* d_units = nullptr;
     std::vector<int32_t> status;  // per pair
     bool any_error = false;
+    // geometry counters of the plan (wsb_batch_plan_stats): the GPU counterpart of EngineStats (engine.py:109-146)
+    int64_t st_stages = 0, st_iters = 0, st_updates = 0, st_pairs = 0;
+    int64_t st_q_max = 0, st_q_add = 0, st_q_lookup = 0;   // thread-instructions x 4 (packed kernels advance two cells per instruction)
 };
 
 struct wsb_batch {
@@ -629,6 +632,15 @@ extern "C" int64_t wsb_batch_kernel_cycles(wsb_batch* b) {
     return (int64_t)mx;
 }
 extern "C" int64_t wsb_batch_h2d_bytes(const wsb_batch* b) { return b ? b->h2d_bytes : 0; }
+
+extern "C" int wsb_batch_plan_stats(const wsb_batch* b, int64_t* out8) {
+    if (!b || !out8 || !b->last_plan) return WSB_E_ARG;
+    const Plan& pl = *b->last_plan;
+    out8[0] = pl.st_stages; out8[1] = pl.st_iters; out8[2] = pl.st_updates;
+    out8[3] = pl.st_q_max / 4; out8[4] = pl.st_q_add / 4; out8[5] = pl.st_q_lookup / 4;
+    out8[6] = (int64_t)pl.groups.size(); out8[7] = pl.st_pairs;
+    return WSB_OK;
+}
 extern "C" int wsb_batch_has_faults(const wsb_batch* b) { return (b && b->last_plan && b->last_plan->any_error) ? 1 : 0; }
 
 // Page-locked host blocks for result downloads, recycled process-wide (cudaHostAlloc of tens of MB costs milliseconds).
@@ -785,6 +797,31 @@ static KernelSel pick_kernel(int variant, int shape, int atype, int gap, bool ma
     }
 }
 
+
+// Per-cell instruction mix of the kernel a launch group runs, in quarter thread-instructions per matrix cell: {max, add /
+// sub, substitution lookup}.  These are the cell bodies of the kernels; tests/test_cpu_host.py pins the
+// packed int16 rows against the SASS of the built library.
+static void op_mix_q(const LaunchGroup& g, int atype, int& qmax, int& qadd, int& qlook) {
+    const bool local = atype == AT_LOCAL, merged = g.gap == GAP_MERGED, exact = g.gap == GAP_EXACT;
+    if (g.long_nw > 0) {
+        if (g.long16) { qmax = (merged ? 4 : 2) + (local ? 1 : 0); qadd = merged ? 6 : 4; qlook = 2; }
+        else { qmax = (merged ? 8 : 4) + (local ? 2 : 0); qadd = merged ? 8 : 4; qlook = 4; }
+        return;
+    }
+    if (g.variant == WSB_VARIANT_S16X2) {   // PRMT + VIADD + (2 | 1) VIMNMX3 + (2 | 1) VIADD per two cells, local: + half a VIMNMX3
+        qmax = (merged ? 4 : 2) + (local ? 1 : 0); qadd = merged ? 6 : 4; qlook = 2;
+        return;
+    }
+    if (g.variant == WSB_VARIANT_F16X2) {
+        const Shape sh = kShapesF16[g.shape];
+        const bool short_ok = local && g.max_n <= sh.P * sh.K && g.max_m <= kShortQRows - 4 * sh.P - 2;
+        if (short_ok) { qmax = merged ? 5 : 3; qadd = merged ? 8 : 6; qlook = 2; }
+        else { qmax = (merged ? 6 : 4) + (local ? 2 : 0); qadd = merged ? 8 : 6; qlook = 2; }
+        return;
+    }
+    qmax = (exact ? 12 : merged ? 12 : 8) + (local ? 4 : 0); qadd = exact ? 20 : 4; qlook = 4;
+}
+
 // ------------------------------------------------------------------------------------------------ planner
 // Length-bucketing partitioner: classify every pair (variant by value range, kernel shape by padded work), sort each
 // class by work so neighbouring lane groups (and the two halves of a packed unit) carry near-equal loads, and emit one
@@ -844,6 +881,42 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
         return n > 2048 || (n > 512 && padded * 100 <= (int64_t)n * 115);
     };
 
+    // geometry counters: per unit the stages of its subject, the wavefront trips of its sweep(s) and the cell updates the
+    // lockstep sweep executes, padding included (the reference's definition, tests/test_engine.py:223-233)
+    auto account_plan = [&](Plan& pl, const std::vector<int32_t>& unit_list) {
+        for (const LaunchGroup& g : pl.groups) {
+            const int nv = (g.long_nw > 0) ? (g.long16 ? 2 : 1) : (g.variant == WSB_VARIANT_I32 ? 1 : 2);
+            const int P = g.long_nw > 0 ? 32 : shape_of(g.variant, g.shape).P;
+            const int W = g.long_nw > 0 ? kLongW : P * shape_of(g.variant, g.shape).K;
+            int qmax, qadd, qlook;
+            op_mix_q(g, atype, qmax, qadd, qlook);
+            for (int64_t u = 0; u < g.n_units; ++u) {
+                int mu = 0, nu = 0, live = 0;
+                for (int v = 0; v < nv; ++v) {
+                    int64_t pr;
+                    if (g.unit_off < 0) { pr = u * nv + v; if (pr >= np) pr = -1; }
+                    else pr = unit_list[(size_t)(g.unit_off + u * nv + v)];
+                    if (pr < 0) continue;
+                    mu = std::max(mu, (int)b->m[pr]); nu = std::max(nu, (int)b->n[pr]); ++live;
+                }
+                if (!live) continue;
+                const int64_t stages = (nu + W - 1) / W;
+                const int64_t updates = stages * (int64_t)mu * W * nv;
+                pl.st_stages += stages; pl.st_iters += stages * (mu + P - 1); pl.st_updates += updates; pl.st_pairs += live;
+                pl.st_q_max += updates * qmax; pl.st_q_add += updates * qadd; pl.st_q_lookup += updates * qlook;
+                if (g.unit_off < 0) {   // identical units: multiply instead of looping over millions of them
+                    const int64_t rest = g.n_units - 1 - (np % nv ? 1 : 0);
+                    if (u == 0 && rest > 0) {
+                        pl.st_stages += stages * rest; pl.st_iters += stages * (mu + P - 1) * rest; pl.st_updates += updates * rest;
+                        pl.st_pairs += (int64_t)live * rest;
+                        pl.st_q_max += updates * qmax * rest; pl.st_q_add += updates * qadd * rest; pl.st_q_lookup += updates * qlook * rest;
+                        u += rest;
+                    }
+                }
+            }
+        }
+    };
+
     if (b->uniform) {
         int var, shape, status;
         classify(b->m[0], b->n[0], var, shape, status);
@@ -855,6 +928,7 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
             g.n_units = var == WSB_VARIANT_I32 ? np : (np + 1) / 2;
             g.unit_off = -1; g.max_m = b->m[0]; g.max_n = b->n[0];
             plan.groups.push_back(g);
+            account_plan(plan, std::vector<int32_t>());
             return WSB_OK;
         }
     }
@@ -1000,6 +1074,7 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
             }
             plan.groups.push_back(g);
         }
+    account_plan(plan, units);
     if (!units.empty()) {
         CUDA_TRY(ctx, cudaMalloc((void**)&plan.d_units, units.size() * sizeof(int32_t)));
         CUDA_TRY(ctx, cudaMemcpyAsync(plan.d_units, units.data(), units.size() * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));

@@ -79,8 +79,12 @@ def f16_range_ok(scheme: ScoringScheme, m: int, n: int) -> bool:
 
 @dataclass
 class EngineStats:
-    """Counters of the reference's CPU engine.  The GPU path keeps cells and stages; the block counters, which count
-    the CPU emulation's memory touches, stay zero (the kernels' traffic is measured with ncu instead)."""
+    """Counters of the reference's engine (engine.py:109-146), filled from the native planner (wsb_batch_plan_stats):
+    stages, wavefront iterations, and the max / add-sub instructions of the executed cell updates (padding included) as
+    thread-instruction counts of the kernel the planner picked -- the packed kernels advance two cells per instruction, so
+    ops per update can be fractional; ops_lookup counts the substitution lookups (PRMT / IDP.4A / HSET2), which the
+    reference's tally folds into its adds.  The block counters count the CPU emulation's memory touches and stay zero
+    (the kernels' traffic is measured with ncu instead)."""
 
     query_load_blocks: int = 0
     query_load_misaligned: int = 0
@@ -93,13 +97,24 @@ class EngineStats:
     iterations: int = 0
     cells: int = 0
     stages: int = 0
+    ops_lookup: int = 0      # extension: substitution lookups
+    updates: int = 0         # extension: cell updates executed, padding included (stages * m * stage width per alignment)
 
     @property
     def ops_total(self) -> int:
         return self.ops_max + self.ops_addsub
 
+    def absorb_plan(self, plan: dict, cells: int) -> None:
+        self.cells += cells
+        self.stages += plan["stages"]
+        self.iterations += plan["iterations"]
+        self.updates += plan["updates"]
+        self.ops_max += plan["ops_max"]
+        self.ops_addsub += plan["ops_addsub"]
+        self.ops_lookup += plan["ops_lookup"]
 
-def _score_pairs(pairs, cfg: AlignConfig, scheme: ScoringScheme, variant: str, device: int = 0):
+
+def _score_pairs(pairs, cfg: AlignConfig, scheme: ScoringScheme, variant: str, device: int = 0, stats=None):
     queries = SequencePool.from_sequences([p[0] for p in pairs])
     subjects = SequencePool.from_sequences([p[1] for p in pairs])
     idx = np.arange(len(pairs), dtype=np.int32)
@@ -108,6 +123,8 @@ def _score_pairs(pairs, cfg: AlignConfig, scheme: ScoringScheme, variant: str, d
     try:
         batch.score(scheme, cfg.align_type, variant, timed=False)
         score, ei, ej, status = batch.fetch_scores()
+        if stats is not None:
+            stats.absorb_plan(batch.plan_stats(), sum(len(q) * len(s) for q, s in pairs))
     finally:
         batch.close()
     for k in range(len(pairs)):
@@ -126,10 +143,7 @@ def engine_score(query: Sequence, subject: Sequence, cfg: AlignConfig, scheme: S
     check_length_bounds(m, n, scheme)
     # tuning.packed is a hint, as in the reference (engine.py:383-400 never looks at it): the planner packs two
     # alignments per register wherever that is exact (int16 / half2) and runs int32 elsewhere
-    score, ei, ej = _score_pairs([(query, subject)], cfg, scheme, "auto")
-    if stats is not None:
-        stats.cells += m * n
-        stats.stages += 1
+    score, ei, ej = _score_pairs([(query, subject)], cfg, scheme, "auto", stats=stats)
     return int(score[0]), (int(ei[0]), int(ej[0])), m * n
 
 
@@ -147,9 +161,6 @@ def engine_score_packed(pair_a: tuple[Sequence, Sequence], pair_b: tuple[Sequenc
                                       f"(max |score| step {scheme.max_step})")
     if scheme.gap_model == "affine" and not merged_state_exact(scheme):
         raise ValueError("packed affine mode requires a merged-state-exact scheme")
-    score, ei, ej = _score_pairs([pair_a, pair_b], cfg, scheme, "auto")
+    score, ei, ej = _score_pairs([pair_a, pair_b], cfg, scheme, "auto", stats=stats)
     cells = len(pair_a[0]) * len(pair_a[1]) + len(pair_b[0]) * len(pair_b[1])
-    if stats is not None:
-        stats.cells += cells
-        stats.stages += 1
     return (int(score[0]), (int(ei[0]), int(ej[0]))), (int(score[1]), (int(ei[1]), int(ej[1]))), cells

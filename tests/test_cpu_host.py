@@ -267,3 +267,44 @@ def test_packed_traceback_fill_keeps_its_max_operand_order():
     assert len(maxes) > 100
     bad = [ln for ln in maxes if re.search(r"VIMNMX\.S16x2 R\d+, P[0-6], P[0-6], R\d+, (0x|-0x|c\[)", ln)]
     assert not bad, bad[:3]
+
+
+def test_plan_stats_instruction_mix_matches_the_built_kernels():
+    """EngineStats.ops_* come from a per-kernel instruction mix (csrc/wsb200.cu: op_mix_q).  Pin the packed int16 rows of
+    that table to the SASS of the built library: per trip of 19 columns x 2 alignments the hot loops must hold the modelled
+    number of packed max / add / lookup instructions (plus the few the hand-over and the record add)."""
+    import shutil, subprocess, collections
+    lib = os.path.join(os.path.dirname(N.__file__), "libwsb200.so")
+    dump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(lib) or not os.path.exists(dump):
+        pytest.skip("library or cuobjdump not available")
+
+    def hot_loop(pattern, op, min_hits):
+        names = subprocess.run([dump, "-elf", lib], capture_output=True, text=True).stdout
+        fn = sorted(f for f in set(re.findall(r"_ZN3wsb\w+", names)) if pattern in f)[0]
+        sass = subprocess.run([dump, "-sass", "-fun", fn, lib], capture_output=True, text=True).stdout
+        ins = [(int(m.group(1), 16), m.group(2), m.group(0)) for m in
+               re.finditer(r"/\*([0-9a-f]{4,5})\*/\s+(?:@!?U?P\d\s+)?([A-Z0-9_.]+)[^;]*;", sass)]
+        best = None
+        for a, o, l in ins:
+            t = re.search(r"BRA\S*\s+(?:\S+,\s*)?0x([0-9a-f]+)", l) if o.startswith("BRA") else None
+            if t and int(t.group(1), 16) < a:
+                body = [x for x in ins if int(t.group(1), 16) <= x[0] <= a]
+                if sum(1 for x in body if x[1].startswith(op)) >= min_hits and (best is None or len(body) < len(best)):
+                    best = body
+        assert best, pattern
+        return collections.Counter(o for _, o, _ in best)
+
+    cells = 2 * 19
+    c = hot_loop("s16_local_short_kernelILi8ELi19ELi1ELi4ELi2ELi1E", "VIMNMX3", 40)       # local, merged affine: 5 / 6 / 2 quarters
+    n_max = sum(v for k, v in c.items() if k.startswith(("VIMNMX", "VIADDMNMX")))
+    n_add = sum(v for k, v in c.items() if k.startswith("VIADD.16"))
+    assert cells * 5 / 4 <= n_max <= cells * 5 / 4 + 4, c
+    assert cells * 6 / 4 <= n_add <= cells * 6 / 4 + 2, c
+    assert c["PRMT"] == cells * 2 // 4
+    c = hot_loop("s16_global_short_kernelILi8ELi19ELi0ELb0ELi1ELi1E", "VIMNMX3", 15)      # global, linear: 2 / 4 / 2 quarters
+    n_max = sum(v for k, v in c.items() if k.startswith(("VIMNMX", "VIADDMNMX")))
+    n_add = sum(v for k, v in c.items() if k.startswith("VIADD.16"))
+    assert cells * 2 / 4 <= n_max <= cells * 2 / 4 + 3, c
+    assert cells * 4 / 4 <= n_add <= cells * 4 / 4 + 3, c
+    assert c["PRMT"] == cells * 2 // 4

@@ -301,3 +301,33 @@ def test_selftest_draws_the_reference_cases_and_agrees_with_the_oracle():
     blob = json.loads(json.dumps(rep["failure"]))
     assert set(blob) >= {"case", "seed", "query", "subject", "align_type", "gap_model", "scheme", "engine", "reference"}
     assert blob["reference"][0] == blob["engine"][0] + 1 and set(blob["query"]) <= set("ACGT")
+
+
+def test_engine_stats_from_the_planner():
+    """EngineStats in the spirit of tests/test_engine.py:187-245: stages, wavefront iterations and ops per executed cell
+    update come back from the native planner (padding included, the reference's definition)."""
+    rng = np.random.default_rng(4)
+    q = W.Sequence("q", rng.integers(0, 4, 150).astype(np.uint8), np.zeros(150, bool))
+    s = W.Sequence("s", rng.integers(0, 4, 150).astype(np.uint8), np.zeros(150, bool))
+    scheme = W.ScoringScheme(2, -1, 2, 1, "affine")
+    st = W.EngineStats()
+    W.engine_score(q, s, W.AlignConfig("local", "affine"), scheme, stats=st, instrument=True)
+    # packed int16 short kernel: lane groups of 8 x 19 columns, two alignments per register (the second half rides empty)
+    assert (st.stages, st.iterations, st.cells) == (1, 150 + 8 - 1, 150 * 150)
+    assert st.updates == 1 * 150 * 152 * 2
+    assert st.ops_max * 4 == st.updates * 5 and st.ops_addsub * 4 == st.updates * 6 and st.ops_lookup * 2 == st.updates
+    st2 = W.EngineStats()
+    lin = W.ScoringScheme(2, -1, 1, 1, "linear")
+    W.engine_score(q, s, W.AlignConfig("global", "linear"), lin, stats=st2, instrument=True)
+    assert st2.ops_max * 2 == st2.updates and st2.ops_addsub == st2.updates      # VIMNMX3 + VIADD, PRMT + VIADD per two cells
+    # a long pair: 512-column stages of the long-read kernel, int32 (5 instructions per cell: 2 max, 2 add, 1 lookup)
+    ql = W.Sequence("q", rng.integers(0, 4, 3000).astype(np.uint8), np.zeros(3000, bool))
+    sl = W.Sequence("s", rng.integers(0, 4, 5000).astype(np.uint8), np.zeros(5000, bool))
+    st3 = W.EngineStats()
+    W.engine_score(ql, sl, W.AlignConfig("global", "affine"), scheme, stats=st3)
+    assert st3.stages == 10 and st3.iterations == 10 * (3000 + 31) and st3.updates == 10 * 3000 * 512
+    assert st3.ops_total == 4 * st3.updates and st3.ops_lookup == st3.updates
+    st3.cells == 3000 * 5000
+    # counters accumulate over calls like the reference's absorb()
+    W.engine_score(q, s, W.AlignConfig("local", "affine"), scheme, stats=st)
+    assert st.stages == 2 and st.cells == 2 * 150 * 150
