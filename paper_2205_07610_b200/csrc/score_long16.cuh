@@ -22,7 +22,9 @@
 
 namespace wsb {
 
-template <int ATYPE, int GAP>
+// AIMM / GIMM > 0: gap costs alpha / gamma as immediates (the host picks such an instantiation when the scheme matches):
+// at ptxas -O1 the packed constants are otherwise re-materialised from the kernel parameters in every row.
+template <int ATYPE, int GAP, int AIMM = 0, int GIMM = 0>
 __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long16_kernel(const LongParams prm) {
     constexpr int K = kLongK, W = kLongW;
     constexpr bool LOCAL = ATYPE == AT_LOCAL;
@@ -39,9 +41,13 @@ __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long16_kernel(const 
     const int NW = blockDim.x >> 5;
     const int w = threadIdx.x >> 5;
     const int t = threadIdx.x & 31;
-    const int alpha = prm.alpha, beta = prm.beta;
-    const int gamma = MERGED ? min(alpha, beta) : alpha;
-    const unsigned c_nalpha = pack16(-alpha), c_ngamma = pack16(-gamma), c_gma = pack16(gamma - alpha), c_nbeta = pack16(-beta);
+    const int alpha = AIMM > 0 ? AIMM : prm.alpha, beta = prm.beta;
+    const int gamma = GIMM > 0 ? GIMM : (MERGED ? min(prm.alpha, beta) : prm.alpha);
+    const unsigned c_nalpha = AIMM > 0 ? ((unsigned)(-AIMM) & 0xffffu) * 0x10001u : pack16(-alpha);
+    const unsigned c_ngamma = GIMM > 0 ? ((unsigned)(-GIMM) & 0xffffu) * 0x10001u : pack16(-gamma);
+    const unsigned c_gma = (AIMM > 0 && GIMM > 0) ? ((unsigned)(GIMM - AIMM) & 0xffffu) * 0x10001u : pack16(gamma - alpha);
+    const unsigned c_nbeta = pack16(-beta);
+    const unsigned s_in_base = (unsigned)__cvta_generic_to_shared(&s_in[threadIdx.x >> 5][0]);
     const unsigned mism4 = (unsigned)(prm.mismatch & 0xff) * 0x01010101u;
     const unsigned match1 = (unsigned)(prm.match & 0xff);
     int2* const bnd_block = prm.bnd + (int64_t)blockIdx.x * (NW + 1) * prm.bnd_rows;
@@ -137,7 +143,9 @@ __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long16_kernel(const 
 
             auto iteration = [&](int it, auto check_tag) {
                 constexpr bool CHECK = decltype(check_tag)::value;
-                const int4 in = s_in[w][(it - 1) & 63];
+                int4 in;   // lane 0's inputs for this row (broadcast load from a precomputed shared-memory address)
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(in.x), "=r"(in.y), "=r"(in.z), "=r"(in.w)
+                             : "r"(s_in_base + 16u * (unsigned)((it - 1) & 63)) : "memory");
                 if (t == 0) {
                     rwA = (unsigned)in.z; rwB = (unsigned)in.w;
                     if (first) { h_l = edge_h16; tg_l = edge_tg16; }

@@ -758,7 +758,7 @@ KernelSel pick_short16_local(int shape, int gap, int alpha, int gamma);
 KernelSel pick_short16_global(int shape, int gap, int alpha, int gamma, bool ragged);
 }
 
-namespace wsb { LongFn pick_long16(int atype, int gap); }   // score_long16.cuh, compiled in wsb200_s16.cu
+namespace wsb { LongFn pick_long16(int atype, int gap, int alpha, int gamma); }   // score_long16.cuh, compiled in wsb200_s16.cu
 
 // short_ok: every unit of the launch fits one stage and the short kernel's query buffer
 static KernelSel pick_kernel(int variant, int shape, int atype, int gap, bool masked, bool short_ok, bool wide,
@@ -1152,7 +1152,8 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
     size_t bnd_need = 0;
     for (const LaunchGroup& g : plan.groups) {
         if (g.long_nw > 0) {
-            LongFn lfn = g.long16 ? pick_long16(atype, g.gap) : pick_long(atype, g.gap, g.cluster > 1);
+            LongFn lfn = g.long16 ? pick_long16(atype, g.gap, sch->gap_open, affine ? std::min(sch->gap_open, sch->gap_extend) : sch->gap_open)
+                                  : pick_long(atype, g.gap, g.cluster > 1);
             if (!lfn) return WSB_E_SCHEME;
             int grid = 1;
             if (g.cluster > 1) {  // one pair per cluster: as many clusters as the device can co-schedule

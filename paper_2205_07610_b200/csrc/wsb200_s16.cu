@@ -41,16 +41,17 @@ KernelSel pick_short16_global(int shape, int gap, int alpha, int gamma, bool rag
     return shape == 0 ? pick_global<8, 16>(gap, alpha, gamma, ragged) : pick_global<8, 19>(gap, alpha, gamma, ragged);
 }
 
-template <int GAP> static LongFn pick_long16_atype(int atype) {
+template <int GAP, int AIMM, int GIMM> static LongFn pick_long16_atype(int atype) {
     switch (atype) {
-        case AT_GLOBAL: return score_long16_kernel<AT_GLOBAL, GAP>;
-        case AT_LOCAL: return score_long16_kernel<AT_LOCAL, GAP>;
-        default: return score_long16_kernel<AT_SEMI, GAP>;
+        case AT_GLOBAL: return score_long16_kernel<AT_GLOBAL, GAP, AIMM, GIMM>;
+        case AT_LOCAL: return score_long16_kernel<AT_LOCAL, GAP, AIMM, GIMM>;
+        default: return score_long16_kernel<AT_SEMI, GAP, AIMM, GIMM>;
     }
 }
-LongFn pick_long16(int atype, int gap) {
-    if (gap == GAP_LINEAR) return pick_long16_atype<GAP_LINEAR>(atype);
-    if (gap == GAP_MERGED) return pick_long16_atype<GAP_MERGED>(atype);
+LongFn pick_long16(int atype, int gap, int alpha, int gamma) {
+    if (gap == GAP_LINEAR) return alpha == 1 ? pick_long16_atype<GAP_LINEAR, 1, 1>(atype) : pick_long16_atype<GAP_LINEAR, 0, 0>(atype);
+    if (gap == GAP_MERGED) return (alpha == 2 && gamma == 1) ? pick_long16_atype<GAP_MERGED, 2, 1>(atype)
+                                                             : pick_long16_atype<GAP_MERGED, 0, 0>(atype);
     return nullptr;
 }
 
