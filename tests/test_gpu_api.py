@@ -1,10 +1,13 @@
 """GPU: the reference-facing Python API (run_batch, engine_score, align, ...) behaves like the reference's."""
+import os
+
 import numpy as np
 import pytest
 
 import oracle
 import paper_2205_07610_b200 as W
 from conftest import COMBOS, load_golden
+from paper_2205_07610_b200 import _native as N
 
 pytestmark = pytest.mark.gpu
 
@@ -331,3 +334,55 @@ def test_engine_stats_from_the_planner():
     # counters accumulate over calls like the reference's absorb()
     W.engine_score(q, s, W.AlignConfig("local", "affine"), scheme, stats=st)
     assert st.stages == 2 and st.cells == 2 * 150 * 150
+
+
+def _gpu_rank_main(rank, world, port, out_dir):
+    """One rank of a two-rank job over gloo, both ranks on GPU 0: plan the shards natively, run MY shard through the product's
+    run_batch, gather the shard results by pair index; rank 0 compares the gathered job with the oracle."""
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(77)                      # every rank builds the same job
+    n = 3000
+    seqs_q = [rng.integers(0, 4, int(rng.integers(20, 400))).astype(np.uint8) for _ in range(n)]
+    seqs_s = [rng.integers(0, 4, int(rng.integers(20, 400))).astype(np.uint8) for _ in range(n)]
+    seqs_q[7] = rng.integers(0, 4, 5000).astype(np.uint8); seqs_s[7] = rng.integers(0, 4, 6000).astype(np.uint8)   # one heavy pair
+    pool = lambda xs: W.SequencePool.from_sequences([W.Sequence(f"x{i}", x, np.zeros(len(x), bool)) for i, x in enumerate(xs)])
+    pq, ps = pool(seqs_q), pool(seqs_s)
+    idx = np.arange(n, dtype=np.int32)
+    shard_of, cells = N.plan_shards(pq.len, ps.len, idx, idx, world)
+    mine = np.nonzero(shard_of == rank)[0]
+    cfg = W.AlignConfig("local", "affine", "traceback")
+    rep = W.run_batch(W.BatchJob(pq, ps, np.stack([mine, mine], 1), cfg, W.ScoringScheme(), devices=[0]))
+    assert rep.total_cells == int(cells[rank])
+    local = torch.zeros(n, 3, dtype=torch.int64)
+    res = rep.results
+    local[torch.from_numpy(mine)] = torch.tensor([[r.score, r.q_end, r.s_end] for r in res], dtype=torch.int64)
+    dist.all_reduce(local, op=dist.ReduceOp.SUM)         # disjoint shards: the sum is the gather
+    cig = [None] * world
+    dist.all_gather_object(cig, {int(p): W.cigar_string(r) for p, r in zip(mine, res)})
+    if rank == 0:
+        import oracle
+        from helpers import make_pool
+        qc, qo, ql = make_pool(seqs_q); sc, so, sl = make_pool(seqs_s)
+        want = oracle.traceback_batch(qc, qo, ql, sc, so, sl, idx, idx, "local", True, 2, -1, 2, 1)
+        got = local.numpy()
+        assert (got[:, 0] == want["score"]).all() and (got[:, 1] == want["q_end"]).all() and (got[:, 2] == want["s_end"]).all()
+        merged = {k: v for d in cig for k, v in d.items()}
+        from conftest import cigar_of
+        assert all(merged[k] == cigar_of(want["ops"][k]) for k in range(n))
+        with open(os.path.join(out_dir, "ok"), "w") as fh:
+            fh.write("ok")
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_ranks_over_gloo_run_their_shards_on_the_gpu(tmp_path):
+    """The multi-rank protocol of bench.py / a multi-process deployment with real GPU work: world size 2 over gloo, both ranks on
+    GPU 0."""
+    import torch.multiprocessing as mp
+    port = 29600 + (os.getpid() % 2000)
+    mp.spawn(_gpu_rank_main, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    assert open(tmp_path / "ok").read() == "ok"
