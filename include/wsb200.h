@@ -122,6 +122,12 @@ int wsb_batch_score(wsb_batch* b, const wsb_scheme* scheme, int align_type, int 
  * status (optional): per-pair wsb_status (0 or WSB_E_LENGTH / WSB_E_RANGE). */
 int wsb_batch_fetch_scores(wsb_batch* b, int32_t* out_score, int32_t* out_i, int32_t* out_j, int32_t* status);
 
+/* wsb_batch_score + wsb_batch_fetch_scores in one call.  While the batch is still uploading piece by piece (the first score
+ * after wsb_batch_create_*_async) the results of every finished piece are downloaded on their own stream under the upload
+ * and the kernels of later pieces, so a step's download costs no time of its own.  Same outputs and status contract. */
+int wsb_batch_score_fetch(wsb_batch* b, const wsb_scheme* scheme, int align_type, int variant, float* kernel_ms,
+                          int32_t* n_launches, int32_t* out_score, int32_t* out_i, int32_t* out_j, int32_t* status);
+
 /* Direction-code fill + on-device walk + run-length CIGAR emission.  cigar receives runs packed as
  * (length << 2) | op with op 0 = M, 1 = I, 2 = D in forward order; pair p owns cigar[cigar_off[p] .. cigar_off[p+1]).
  * cigar_off has n_pairs + 1 entries.  If cigar_cap is too small the call returns WSB_E_CAPACITY and

@@ -25,7 +25,7 @@ EXPORTED_SYMBOLS = (
     "wsb_batch_traceback", "wsb_batch_fetch_traceback", "wsb_batch_total_cells", "wsb_score_batch",
     "wsb_traceback_batch", "wsb_merged_state_exact", "wsb_f16_range_ok", "wsb_plan_shards", "wsb_batch_has_faults", "wsb_pinned_alloc",
     "wsb_pinned_free", "wsb_batch_total_runs", "wsb_batch_h2d_bytes", "wsb_compact_pool", "wsb_batch_kernel_cycles",
-    "wsb_batch_set_tb_scratch", "wsb_batch_tb_info", "wsb_batch_plan_stats",
+    "wsb_batch_set_tb_scratch", "wsb_batch_tb_info", "wsb_batch_plan_stats", "wsb_batch_score_fetch",
 )
 
 
@@ -46,6 +46,9 @@ def load():
     if not os.path.exists(_LIB_PATH):
         raise DeviceError(f"{_LIB_PATH} is missing: build it with `python -m paper_2205_07610_b200.build` "
                           "(there is no CPU fallback)")
+    # upload, download, compute and the launch-group streams of a context should not share hardware connections (default 8
+    # per process); takes effect when CUDA has not been initialised yet in this process
+    os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
     lib = ctypes.CDLL(_LIB_PATH)
     p, i32, i64, ci = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int
     lib.wsb_strerror.restype = ctypes.c_char_p
@@ -66,6 +69,7 @@ def load():
     lib.wsb_batch_destroy.restype = None
     lib.wsb_batch_score.argtypes = [p, p, ci, ci, p, p]
     lib.wsb_batch_fetch_scores.argtypes = [p, p, p, p, p]
+    lib.wsb_batch_score_fetch.argtypes = [p, p, ci, ci, p, p, p, p, p, p]
     lib.wsb_batch_traceback.argtypes = [p, p, ci, p, p]
     lib.wsb_batch_fetch_traceback.argtypes = [p, p, p, p, p, p, p, i64, p, p]
     lib.wsb_batch_total_cells.argtypes = [p]
@@ -92,6 +96,12 @@ def load():
 
 def _ptr(a):
     return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def zeros_view(n: int) -> np.ndarray:
+    """n int32 zeros that cost nothing: a read-only broadcast of one element (numpy zero-fills a real 16 MB array, ~2 ms per
+    4 M pairs -- the per-pair status of a batch without faults is only ever read)."""
+    return np.broadcast_to(np.zeros(1, np.int32), (int(n),))
 
 
 def pinned_empty(n: int, dtype=np.int32) -> np.ndarray:
@@ -285,6 +295,33 @@ class Batch:
             raise status_exception(rc, self.ctx.last_error())
         return float(ms.value), int(nl.value)
 
+    def score_fetch(self, scheme, align_type: str, variant: str = "auto", dest=None, timed: bool = True):
+        """score() + fetch_scores() in one native call: the results of pieces that have finished travel back while later
+        pieces are still uploading and running.  Returns (kernel_ms, launches, (score, end_i, end_j, status))."""
+        n = self.n_pairs
+        if dest is not None:
+            score, ei, ej = dest
+            assert all(a.dtype == np.int32 and a.flags.c_contiguous and len(a) == n for a in dest)
+        else:
+            score, ei, ej = (pinned_empty(n) for _ in range(3)) if n >= 65536 else (np.empty(n, np.int32) for _ in range(3))
+        s = scheme_struct(scheme)
+        ms = ctypes.c_float(0.0)
+        nl = ctypes.c_int32(0)
+        rc = self._lib.wsb_batch_score_fetch(self._h, ctypes.byref(s), ALIGN_TYPE_ID[align_type], VARIANT_ID[variant],
+                                             ctypes.byref(ms) if timed else None, ctypes.byref(nl), _ptr(score), _ptr(ei), _ptr(ej),
+                                             None)
+        if rc:
+            raise status_exception(rc, self.ctx.last_error())
+        self.has_faults = bool(self._lib.wsb_batch_has_faults(self._h))
+        if self.has_faults:
+            status = np.empty(n, np.int32)
+            rc = self._lib.wsb_batch_fetch_scores(self._h, _ptr(score), _ptr(ei), _ptr(ej), _ptr(status))
+            if rc:
+                raise status_exception(rc, self.ctx.last_error())
+        else:
+            status = zeros_view(n)
+        return float(ms.value), int(nl.value), (score, ei, ej, status)
+
     def fetch_scores(self, dest=None):
         """(score, end_i, end_j, status).  dest: three preallocated int32 arrays of n_pairs elements to download into (the
         multi-GPU runner passes slices of the job-wide result arrays, so shard results land in place)."""
@@ -302,7 +339,7 @@ class Batch:
         if rc:
             raise status_exception(rc, self.ctx.last_error())
         if status is None:
-            status = np.zeros(n, np.int32)  # calloc: costs nothing until somebody reads it
+            status = zeros_view(n)
         return score, ei, ej, status
 
     def plan_stats(self) -> dict:
@@ -354,7 +391,7 @@ class Batch:
                                                  _ptr(status))
         if rc:
             raise status_exception(rc, self.ctx.last_error())
-        out["status"] = status if status is not None else np.zeros(n, np.int32)
+        out["status"] = status if status is not None else zeros_view(n)
         out["cigar"] = cig[:int(off[n])]
         out["cigar_off"] = off
         return out

@@ -205,8 +205,7 @@ def _run_shard(device: int, queries: SequencePool, subjects: SequencePool, pair_
                 out["tb"] = batch.fetch_traceback()
                 out["faults"] = batch.has_faults
             else:
-                out["ms"], out["launches"] = batch.score(scheme, cfg.align_type, variant)
-                out["scores"] = batch.fetch_scores(dest)
+                out["ms"], out["launches"], out["scores"] = batch.score_fetch(scheme, cfg.align_type, variant, dest)
                 out["faults"] = batch.has_faults
         finally:
             batch.close()
@@ -305,7 +304,7 @@ def run_batch(job: BatchJob) -> BatchReport:
     if single and cfg.result_mode != "traceback":  # one shard: the fetched arrays are the result arrays
         score, qe, se, status = outs[0]["scores"]
         if cfg.align_type == "global":   # the kernels report (m, n) as the end cell
-            qs = np.zeros(n, np.int32); ss = qs
+            qs = N.zeros_view(n); ss = qs
         else:
             qs, ss = qe, se
     elif in_place:
@@ -348,9 +347,9 @@ def run_batch(job: BatchJob) -> BatchReport:
                 if len(idx):
                     status[int(idx[0]):int(idx[-1]) + 1] = out["scores"][3]
         else:
-            status = np.zeros(n, np.int32)   # calloc: costs nothing until somebody reads it
+            status = N.zeros_view(n)
         if cfg.align_type == "global":
-            qs = np.zeros(n, np.int32); ss = qs
+            qs = N.zeros_view(n); ss = qs
         else:
             qs, ss = qe, se
     else:

@@ -2,6 +2,7 @@
 // and the C ABI declared in include/wsb200.h.  No CPU compute path exists here: every alignment runs in the CUDA
 // kernels of score_kernels.cuh / traceback_kernels.cuh.
 #include "../../include/wsb200.h"
+#include <chrono>
 #include "score_kernels.cuh"
 #include "score_short.cuh"
 #include "score_long.cuh"
@@ -31,6 +32,8 @@ struct wsb_ctx {
     int sm_count = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;  // host-to-device uploads of a batch run here, overlapping the kernels of earlier pieces
+    cudaStream_t dl_stream = nullptr;    // device-to-host result downloads of finished pieces (wsb_batch_score_fetch)
+    cudaEvent_t dl_ev[16] = {};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // launch groups of the long-read kernel run side by side on these streams (fork after ev0, join before ev1)
     static constexpr int kAux = 6;
@@ -268,6 +271,11 @@ extern "C" int wsb_ctx_create(int device, wsb_ctx** out) {
         cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        // created third, before the six launch-group streams: a process has 8 hardware connections by default
+        // (CUDA_DEVICE_MAX_CONNECTIONS) and streams beyond that share one; a download stream that shares the upload stream's
+        // connection queues every later upload piece behind a download that is waiting for its kernel (measured: the
+        // piecewise pipeline degrades to upload + kernel, 18 -> 22 ms per 4 M pairs)
+        cudaStreamCreateWithFlags(&c->dl_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
         (void)cudaGetLastError();
         delete c;
@@ -298,6 +306,8 @@ extern "C" void wsb_ctx_destroy(wsb_ctx* c) {
     if (c->d_cflags) cudaFree(c->d_cflags);
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    if (c->dl_stream) cudaStreamDestroy(c->dl_stream);
+    for (cudaEvent_t e : c->dl_ev) if (e) cudaEventDestroy(e);
     delete c;
 }
 
@@ -1112,8 +1122,25 @@ static int check_scheme(const wsb_scheme* s, int atype) {
 
 // plan_only: build (or reuse) the plan and resolve empty-side pairs, but launch no score kernel (the traceback fill of
 // global / semiglobal alignments produces score and end cell itself)
+struct FetchDst { int32_t* score = nullptr; int32_t* i = nullptr; int32_t* j = nullptr; bool done = false; bool mapped = false; };
+
+// 16-byte vector copies of three result arrays into page-locked host memory (unified addressing: same pointer on the device)
+__global__ void results_home_kernel(const int32_t* s0, const int32_t* s1, const int32_t* s2, int32_t* d0, int32_t* d1, int32_t* d2,
+                                    int64_t n) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x, first = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool vec = ((reinterpret_cast<uintptr_t>(s0) | reinterpret_cast<uintptr_t>(s1) | reinterpret_cast<uintptr_t>(s2) |
+                       reinterpret_cast<uintptr_t>(d0) | reinterpret_cast<uintptr_t>(d1) | reinterpret_cast<uintptr_t>(d2)) & 15) == 0;
+    const int64_t n4 = vec ? n / 4 : 0;
+    for (int64_t k = first; k < n4; k += stride) {
+        reinterpret_cast<int4*>(d0)[k] = reinterpret_cast<const int4*>(s0)[k];
+        reinterpret_cast<int4*>(d1)[k] = reinterpret_cast<const int4*>(s1)[k];
+        reinterpret_cast<int4*>(d2)[k] = reinterpret_cast<const int4*>(s2)[k];
+    }
+    for (int64_t k = n4 * 4 + first; k < n; k += stride) { d0[k] = s0[k]; d1[k] = s1[k]; d2[k] = s2[k]; }
+}
+
 static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int variant, float* kernel_ms,
-                            int32_t* n_launches, bool plan_only) {
+                            int32_t* n_launches, bool plan_only, FetchDst* fetch = nullptr) {
     if (!b) return WSB_E_ARG;
     std::lock_guard<std::recursive_mutex> lock_(b->ctx->mu);
     int rc = check_scheme(sch, atype);
@@ -1306,6 +1333,17 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
                 geo[k].fn<<<grid, kThreads, geo[k].smem, ctx->stream>>>(prm);
                 CUDA_TRY(ctx, cudaGetLastError());
                 ++launches;
+                if (fetch && fetch->score && fetch->mapped && pc < 16) {   // results of this piece go home while later pieces upload and run
+                    if (!ctx->dl_ev[pc]) CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->dl_ev[pc], cudaEventDisableTiming));
+                    CUDA_TRY(ctx, cudaEventRecord(ctx->dl_ev[pc], ctx->stream));
+                    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->dl_stream, ctx->dl_ev[pc], 0));
+                    // a small kernel stores the piece into the page-locked (device-visible) destination: a copy-engine
+                    // download would queue behind the batch's own pending uploads and block this thread until they drained
+                    results_home_kernel<<<32, 256, 0, ctx->dl_stream>>>(b->d_score + lo, b->d_i + lo, b->d_j + lo, fetch->score + lo,
+                                                                        fetch->i + lo, fetch->j + lo, hi - lo);
+                    CUDA_TRY(ctx, cudaGetLastError());
+                    fetch->done = true;
+                }
             }
             continue;
         }
@@ -1387,11 +1425,63 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
         }
     }
     CUDA_TRY(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+    if (fetch && fetch->score && !plan_only) {
+        const size_t bytes = sizeof(int32_t) * (size_t)b->n_pairs;
+        bool refetch = !fetch->done;
+        if (fetch->done) {   // pieces went home early; pairs a packed kernel handed back were re-scored after that
+            int32_t handed_back = 0;
+            static const bool trace = getenv("WSB_TRACE") != nullptr;
+            const auto t_a = std::chrono::steady_clock::now();
+            if (b->d_redo) CUDA_TRY(ctx, cudaMemcpyAsync(&handed_back, b->d_redo, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+            CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+            const auto t_b = std::chrono::steady_clock::now();
+            CUDA_TRY(ctx, cudaStreamSynchronize(ctx->dl_stream));
+            if (trace) {
+                const auto t_c = std::chrono::steady_clock::now();
+                fprintf(stderr, "[wsb] score_fetch: wait for kernels %.2f ms, then for downloads %.2f ms\n",
+                        std::chrono::duration<double, std::milli>(t_b - t_a).count(), std::chrono::duration<double, std::milli>(t_c - t_b).count());
+            }
+            bool any_empty = b->uniform ? (b->m[0] == 0 || b->n[0] == 0) : true;
+            refetch = handed_back > 0 || any_empty;
+        }
+        if (refetch) {
+            CUDA_TRY(ctx, cudaMemcpyAsync(fetch->score, b->d_score, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+            CUDA_TRY(ctx, cudaMemcpyAsync(fetch->i, b->d_i, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+            CUDA_TRY(ctx, cudaMemcpyAsync(fetch->j, b->d_j, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+            CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+        }
+    }
     if (kernel_ms) {
         CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev1));
         CUDA_TRY(ctx, cudaEventElapsedTime(kernel_ms, ctx->ev0, ctx->ev1));
     }
     if (n_launches) *n_launches = launches;
+    return WSB_OK;
+}
+
+// Score and download in one call: when the batch is still uploading piece by piece, the results of every finished piece
+// travel back on a third stream while later pieces upload and run (PCIe is full duplex), so the download of the step hides
+// behind its upload instead of following it.  Same results and status contract as wsb_batch_score + wsb_batch_fetch_scores.
+extern "C" int wsb_batch_score_fetch(wsb_batch* b, const wsb_scheme* sch, int atype, int variant, float* kernel_ms,
+                                     int32_t* n_launches, int32_t* out_score, int32_t* out_i, int32_t* out_j, int32_t* status) {
+    if (!b || !out_score || !out_i || !out_j) return WSB_E_ARG;
+    std::lock_guard<std::recursive_mutex> lock_(b->ctx->mu);
+    FetchDst dst;
+    dst.score = out_score; dst.i = out_i; dst.j = out_j;
+    {   // early piece downloads need a destination the device can write: page-locked host memory
+        cudaPointerAttributes a0 = {}, a1 = {}, a2 = {};
+        dst.mapped = cudaPointerGetAttributes(&a0, out_score) == cudaSuccess && a0.type == cudaMemoryTypeHost &&
+                     cudaPointerGetAttributes(&a1, out_i) == cudaSuccess && a1.type == cudaMemoryTypeHost &&
+                     cudaPointerGetAttributes(&a2, out_j) == cudaSuccess && a2.type == cudaMemoryTypeHost;
+        (void)cudaGetLastError();
+    }
+    const int rc = batch_score_impl(b, sch, atype, variant, kernel_ms, n_launches, false, &dst);
+    if (rc) return rc;
+    if (status) {
+        const size_t bytes = sizeof(int32_t) * (size_t)b->n_pairs;
+        if (b->last_plan) std::memcpy(status, b->last_plan->status.data(), bytes);
+        else std::memset(status, 0, bytes);
+    }
     return WSB_OK;
 }
 
