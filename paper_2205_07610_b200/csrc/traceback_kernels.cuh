@@ -318,7 +318,9 @@ struct TbCursor {
     __device__ __forceinline__ uint32_t at(int i) const {   // code of cell (i, current column), as tb_code_at returns it
         const int it = i + t;
         const int64_t entry = lane_major ? ((int64_t)st * P + t) * rows4 + (it - 1) : ((int64_t)st * (m + P - 1) + (it - 1)) * P + t;
-        const uint32_t bits = __ldcg(code + entry * NW + (c >> 3)) >> (c & 7);
+        // read-only path through L1: with the lane-major layout the next three steps up or diagonal hit the sector this load
+        // brings in (the codes were written by an earlier kernel, so the non-coherent path is safe)
+        const uint32_t bits = (lane_major ? __ldg(code + entry * NW + (c >> 3)) : __ldcg(code + entry * NW + (c >> 3))) >> (c & 7);
         const bool pd = bits & 1u, pm = bits & 0x100u;
         const uint32_t origin = pm ? (pd ? 1u : 2u) : ((LOCAL && pd) ? 0u : 3u);
         return origin | ((bits >> 14) & 4u) | ((bits >> 21) & 8u);
