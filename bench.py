@@ -386,7 +386,7 @@ def main():
             _ = int(rep_p.results.score[0]) if isinstance(rep_p.results, W.ResultArray) else rep_p.results[0].score
         dt = time.perf_counter() - t0
         e2e_packed = {"value": cells * e2e_steps / dt / 1e9, "unit": "GCUPS", "h2d_bytes_per_step": int(rep_p.h2d_bytes),
-                      "d2h_bytes_per_step": int(rep_p.d2h_bytes), "steps": e2e_steps,
+                      "d2h_bytes_per_step": int(rep_p.d2h_bytes), "steps": e2e_steps, "run_batch_wall_ms": rep_p.wall_time * 1e3,
                       "host_format": "2-bit packed pools (the reference's Sequence.data layout), packed outside the timed region"}
 
     sharded = None
