@@ -78,6 +78,14 @@ int wsb_ctx_create(int device, wsb_ctx** out);
 void wsb_ctx_destroy(wsb_ctx* ctx);
 const char* wsb_last_error(const wsb_ctx* ctx);
 int wsb_ctx_sm_count(const wsb_ctx* ctx);
+/* Host threads that pack large one-byte-per-symbol pools (>= 262144 pairs and >= 32 MB: the piecewise upload) into the 2-bit
+ * layout before they cross the bus -- a quarter of the bytes; the kernels of a piece start as soon as its slice is expanded on
+ * the device.  Flagged symbols have no 2-bit code: a slice that holds one travels as plain bytes.  threads = 0 switches the
+ * packing off (pools go up as they are: the better choice when several GPUs, each behind its own PCIe link, share the host
+ * cores), -1 restores the default (WSB_HOST_PACK_THREADS, else min(16, cores - 1)).  No counterpart in the reference (its
+ * workers read host memory in place, batch.py:213-240). */
+int wsb_ctx_set_host_pack_threads(wsb_ctx* ctx, int threads);
+const char* wsb_host_pack_isa(void);   /* "avx512bw", "bmi2" or "plain": the packing body the running CPU selected */
 
 /* ---- resident-batch API ---- */
 

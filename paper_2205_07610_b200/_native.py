@@ -26,6 +26,7 @@ EXPORTED_SYMBOLS = (
     "wsb_traceback_batch", "wsb_merged_state_exact", "wsb_f16_range_ok", "wsb_plan_shards", "wsb_batch_has_faults", "wsb_pinned_alloc",
     "wsb_pinned_free", "wsb_batch_total_runs", "wsb_batch_h2d_bytes", "wsb_compact_pool", "wsb_batch_kernel_cycles",
     "wsb_batch_set_tb_scratch", "wsb_batch_tb_info", "wsb_batch_plan_stats", "wsb_batch_score_fetch",
+    "wsb_ctx_set_host_pack_threads", "wsb_host_pack_isa",
 )
 
 
@@ -61,6 +62,8 @@ def load():
     lib.wsb_ctx_destroy.argtypes = [p]
     lib.wsb_ctx_destroy.restype = None
     lib.wsb_ctx_sm_count.argtypes = [p]
+    lib.wsb_ctx_set_host_pack_threads.argtypes = [p, ci]
+    lib.wsb_host_pack_isa.restype = ctypes.c_char_p
     lib.wsb_batch_create.argtypes = [p, p, p, p, i64, p, p, p, i64, p, p, i64, p]
     lib.wsb_batch_create_async.argtypes = [p, p, p, p, i64, p, p, p, i64, p, p, i64, p]
     lib.wsb_batch_create_packed_async.argtypes = [p, p, p, i64, p, p, i64, p, p, i64, p, p, i64, p, p, i64, p]
@@ -203,6 +206,12 @@ class Context:
     def last_error(self) -> str:
         return self._lib.wsb_last_error(self._h).decode()
 
+    def set_host_pack_threads(self, threads: int) -> None:
+        """Host threads that pack large byte pools into the 2-bit layout before upload (0: off, -1: library default)."""
+        rc = self._lib.wsb_ctx_set_host_pack_threads(self._h, int(threads))
+        if rc:
+            raise status_exception(rc, "host_pack_threads")
+
     def close(self):
         if getattr(self, "_h", None):
             self._lib.wsb_ctx_destroy(self._h)
@@ -217,6 +226,14 @@ class Context:
 
 class Batch:
     """Device-resident pools + pair list (wsb_batch)."""
+
+    _h2d_final = 0
+
+    @property
+    def h2d_bytes(self) -> int:
+        """Bytes that crossed the bus for this batch so far (regular metadata is generated on the device; host-packed
+        pools count as packed).  Final once the first score / traceback call has returned."""
+        return int(self._lib.wsb_batch_h2d_bytes(self._h)) if getattr(self, "_h", None) else self._h2d_final
 
     def __init__(self, ctx: Context, q_codes, q_off, q_len, s_codes, s_off, s_len, pair_q, pair_s, packed=None):
         """packed = ((q_packed, q_flag_pos), (s_packed, s_flag_pos)): both pools in the 2-bit layout (four symbols per
@@ -249,7 +266,6 @@ class Batch:
             self._keep = None
             raise status_exception(rc, ctx.last_error())
         self._h = h
-        self.h2d_bytes = int(self._lib.wsb_batch_h2d_bytes(h))   # what actually crossed the bus (regular metadata is generated on the device)
 
     @classmethod
     def uniform(cls, ctx: Context, q_pool, q_len: int, s_pool, s_len: int, n_pairs: int, packed: bool = False) -> "Batch":
@@ -270,7 +286,6 @@ class Batch:
             self._keep = None
             raise status_exception(rc, ctx.last_error())
         self._h = h
-        self.h2d_bytes = int(self._lib.wsb_batch_h2d_bytes(h))
         return self
 
     @property
@@ -398,6 +413,7 @@ class Batch:
 
     def close(self):
         if getattr(self, "_h", None):
+            self._h2d_final = int(self._lib.wsb_batch_h2d_bytes(self._h))
             self._lib.wsb_batch_destroy(self._h)
             self._h = None
         self._keep = None

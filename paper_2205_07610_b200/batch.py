@@ -179,10 +179,33 @@ def _variant_for(job: BatchJob, cfg: AlignConfig) -> str:
     return env if env in ("auto", "f16x2", "i32") else "auto"
 
 
+def _host_pack_policy() -> int:
+    """Host threads for the packed upload of a single-shard job: the library default (-1: min(16, cores)) when this process
+    has the host to itself, 0 (plain uploads) when torchrun runs one rank per GPU on it -- every rank has its own PCIe link
+    but they all share the cores.  Jobs sharded over several devices never pack (same reason).  WSB_HOST_PACK_THREADS overrides."""
+    if os.environ.get("WSB_HOST_PACK_THREADS") is not None:
+        return -1
+    try:
+        ranks = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+    except ValueError:
+        ranks = 1
+    return -1 if ranks <= 1 else 0
+
+
+def host_pack_info() -> dict:
+    """What the packed upload of a single-shard job would use in this process: {"threads": default (-1), forced count or 0
+    (off), "isa": packing body of the running CPU}."""
+    env = os.environ.get("WSB_HOST_PACK_THREADS")
+    return {"threads": int(env) if env is not None else _host_pack_policy(), "isa": N.load().wsb_host_pack_isa().decode(),
+            "cores": os.cpu_count()}
+
+
 def _run_shard(device: int, queries: SequencePool, subjects: SequencePool, pair_q: np.ndarray, pair_s: np.ndarray,
-               cfg: AlignConfig, scheme: ScoringScheme, variant: str, out: dict, regular: bool = False, dest=None):
+               cfg: AlignConfig, scheme: ScoringScheme, variant: str, out: dict, regular: bool = False, dest=None,
+               host_pack: int = -1):
     try:
         ctx = get_context(device)
+        ctx.set_host_pack_threads(host_pack)
         both_packed = queries.packed is not None and subjects.packed is not None
         no_flags = both_packed and not (queries.flag_pos is not None and len(queries.flag_pos)) and \
             not (subjects.flag_pos is not None and len(subjects.flag_pos))
@@ -198,7 +221,6 @@ def _run_shard(device: int, queries: SequencePool, subjects: SequencePool, pair_
             batch = N.Batch(ctx, queries.codes, queries.off, queries.len, subjects.codes, subjects.off, subjects.len,
                             pair_q, pair_s)
         try:
-            out["h2d"] = batch.h2d_bytes
             out["cells"] = batch.total_cells
             if cfg.result_mode == "traceback":
                 out["ms"], out["launches"] = batch.traceback(scheme, cfg.align_type)
@@ -207,6 +229,7 @@ def _run_shard(device: int, queries: SequencePool, subjects: SequencePool, pair_
             else:
                 out["ms"], out["launches"], out["scores"] = batch.score_fetch(scheme, cfg.align_type, variant, dest)
                 out["faults"] = batch.has_faults
+            out["h2d"] = batch.h2d_bytes   # read after the run: a host-packed upload counts its bytes as the pieces are queued
         finally:
             batch.close()
     except BaseException as exc:  # re-raised by the caller in the submitting thread
@@ -224,7 +247,7 @@ def _run_sliced_shard(device: int, queries: SequencePool, subjects: SequencePool
             lo, hi = int(idx[0]), int(idx[-1]) + 1
             q_sub, s_sub = queries.slice_uniform(lo, hi), subjects.slice_uniform(lo, hi)
             ident = np.arange(hi - lo, dtype=np.int32)
-            return _run_shard(device, q_sub, s_sub, ident, ident, cfg, scheme, variant, out, True, dest)
+            return _run_shard(device, q_sub, s_sub, ident, ident, cfg, scheme, variant, out, True, dest, host_pack=0)
         pq, ps = pair_q[idx], pair_s[idx]
 
         def cut(pool, col):
@@ -235,7 +258,7 @@ def _run_sliced_shard(device: int, queries: SequencePool, subjects: SequencePool
         q_sub, pq = cut(queries, pq)
         s_sub, ps = cut(subjects, ps)
         _run_shard(device, q_sub, s_sub, np.ascontiguousarray(pq, np.int32), np.ascontiguousarray(ps, np.int32), cfg, scheme,
-                   variant, out, False)
+                   variant, out, False, host_pack=0)
     except BaseException as exc:
         out["error"] = exc
 
@@ -285,7 +308,7 @@ def run_batch(job: BatchJob) -> BatchReport:
         if len(idx) == 0:
             continue
         if len(devices) == 1:  # no thread hop for the common single-GPU case
-            _run_shard(dev, queries, subjects, pair_q, pair_s, cfg, job.scheme, variant, out, regular)
+            _run_shard(dev, queries, subjects, pair_q, pair_s, cfg, job.scheme, variant, out, regular, host_pack=_host_pack_policy())
             continue
         dest = tuple(a[int(idx[0]):int(idx[-1]) + 1] for a in whole) if in_place else None
         th = threading.Thread(target=_run_sliced_shard, name=f"waveseq-gpu-{dev}",

@@ -9,8 +9,8 @@ PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG_DIR, "csrc")
 LIB_PATH = os.path.join(PKG_DIR, "libwsb200.so")
 # translation units and their extra flags: the packed int16 short-read kernels are built with ptxas -O1 (see wsb200_s16.cu)
-SOURCES = {"wsb200.cu": [], "wsb200_s16.cu": ["-Xptxas", "-O1"]}
-DEPS = ["wsb200.cu", "wsb200_s16.cu", "score_kernels.cuh", "score_short.cuh", "score_short16.cuh", "score_short16g.cuh",
+SOURCES = {"wsb200.cu": [], "wsb200_s16.cu": ["-Xptxas", "-O1"], "hostpack.cpp": []}
+DEPS = ["wsb200.cu", "wsb200_s16.cu", "hostpack.cpp", "hostpack.h", "score_kernels.cuh", "score_short.cuh", "score_short16.cuh", "score_short16g.cuh",
         "score_long.cuh", "score_long16.cuh", "traceback_kernels.cuh", "traceback_fill16.cuh", "traceback_host.inl",
         "traceback_band.cuh", "traceback_band_host.inl", os.path.join("..", "..", "include", "wsb200.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC"]
@@ -33,7 +33,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None) ->
 
         def compile_one(item):
             src, flags = item
-            obj = os.path.join(objdir, src.replace(".cu", ".o"))
+            obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
             cmd = [nvcc, *extra, *NVCC_FLAGS, *flags, *(["-Xptxas=-v"] if verbose else []), "-c", "-o", obj, os.path.join(CSRC, src)]
             subprocess.check_call(cmd, cwd=CSRC)
             return obj

@@ -258,7 +258,7 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
         prm.tb_p = P; prm.tb_k = K; prm.one = 1; prm.run_tmp = d_run_tmp;
         prm.lane_major = fill16 ? 1 : 0;
 
-        if (by_piece) TB_TRY(cudaStreamWaitEvent(ctx->stream, b->piece_ev[piece], 0));
+        if (by_piece) TB_TRY(b->wait_piece(ctx->stream, piece));
         TB_TRY(cudaEventRecord(e0, ctx->stream));
         if (fill16) {
             const int64_t units = (count + 1) / 2;

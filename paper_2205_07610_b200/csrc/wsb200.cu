@@ -18,11 +18,15 @@
 #include <mutex>
 #include <new>
 #include <numeric>
+#include <atomic>
+#include <condition_variable>
 #include <string>
 #include <thread>
 #include <tuple>
 #include <type_traits>
 #include <vector>
+
+#include "hostpack.h"
 
 using namespace wsb;
 
@@ -42,6 +46,9 @@ struct wsb_ctx {
     unsigned int* d_queues = nullptr;  // work-queue heads of the long-read launches
     int32_t* d_cflags = nullptr;       // cluster launches of the long-read kernel: 160 ints per cluster
     std::string last_error;
+    // Host threads that pack large byte pools into the 2-bit layout before they cross the bus (hostpack.cpp); 0 = pools go up
+    // as they are.  -1 = default: WSB_HOST_PACK_THREADS, else min(16, cores - 1).  wsb_ctx_set_host_pack_threads overrides.
+    int host_pack_threads = -1;
     // One context serves every host thread that aligns on its GPU (the reference runs independent alignments
     // concurrently, batch.py:213-240): each entry point that touches the context's streams, events, queues or block
     // cache holds this lock for its whole duration.  Recursive: the one-shot calls nest the batch calls.
@@ -104,8 +111,49 @@ struct Plan {
     int64_t st_q_max = 0, st_q_add = 0, st_q_lookup = 0;   // thread-instructions x 4 (packed kernels advance two cells per instruction)
 };
 
+// Host-packed upload of a batch whose pools arrive as one-byte codes: T worker threads turn each upload piece into the
+// 2-bit layout inside a page-locked staging block; whichever worker finishes a piece last queues its copy, the expanding
+// kernel and the piece's event on the copy stream (pieces complete in order: every worker walks them in order).  A
+// consumer that wants to wait for piece k on a stream first waits, on the host, until that event HAS been recorded
+// (cudaStreamWaitEvent on an event nobody recorded yet returns at once).  A slice with a flagged symbol (no 2-bit
+// encoding) goes up as plain bytes.
+struct HostPacker {
+    static constexpr int kMaxPieces = 16;
+    std::vector<std::thread> workers;
+    std::mutex mu;
+    std::condition_variable cv;
+    int queued = 0;                       // packed pieces whose event is recorded (guarded by mu); they complete in order
+    int n_packed = 0;                     // pieces 0 .. n_packed-1 are packed; the rest go up as plain bytes, a chunk behind every
+                                          // packed piece (all of them queued once the last packed piece is)
+    std::atomic<int> done[kMaxPieces];    // workers that finished piece k
+    std::atomic<int> flagged[kMaxPieces][2];
+    bool raw_done[kMaxPieces] = {};       // plain-byte pieces whose event is recorded (touched by the queueing worker only)
+    std::atomic<int> error{0};            // first cudaError_t a worker saw
+    std::atomic<long long> bytes{0};      // bytes queued for the bus
+    void* host_stage = nullptr;           // page-locked, from wsb_pinned_alloc
+    HostPacker() { for (auto& d : done) d.store(0); for (auto& f : flagged) { f[0].store(0); f[1].store(0); } }
+    void wait_queued(int k) { const int need = std::min(k, n_packed - 1); std::unique_lock<std::mutex> lk(mu); cv.wait(lk, [&] { return queued > need; }); }
+    void join() { for (auto& t : workers) if (t.joinable()) t.join(); workers.clear(); }
+};
+extern "C" int wsb_pinned_alloc(size_t bytes, void** out);
+extern "C" void wsb_pinned_free(void* p);
+
 struct wsb_batch {
     wsb_ctx* ctx = nullptr;
+    HostPacker* packer = nullptr;
+    // stream `s` waits for upload piece k (host-packed uploads: the piece's event is first awaited on the host)
+    cudaError_t wait_piece(cudaStream_t s, int k) {
+        if (packer) {
+            packer->wait_queued(k);
+            if (packer->error.load()) return (cudaError_t)packer->error.load();
+        }
+        return cudaStreamWaitEvent(s, piece_ev[k], 0);
+    }
+    void finish_packer() {   // all pieces queued; bytes accounted
+        if (!packer) return;
+        packer->join();
+        h2d_bytes += packer->bytes.exchange(0);
+    }
     int64_t n_q = 0, n_s = 0, n_pairs = 0;
     uint8_t *d_qcodes = nullptr, *d_scodes = nullptr;
     int64_t *d_qoff = nullptr, *d_soff = nullptr;
@@ -313,6 +361,13 @@ extern "C" void wsb_ctx_destroy(wsb_ctx* c) {
 
 extern "C" const char* wsb_last_error(const wsb_ctx* c) { return c ? c->last_error.c_str() : "null context"; }
 extern "C" int wsb_ctx_sm_count(const wsb_ctx* c) { return c ? c->sm_count : 0; }
+extern "C" int wsb_ctx_set_host_pack_threads(wsb_ctx* c, int threads) {
+    if (!c || threads < -1) return WSB_E_ARG;
+    std::lock_guard<std::recursive_mutex> lock_(c->mu);
+    c->host_pack_threads = threads;
+    return WSB_OK;
+}
+extern "C" const char* wsb_host_pack_isa(void) { return hostpack_isa(); }
 
 // ------------------------------------------------------------------------------------------------ batch
 // Metadata arrays of regular batches (equal-length reads laid out back to back, pair i = (i, i)) are arithmetic
@@ -350,8 +405,10 @@ extern "C" void wsb_batch_destroy(wsb_batch* b) {
     if (!b) return;
     std::lock_guard<std::recursive_mutex> lock_(b->ctx->mu);
     cudaSetDevice(b->ctx->device);
+    if (b->packer) b->packer->join();    // its workers queue work on the copy stream
     cudaStreamSynchronize(b->ctx->copy_stream);
     cudaStreamSynchronize(b->ctx->stream);
+    if (b->packer) { if (b->packer->host_stage) wsb_pinned_free(b->packer->host_stage); delete b->packer; b->packer = nullptr; }
     for (int k = 0; k < wsb_batch::kMaxPieces; ++k) if (b->piece_ev[k]) cudaEventDestroy(b->piece_ev[k]);
     if (b->d_cycles) b->ctx->release(b->d_cycles);
     for (void* p : {(void*)b->d_qcodes, (void*)b->d_scodes, (void*)b->d_qoff, (void*)b->d_soff, (void*)b->d_qlen,
@@ -488,6 +545,11 @@ static int batch_create_impl(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t
         static const int want = [] { const char* e = getenv("WSB_PIECES"); return e ? atoi(e) : 8; }();   // tuning aid
         n_pieces = std::min<int>(wsb_batch::kMaxPieces, std::max(1, want));
     }
+    // Half-size pieces at both ends (one piece more): the first kernels start after half a piece's upload, and only half a
+    // piece's kernels remain once the last byte has landed.
+    const bool half_ends = n_pieces >= 4 && n_pieces < wsb_batch::kMaxPieces;
+    const int whole_pieces = n_pieces;
+    if (half_ends) ++n_pieces;
     b->n_pieces = n_pieces;
     std::vector<int64_t> need_q((size_t)n_pieces, 0), need_s((size_t)n_pieces, 0);
     {
@@ -502,7 +564,8 @@ static int batch_create_impl(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t
             need_q[k] = mq; need_s[k] = msq;
         };
         for (int k = 0; k < n_pieces; ++k)   // boundaries on multiples of 2048 pairs (packed units never straddle pieces)
-            b->piece_end[k] = k + 1 == n_pieces ? n_pairs : std::min<int64_t>(n_pairs, (n_pairs * (k + 1) / n_pieces + 2047) / 2048 * 2048);
+            b->piece_end[k] = k + 1 == n_pieces ? n_pairs
+                              : std::min<int64_t>(n_pairs, ((half_ends ? n_pairs * (2 * k + 1) / (2 * whole_pieces) : n_pairs * (k + 1) / n_pieces) + 2047) / 2048 * 2048);
         // the arithmetic shortcut holds only for reads stored back to back from offset 0 (always true for the vouched
         // uniform entry); strided or prefixed pools with an identity pair list take the scan below
         const bool back_to_back = regular && ap_off[0] && o0[0] == 0 && od[0] == l0[0] && ap_off[1] && o0[1] == 0 && od[1] == l0[1];
@@ -551,8 +614,145 @@ static int batch_create_impl(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t
         unpack2_kernel<<<(unsigned)((b1 - b0 + 255) / 256), 256, 0, ctx->copy_stream>>>(stage + b0, b0, lo, hi, dst);
         return cudaGetLastError();
     };
+    // Host-packed upload: byte pools of a piecewise batch are packed by worker threads, piece by piece (see HostPacker)
+    int pack_threads = 0;
+    if (!pk.q_packed && !pk.s_packed && n_pieces > 1) {
+        pack_threads = ctx->host_pack_threads;
+        if (pack_threads < 0) {
+            static const int dflt = [] {
+                const char* ev = getenv("WSB_HOST_PACK_THREADS");
+                // one core stays free for the thread that launches the kernels of the pieces as they land (cfg2 on 16 cores:
+                // 20.2 ms per call with 15 packers, 21-24 ms with 16)
+                const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+                return ev ? atoi(ev) : (int)std::min(16u, hw > 2 ? hw - 1 : hw);
+            }();
+            pack_threads = dflt;
+        }
+        pack_threads = std::max(0, std::min(pack_threads, 64));
+    }
+    if (pack_threads > 0) {
+        const int64_t qb = q_total / 4 + 2, sb = s_total / 4 + 2;
+        if ((e = ctx->alloc((void**)&stage_q, (size_t)qb)) != cudaSuccess) return fail(e);
+        if ((e = ctx->alloc((void**)&stage_s, (size_t)sb)) != cudaSuccess) return fail(e);
+        b->stage_blocks[0] = stage_q; b->stage_blocks[1] = stage_s;
+        for (int k = 0; k < n_pieces; ++k)
+            if ((e = cudaEventCreateWithFlags(&b->piece_ev[k], cudaEventDisableTiming)) != cudaSuccess) return fail(e);
+        HostPacker* hp = new (std::nothrow) HostPacker();
+        if (!hp) return fail(cudaErrorMemoryAllocation);
+        b->packer = hp;
+        if (wsb_pinned_alloc((size_t)(qb + sb), &hp->host_stage) != WSB_OK) return fail(cudaErrorMemoryAllocation);
+        uint8_t* const hq = static_cast<uint8_t*>(hp->host_stage);
+        uint8_t* const hs = hq + qb;
+        // metadata queued above (and everything else on the copy stream so far) precedes piece 0's event, as before
+        const int T = pack_threads;
+        const int device = ctx->device;
+        cudaStream_t cs = ctx->copy_stream;
+        // WSB_HOST_PACK_RAW=r lets the last r pieces travel as plain bytes meanwhile, in chunks queued behind each packed piece.
+        // Off by default: on the bench host the copy engine's reads and the packers' reads share the memory system, and
+        // every mix measured slower than packing everything (cfg2, 16 threads: 20.6 ms packed, 23-25 ms with 1-3 plain
+        // pieces, 24.3 ms all plain).
+        static const int raw_env = [] { const char* ev = getenv("WSB_HOST_PACK_RAW"); return ev ? atoi(ev) : 0; }();
+        int n_raw = raw_env;
+        n_raw = std::max(0, std::min(n_raw, n_pieces - 1));
+        const int n_packed = n_pieces - n_raw;
+        hp->n_packed = n_packed;
+        uint8_t *dq = b->d_qcodes, *dsc = b->d_scodes;
+        cudaEvent_t* evs = b->piece_ev;
+        static const bool trace = getenv("WSB_TRACE") != nullptr;
+        const auto t_start = std::chrono::steady_clock::now();
+        auto worker = [=](int t) {
+            int64_t lo[2] = {0, 0};       // symbols of either pool already covered by earlier pieces
+            for (int k = 0; k < n_packed; ++k) {
+                const int64_t hi[2] = {std::max(lo[0], need_q[k]), std::max(lo[1], need_s[k])};
+                int64_t pb0[2], pb1[2];   // packed bytes this piece adds (a byte shared with the previous piece stays as it is)
+                for (int v = 0; v < 2; ++v) {
+                    pb0[v] = (lo[v] + 3) / 4; pb1[v] = (hi[v] + 3) / 4;
+                    if (pb1[v] > pb0[v]) {
+                        const int64_t span = pb1[v] - pb0[v];
+                        const int64_t a = pb0[v] + span * t / T / 64 * 64, z = t + 1 == T ? pb1[v] : pb0[v] + span * (t + 1) / T / 64 * 64;
+                        if (z > a && hostpack_range(v ? s_codes : q_codes, v ? s_total : q_total, v ? hs : hq, a, z)) hp->flagged[k][v].store(1);
+                    }
+                }
+                if (hp->done[k].fetch_add(1) + 1 == T) {   // last one out queues the piece
+                    cudaError_t ce = cudaSetDevice(device);
+                    for (int v = 0; v < 2 && ce == cudaSuccess; ++v) {
+                        if (hi[v] <= lo[v]) continue;
+                        const uint8_t* codes = v ? s_codes : q_codes;
+                        uint8_t* dst = v ? dsc : dq;
+                        if (hp->flagged[k][v].load()) {   // a flagged symbol: this slice travels as plain bytes
+                            hp->bytes += hi[v] - lo[v];
+                            ce = cudaMemcpyAsync(dst + lo[v], codes + lo[v], (size_t)(hi[v] - lo[v]), cudaMemcpyHostToDevice, cs);
+                            continue;
+                        }
+                        uint8_t* hst = v ? hs : hq;
+                        uint8_t* dstage = v ? stage_s : stage_q;
+                        if (pb1[v] > pb0[v]) {
+                            hp->bytes += pb1[v] - pb0[v];
+                            ce = cudaMemcpyAsync(dstage + pb0[v], hst + pb0[v], (size_t)(pb1[v] - pb0[v]), cudaMemcpyHostToDevice, cs);
+                            if (ce != cudaSuccess) break;
+                        }
+                        // a byte shared with the previous piece is on the device already -- unless that piece's slice went up
+                        // as plain bytes (flagged): then the few symbols of the shared byte are copied as bytes too
+                        const int64_t u0 = lo[v] / 4, u1 = (hi[v] + 3) / 4;
+                        int64_t sym_lo = lo[v];
+                        if (u0 < pb0[v] && k > 0 && hp->flagged[k - 1][v].load()) {
+                            const int64_t edge = std::min(hi[v], pb0[v] * 4);
+                            hp->bytes += edge - lo[v];
+                            ce = cudaMemcpyAsync(dst + lo[v], codes + lo[v], (size_t)(edge - lo[v]), cudaMemcpyHostToDevice, cs);
+                            if (ce != cudaSuccess) break;
+                            sym_lo = edge;
+                        }
+                        if (hi[v] > sym_lo) {
+                            const int64_t f0 = sym_lo / 4;
+                            unpack2_kernel<<<(unsigned)((u1 - f0 + 255) / 256), 256, 0, cs>>>(dstage + f0, f0, sym_lo, hi[v], dst);
+                            ce = cudaGetLastError();
+                        }
+                    }
+                    if (ce == cudaSuccess) ce = cudaEventRecord(evs[k], cs);
+                    if (n_raw > 0 && ce == cudaSuccess) {
+                        // the plain-byte region (everything behind the last packed piece), cut into n_packed chunks: chunk k
+                        // follows packed piece k on the same stream (one copy engine serves host-to-device traffic, so a
+                        // long plain copy on a second stream would stall the packed pieces behind it)
+                        int64_t r0[2] = {0, 0};
+                        for (int j = 0; j < n_packed; ++j) { r0[0] = std::max(r0[0], need_q[j]); r0[1] = std::max(r0[1], need_s[j]); }
+                        const int64_t tot[2] = {q_total, s_total};
+                        int64_t c_lo[2], c_hi[2];
+                        for (int v = 0; v < 2; ++v) {
+                            const int64_t span = std::max<int64_t>(0, tot[v] - r0[v]);
+                            c_lo[v] = r0[v] + span * k / n_packed; c_hi[v] = k + 1 == n_packed ? tot[v] : r0[v] + span * (k + 1) / n_packed;
+                            if (c_hi[v] > c_lo[v] && ce == cudaSuccess) {
+                                hp->bytes += c_hi[v] - c_lo[v];
+                                ce = cudaMemcpyAsync((v ? dsc : dq) + c_lo[v], (v ? s_codes : q_codes) + c_lo[v], (size_t)(c_hi[v] - c_lo[v]),
+                                                     cudaMemcpyHostToDevice, cs);
+                            }
+                        }
+                        // a plain piece is complete once the chunks up to its end are on the stream
+                        for (int j = n_packed; j < n_pieces && ce == cudaSuccess; ++j) {
+                            const bool now = k + 1 == n_packed || (c_hi[0] >= need_q[j] && c_hi[1] >= need_s[j]);
+                            if (now && !hp->raw_done[j]) { hp->raw_done[j] = true; ce = cudaEventRecord(evs[j], cs); }
+                        }
+                    }
+                    if (ce != cudaSuccess) { int zero = 0; hp->error.compare_exchange_strong(zero, (int)ce); }
+                    { std::lock_guard<std::mutex> lk(hp->mu); hp->queued = k + 1; }
+                    hp->cv.notify_all();
+                    if (trace) fprintf(stderr, "[wsb] host pack: piece %d queued at %.2f ms (%s, %d threads)\n", k,
+                                       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count(), hostpack_isa(), T);
+                }
+                lo[0] = hi[0]; lo[1] = hi[1];
+            }
+        };
+        try {
+            for (int t = 0; t < T; ++t) hp->workers.emplace_back(worker, t);
+        } catch (...) {
+            // could not start every worker: nobody would ever complete a piece.  Let the started ones run out (they only
+            // pack), then fall back to the plain upload below.
+            hp->join();
+            for (auto& d : hp->done) d.store(0);
+            pack_threads = 0;
+        }
+    }
     int64_t done_q = 0, done_s = 0;
-    for (int k = 0; k < n_pieces; ++k) {
+    for (int k = 0; k < n_pieces && pack_threads == 0; ++k) {
         if ((e = send(q_codes, pk.q_packed, stage_q, b->d_qcodes, done_q, need_q[k])) != cudaSuccess) return fail(e);
         done_q = std::max(done_q, need_q[k]);
         if ((e = send(s_codes, pk.s_packed, stage_s, b->d_scodes, done_s, need_s[k])) != cudaSuccess) return fail(e);
@@ -569,8 +769,12 @@ static int batch_create_impl(wsb_ctx* ctx, const uint8_t* q_codes, const int64_t
                 set_flags_kernel<<<(unsigned)((pk.n_s_flags + 255) / 256), 256, 0, ctx->copy_stream>>>(dflags_s, pk.n_s_flags, s_total, b->d_scodes);
             }
         }
-        if ((e = cudaEventCreateWithFlags(&b->piece_ev[k], cudaEventDisableTiming)) != cudaSuccess) return fail(e);
+        if (!b->piece_ev[k] && (e = cudaEventCreateWithFlags(&b->piece_ev[k], cudaEventDisableTiming)) != cudaSuccess) return fail(e);
         if ((e = cudaEventRecord(b->piece_ev[k], ctx->copy_stream)) != cudaSuccess) return fail(e);
+    }
+    if (pack_threads == 0 && b->packer) {   // workers could not be started: plain upload done above
+        if (b->packer->host_stage) wsb_pinned_free(b->packer->host_stage);
+        delete b->packer; b->packer = nullptr;
     }
     // staging areas are only touched by work already queued on the copy stream: hand them back to the cache now, the
     // next user of those blocks is ordered behind this batch on the same streams
@@ -623,6 +827,7 @@ extern "C" int wsb_batch_create(wsb_ctx* ctx, const uint8_t* q_codes, const int6
     std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
     int rc = wsb_batch_create_async(ctx, q_codes, q_off, q_len, n_q, s_codes, s_off, s_len, n_s, pair_q, pair_s, n_pairs, out);
     if (rc) return rc;
+    (*out)->finish_packer();
     cudaError_t e = cudaStreamSynchronize(ctx->copy_stream);  // host arrays may be reused by the caller after return
     if (e != cudaSuccess) { ctx->last_error = cudaGetErrorString(e); wsb_batch_destroy(*out); *out = nullptr; return WSB_E_CUDA; }
     return WSB_OK;
@@ -641,7 +846,7 @@ extern "C" int64_t wsb_batch_kernel_cycles(wsb_batch* b) {
     for (auto v : h) mx = std::max(mx, v);
     return (int64_t)mx;
 }
-extern "C" int64_t wsb_batch_h2d_bytes(const wsb_batch* b) { return b ? b->h2d_bytes : 0; }
+extern "C" int64_t wsb_batch_h2d_bytes(const wsb_batch* b) { return b ? b->h2d_bytes + (b->packer ? (int64_t)b->packer->bytes.load() : 0) : 0; }
 
 extern "C" int wsb_batch_plan_stats(const wsb_batch* b, int64_t* out8) {
     if (!b || !out8 || !b->last_plan) return WSB_E_ARG;
@@ -1252,7 +1457,7 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
     // plan_only (traceback of global / semiglobal batches): the caller fills chunk by chunk and waits per upload piece itself
     const bool defer_upload = plan_only && b->upload_pending && b->n_pieces > 1 && b->n_pieces_usable != 1;
     if (b->upload_pending && !piecewise && !defer_upload && b->n_pieces > 0)
-        CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, b->piece_ev[b->n_pieces - 1], 0));
+        CUDA_TRY(ctx, b->wait_piece(ctx->stream, b->n_pieces - 1));
 
     bool any_s16 = false;
     int s16_gap = GAP_MERGED;
@@ -1326,7 +1531,7 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
             for (int pc = 0; pc < b->n_pieces; ++pc) {
                 const int64_t lo = pc == 0 ? 0 : b->piece_end[pc - 1], hi = b->piece_end[pc];
                 if (hi <= lo) continue;
-                CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, b->piece_ev[pc], 0));
+                CUDA_TRY(ctx, b->wait_piece(ctx->stream, pc));
                 prm.pair_base = lo; prm.n_pairs = hi; prm.n_units = (hi - lo + nv - 1) / nv;
                 const int64_t blocks = (prm.n_units + gpb - 1) / gpb;
                 const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, resident));
@@ -1415,7 +1620,7 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
         if (any_empty) {
             // deferred upload (traceback of a large global / semiglobal batch): the metadata this kernel reads travels on
             // the copy stream; piece 0's event is recorded behind all of it
-            if (defer_upload && b->n_pieces > 0) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, b->piece_ev[0], 0));
+            if (defer_upload && b->n_pieces > 0) CUDA_TRY(ctx, b->wait_piece(ctx->stream, 0));
             const int thr = 256;
             empty_side_kernel<<<(unsigned)((b->n_pairs + thr - 1) / thr), thr, 0, ctx->stream>>>(
                 b->d_pq, b->d_ps, b->d_qlen, b->d_slen, b->n_pairs, atype, affine ? 1 : 0, sch->gap_open, beta_eff,

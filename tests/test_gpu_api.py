@@ -386,3 +386,79 @@ def test_two_ranks_over_gloo_run_their_shards_on_the_gpu(tmp_path):
     port = 29600 + (os.getpid() % 2000)
     mp.spawn(_gpu_rank_main, args=(2, port, str(tmp_path)), nprocs=2, join=True)
     assert open(tmp_path / "ok").read() == "ok"
+
+
+def test_host_packed_upload_matches_the_plain_upload(monkeypatch):
+    """Large byte pools are packed into the 2-bit layout by host threads, piece by piece, and expanded on the device
+    (hostpack.cpp, HostPacker in wsb200.cu): a quarter of the bytes on the bus, identical results.  Covered: a reads
+    matrix (metadata-free path), ragged pools whose piece boundaries fall inside a packed byte, flagged symbols (their
+    slice travels as plain bytes, also next to a shared byte), score-only and traceback, and the oracle on a sample."""
+    from paper_2205_07610_b200 import batch as B
+    from paper_2205_07610_b200.engine import get_context
+    monkeypatch.delenv("WSB_HOST_PACK_THREADS", raising=False)
+    monkeypatch.delenv("LOCAL_WORLD_SIZE", raising=False)
+    assert N.load().wsb_host_pack_isa().decode() in ("avx512bw", "bmi2", "plain")
+    rng = np.random.default_rng(77)
+    scheme = W.ScoringScheme()
+
+    def run(pq, ps, pairs, cfg, threads):
+        monkeypatch.setattr(B, "_host_pack_policy", lambda: threads)
+        return W.run_batch(W.BatchJob(pq, ps, pairs, cfg, scheme))
+
+    def same(a, b, what):
+        for f in ("score", "q_start", "q_end", "s_start", "s_end"):
+            assert (getattr(a.results, f) == getattr(b.results, f)).all(), (what, f)
+        if a.results.runs is not None:
+            assert (a.results.runs == b.results.runs).all() and (a.results.run_off == b.results.run_off).all(), what
+
+    # 1. reads matrix, 300 k x 150 bp (90 MB): the bench's path
+    n, L = 300_000, 150
+    q = rng.integers(0, 4, (n, L), dtype=np.uint8)
+    s = q.copy()
+    mut = rng.random((n, L)) < 0.1
+    s[mut] = rng.integers(0, 4, int(mut.sum()), dtype=np.uint8)
+    idx = np.arange(n, dtype=np.int32)
+    pairs = np.stack([idx, idx], 1)
+    for flagged in (False, True):
+        if flagged:   # first piece, a middle piece, the very last symbol
+            q[5, 7] = 4; s[n // 2 + 3, 1] = 4; s[n - 1, L - 1] = 4
+        pq, ps = W.SequencePool.from_uniform(q), W.SequencePool.from_uniform(s)
+        for cfg in (W.AlignConfig("local", "affine"), W.AlignConfig("semiglobal", "affine", "traceback")):
+            plain = run(pq, ps, pairs, cfg, 0)
+            packed = run(pq, ps, pairs, cfg, 5)   # an odd thread count: slices of unequal size
+            same(plain, packed, (flagged, cfg.align_type))
+            assert plain.h2d_bytes >= 2 * n * L
+            if not flagged:
+                assert 2 * n * L // 4 <= packed.h2d_bytes <= plain.h2d_bytes // 4 + 4096
+            else:
+                assert packed.h2d_bytes < plain.h2d_bytes
+        if not flagged:
+            sample = np.sort(rng.choice(n, 2000, replace=False)).astype(np.int32)
+            off = np.arange(n, dtype=np.int64) * L
+            ln = np.full(n, L, np.int32)
+            want, wi, wj = oracle.score_batch(q.reshape(-1), off, ln, s.reshape(-1), off, ln, sample, sample, "local", True,
+                                              scheme.match_score, scheme.mismatch_score, scheme.gap_open, scheme.gap_extend)
+            got = run(pq, ps, pairs, W.AlignConfig("local", "affine"), -1).results
+            assert (got.score[sample] == want).all() and (got.q_end[sample] == wi).all() and (got.s_end[sample] == wj).all()
+
+    # 2. ragged pools with explicit offsets: 270 k pairs of 101..163 symbols, piece boundaries inside packed bytes
+    n = 270_000
+    ql = rng.integers(101, 164, n).astype(np.int32)
+    sl = rng.integers(101, 164, n).astype(np.int32)
+    qo = np.zeros(n, np.int64); qo[1:] = np.cumsum(ql[:-1])
+    so = np.zeros(n, np.int64); so[1:] = np.cumsum(sl[:-1])
+    qc = rng.integers(0, 4, int(ql.sum()), dtype=np.uint8)
+    sc = rng.integers(0, 4, int(sl.sum()), dtype=np.uint8)
+    idx = np.arange(n, dtype=np.int32)
+    pairs = np.stack([idx, idx], 1)
+    for flagged in (False, True):
+        if flagged:
+            sc[int(so[n // 8 * 3]) - 1] = 4    # the last symbol before a boundary region
+            qc[int(qo[n // 2]) + 2] = 4
+        pq, ps = W.SequencePool(qc, qo, ql), W.SequencePool(sc, so, sl)
+        for cfg in (W.AlignConfig("global", "affine"), W.AlignConfig("local", "affine")):
+            plain = run(pq, ps, pairs, cfg, 0)
+            packed = run(pq, ps, pairs, cfg, 16)
+            same(plain, packed, ("ragged", flagged, cfg.align_type))
+            assert packed.h2d_bytes < plain.h2d_bytes
+    get_context(0).set_host_pack_threads(-1)
