@@ -46,7 +46,7 @@ struct LongParams {
     unsigned int* queue;   // work queue head, zeroed before the launch
     int32_t* redo; int32_t* redo_count;   // packed int16 kernel (score_long16.cuh): pairs handed back to this kernel
     const int32_t* n_units_dev;           // re-score launch: number of units is read from the device
-    int32_t* cflags;       // cluster launches: per cluster 160 ints (progress counters of its warps, unit slot, reduction slots)
+    int32_t* cflags;       // cluster launches: per cluster kLongCf ints (progress counters of its warps, unit slot, reduction slots)
     int32_t one;           // 1, opaque to the compiler: keeps selected adds on the FMA pipe as IMAD
 };
 
@@ -63,6 +63,11 @@ __device__ __forceinline__ int fma_add(int a, int one, int b) {
 }
 
 using LongFn = void (*)(const LongParams);
+
+// flag block of a cluster launch (LongParams::cflags): progress counters of up to 16 x 16 warps + 1, stage counter, unit slot,
+// one (value, row, column) reduction slot per block
+constexpr int kLongCf = 320, kLongCfNext = 257, kLongCfUnit = 258, kLongCfRed = 260;
+constexpr int kLongCfClusters = 256;   // flag blocks per cluster size (2, 4, 8, 16)
 
 template <int ATYPE, int GAP, bool CLUSTER = false>
 __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long_kernel(const LongParams prm) {
@@ -96,19 +101,20 @@ __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long_kernel(const Lo
     const unsigned mism4 = (unsigned)(mism & 0xff) * 0x01010101u;
     const int64_t cluster_id = blockIdx.x / CS;
     int2* const bnd_block = prm.bnd + cluster_id * (GW + 1) * prm.bnd_rows;
-    int32_t* const cf = CS > 1 ? prm.cflags + cluster_id * 160 : nullptr;   // [0..128] progress, [129] next stage, [130] unit, [132..155] reduction
+    // per cluster kLongCf ints: [0..256] progress (up to 16 blocks x 16 warps + 1), [257] next stage, [258] unit, [260..307] reduction
+    int32_t* const cf = CS > 1 ? prm.cflags + cluster_id * kLongCf : nullptr;
     volatile int* prog = CS > 1 ? cf : s_prog;
-    int* const next_stage = CS > 1 ? cf + 129 : &s_next;
+    int* const next_stage = CS > 1 ? cf + kLongCfNext : &s_next;
 
     for (;;) {
         // previous pair fully retired (progress counters, reduction slots), next unit fetched by one thread
         if (CS > 1) {
             cluster.sync();
-            if (crank == 0 && threadIdx.x == 0) cf[130] = (int)atomicAdd(prm.queue, 1u);
-            if (crank == 0 && threadIdx.x < 130) cf[threadIdx.x] = 0;
+            if (crank == 0 && threadIdx.x == 0) cf[kLongCfUnit] = (int)atomicAdd(prm.queue, 1u);
+            if (crank == 0 && threadIdx.x < kLongCfUnit) cf[threadIdx.x] = 0;
             __threadfence();
             cluster.sync();
-            if (threadIdx.x == 0) s_unit = *(volatile int*)(cf + 130);
+            if (threadIdx.x == 0) s_unit = *(volatile int*)(cf + kLongCfUnit);
             __syncthreads();
         } else {
             __syncthreads();
@@ -303,7 +309,7 @@ __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long_kernel(const Lo
                 if (better_cell(s_red[x][0], s_red[x][1], s_red[x][2], bv, bi, bj)) {
                     bv = s_red[x][0]; bi = s_red[x][1]; bj = s_red[x][2];
                 }
-            if (CS > 1) { cf[132 + 3 * crank] = bv; cf[133 + 3 * crank] = bi; cf[134 + 3 * crank] = bj; __threadfence(); }
+            if (CS > 1) { cf[kLongCfRed + 3 * crank] = bv; cf[kLongCfRed + 1 + 3 * crank] = bi; cf[kLongCfRed + 2 + 3 * crank] = bj; __threadfence(); }
             else {
                 if (LOCAL && bv <= 0) { bv = 0; bi = 0; bj = 0; }
                 prm.out_score[p] = bv; prm.out_i[p] = bi; prm.out_j[p] = bj;
@@ -312,7 +318,7 @@ __global__ void __launch_bounds__(kLongMaxWarps * 32) score_long_kernel(const Lo
         if (CS > 1) {
             cluster.sync();
             if (crank == 0 && threadIdx.x == 0) {
-                volatile int* r = cf + 132;
+                volatile int* r = cf + kLongCfRed;
                 int bv = r[0], bi = r[1], bj = r[2];
                 for (int x = 1; x < CS; ++x)
                     if (better_cell(r[3 * x], r[3 * x + 1], r[3 * x + 2], bv, bi, bj)) { bv = r[3 * x]; bi = r[3 * x + 1]; bj = r[3 * x + 2]; }

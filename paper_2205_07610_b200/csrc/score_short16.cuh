@@ -259,6 +259,7 @@ __global__ void __launch_bounds__(kThreads, MINB) s16_local_short_kernel(const S
 
         // query buffer: P pad rows, the rows of both queries as row words, then pad rows for the ramp-down.  The byte
         // loads of four rows are in flight before the first is used.
+#ifndef WSB_ABL_NOQBUF     // timing experiment only
         {
             constexpr int UNR = 4;
             const int total = mm_w + 2 * P + 2;
@@ -279,12 +280,19 @@ __global__ void __launch_bounds__(kThreads, MINB) s16_local_short_kernel(const S
                 }
             }
         }
+#endif
         // per column: PRMT selector of the two subject symbols, TA = T - alpha (whole quads: the snapshot source), TG = T - gamma,
         // D = diagonal candidate of the NEXT row (H of the column to the left + sigma of the next row's symbol)
         unsigned sel[K], TA[GAP == GAP_MERGED ? K : NW], TG[GAP == GAP_MERGED ? NW : 1], D[K];   // the snapshot source holds whole quads
         D[0] = 0u;
+#ifdef WSB_ABL_NOSEL       // timing experiment only
+        bool flagged_subject = false;
+#pragma unroll
+        for (int c = 0; c < K; ++c) sel[c] = 0x9180u + (unsigned)(ssh[0] + c);
+#else
         const bool flagged_subject = build_selectors16<K>(raw[gib][1], raw[gib][3], ssh[0] + col0, ssh[1] + col0, n[0] - col0,
                                                           n[1] - col0, sel);
+#endif
 #pragma unroll
         for (int c = 0; c < K; ++c) {
             TA[c] = c_nalpha;
@@ -417,6 +425,9 @@ __global__ void __launch_bounds__(kThreads, MINB) s16_local_short_kernel(const S
         }
 
         // reduce over the group: max value, then smallest row, then smallest strip; the winner resolves its column
+#ifdef WSB_ABL_NOFIN       // timing experiment only
+        if (t == 0 && pidx[0] >= 0) prm.out_score[pidx[0]] = (int)bestvec;
+#else
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
             int bv = half16(bestvec, v);
@@ -454,6 +465,7 @@ __global__ void __launch_bounds__(kThreads, MINB) s16_local_short_kernel(const S
                 prm.out_j[pidx[v]] = j;
             }
         }
+#endif
     }
     // cycle-based roofline fraction: a resident block lives as long as the launch, so the largest value is the
     // launch's duration in cycles of the SM it ran on

@@ -44,11 +44,13 @@ struct wsb_ctx {
     cudaStream_t aux[kAux] = {};
     cudaEvent_t aux_done[kAux] = {};
     unsigned int* d_queues = nullptr;  // work-queue heads of the long-read launches
-    int32_t* d_cflags = nullptr;       // cluster launches of the long-read kernel: 160 ints per cluster
+    int32_t* d_cflags = nullptr;       // cluster launches of the long-read kernel: kLongCf ints per cluster, kLongCfClusters per cluster size
     std::string last_error;
     // Host threads that pack large byte pools into the 2-bit layout before they cross the bus (hostpack.cpp); 0 = pools go up
     // as they are.  -1 = default: WSB_HOST_PACK_THREADS, else min(16, cores - 1).  wsb_ctx_set_host_pack_threads overrides.
     int host_pack_threads = -1;
+    int cluster16 = -1;                // 1: the device schedules clusters of 16 blocks x 16 warps of the long-read kernel (non-portable
+                                       // size); -1: not probed yet (probe_cluster16)
     // One context serves every host thread that aligns on its GPU (the reference runs independent alignments
     // concurrently, batch.py:213-240): each entry point that touches the context's streams, events, queues or block
     // cache holds this lock for its whole duration.  Recursive: the one-shot calls nest the batch calls.
@@ -330,8 +332,8 @@ extern "C" int wsb_ctx_create(int device, wsb_ctx** out) {
         return WSB_E_CUDA;
     }
     bool ok = cudaMalloc((void**)&c->d_queues, 64 * sizeof(unsigned int)) == cudaSuccess &&
-              cudaMalloc((void**)&c->d_cflags, 1024 * 160 * sizeof(int32_t)) == cudaSuccess &&
-              cudaMemset(c->d_cflags, 0, 1024 * 160 * sizeof(int32_t)) == cudaSuccess;
+              cudaMalloc((void**)&c->d_cflags, 4 * kLongCfClusters * kLongCf * sizeof(int32_t)) == cudaSuccess &&
+              cudaMemset(c->d_cflags, 0, 4 * kLongCfClusters * kLongCf * sizeof(int32_t)) == cudaSuccess;
     for (int k = 0; k < wsb_ctx::kAux && ok; ++k)
         ok = cudaStreamCreateWithFlags(&c->aux[k], cudaStreamNonBlocking) == cudaSuccess &&
              cudaEventCreateWithFlags(&c->aux_done[k], cudaEventDisableTiming) == cudaSuccess;
@@ -966,6 +968,25 @@ static LongFn pick_long(int atype, int gap, bool cluster) {
     return nullptr;
 }
 
+// Can a cluster of 16 blocks x 16 warps of the long-read kernel be resident?  (non-portable cluster size: opt-in per kernel)
+static bool probe_cluster16(wsb_ctx* ctx) {
+    if (ctx->cluster16 >= 0) return ctx->cluster16 == 1;
+    ctx->cluster16 = 0;
+    LongFn fn = pick_long(AT_LOCAL, GAP_MERGED, true);
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(16); cfg.blockDim = dim3(kLongMaxWarps * 32);
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 16; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+        cfg.attrs = at; cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) == cudaSuccess && n >= 1) ctx->cluster16 = 1;
+    }
+    (void)cudaGetLastError();
+    return ctx->cluster16 == 1;
+}
+
 // The packed int16 short-read kernels live in their own translation unit (wsb200_s16.cu, built with -Xptxas -O1: ptxas'
 // default scheduling costs those two kernels 3-4 %, every other kernel is at its best with the default).
 namespace wsb {
@@ -1202,22 +1223,30 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
                 twins.emplace_back(cand[k], cand[k + 1]); k += 2;
             } else { singles.push_back(cand[k]); ++k; }
         }
-        // class index = log2(warps per pair): 0..4 -> 1..16 warps in one block, 5..7 -> clusters of 2, 4, 8 blocks x 16 warps
-        std::vector<int64_t> by_class[8];
+        // class index = log2(warps per pair): 0..4 -> 1..16 warps in one block, 5..8 -> clusters of 2, 4, 8, 16 blocks x 16 warps
+        // (16: the non-portable cluster size, where the device schedules it)
+        std::vector<int64_t> by_class[9];
         std::vector<std::pair<int64_t, int64_t>> twins_by_class[5];
         const double machine_warps = (double)ctx->sm_count * 20.0;
         const double makespan = std::max(long_iters / machine_warps, 1.0);
         static const char* no_cluster = getenv("WSB_NO_CLUSTER");  // tuning aid
-        const int max_class = (no_cluster && no_cluster[0]) ? 4 : 7;
+        // Clusters of 16 blocks (non-portable size) are opt-in (WSB_CLUSTER16=1): measured on cfg5's 8-way shards they lose
+        // (a shard holds ~16 pairs of that class; 7 clusters of 16 are co-resident against 15 of 8: 164 ms per shard
+        // against 140 ms), and on the whole batch too (679 against 622 ms).
+        static const char* want_cluster16 = getenv("WSB_CLUSTER16");
+        const int max_class = (no_cluster && no_cluster[0]) ? 4 : (want_cluster16 && want_cluster16[0] == '1' && probe_cluster16(ctx)) ? 8 : 7;
         auto pick_class = [&](int64_t p, int top) {
             const int stages = (b->n[p] + kLongW - 1) / kLongW;
             const double t1 = (double)stages * (b->m[p] + 31);
             // warps per pair come from powers of two: blocks then spread evenly over the four schedulers of an SM
             // ... but a cluster only up to about twice the pair's proportional share of the machine, or a few giants that
             // dominate the batch would queue behind each other in half-idle clusters
-            const double share_cap = std::max(1.0, 2.0 * t1 / std::max(long_iters, 1.0) * machine_warps);
+            static const double share_factor = [] { const char* e = getenv("WSB_SHARE_CAP"); return e ? atof(e) : 2.0; }();   // tuning aid
+            const double share_cap = std::max(1.0, share_factor * t1 / std::max(long_iters, 1.0) * machine_warps);
             int lo = 0;
-            while (lo < top && (2 << lo) <= stages && (lo < 4 || (double)(2 << lo) <= share_cap) &&
+            // (the step to 16 blocks is taken as soon as 128 warps no longer cover the stages in one round: a 100 kbp subject
+            // has 196 stages)
+            while (lo < top && ((2 << lo) <= stages || (lo == 7 && stages > (1 << lo))) && (lo < 4 || (double)(2 << lo) <= share_cap) &&
                    t1 / (1 << lo) > 0.25 * makespan) ++lo;
             int best = lo;
             double best_cost = 1e300;
@@ -1250,7 +1279,7 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
             }
             plan.groups.push_back(g);
         }
-        for (int c = 7; c >= 0; --c) {
+        for (int c = 8; c >= 0; --c) {
             auto& v = by_class[c];
             if (v.empty()) continue;
             std::stable_sort(v.begin(), v.end(), by_work);
@@ -1397,8 +1426,9 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
                 at[0].val.clusterDim.x = (unsigned)g.cluster; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
                 cfg.attrs = at; cfg.numAttrs = 1;
                 int max_clusters = 0;
+                if (g.cluster > 8) CUDA_TRY(ctx, cudaFuncSetAttribute(lfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
                 CUDA_TRY(ctx, cudaOccupancyMaxActiveClusters(&max_clusters, lfn, &cfg));
-                max_clusters = std::max(1, std::min(max_clusters, 256));   // three cluster classes share 1024 flag blocks
+                max_clusters = std::max(1, std::min(max_clusters, kLongCfClusters));   // flag blocks per cluster size
                 grid = g.cluster * (int)std::min<int64_t>(g.n_units, max_clusters);
             } else {
                 int per_sm = 0;
@@ -1487,7 +1517,7 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
             lp.queue = ctx->d_queues + k; lp.one = 1;
             lp.redo = b->d_redo_long ? b->d_redo_long + 4 : nullptr; lp.redo_count = b->d_redo_long; lp.n_units_dev = nullptr;
             if (g.long16) { any_l16 = true; l16_gap = g.gap; l16_rows = std::max(l16_rows, geo[k].bnd_rows); }
-            lp.cflags = ctx->d_cflags + (size_t)256 * 160 * (size_t)(g.cluster == 2 ? 0 : g.cluster == 4 ? 1 : 2);
+            lp.cflags = ctx->d_cflags + (size_t)kLongCfClusters * kLongCf * (size_t)(g.cluster == 2 ? 0 : g.cluster == 4 ? 1 : g.cluster == 8 ? 2 : 3);
             if (g.cluster > 1) {
                 cudaLaunchConfig_t cfg = {};
                 cfg.gridDim = dim3((unsigned)geo[k].grid); cfg.blockDim = dim3((unsigned)(g.long_nw * 32));
@@ -1496,6 +1526,8 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
                 at[0].id = cudaLaunchAttributeClusterDimension;
                 at[0].val.clusterDim.x = (unsigned)g.cluster; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
                 cfg.attrs = at; cfg.numAttrs = 1;
+                static const bool trace_cl = getenv("WSB_TRACE") != nullptr;
+                if (trace_cl) fprintf(stderr, "[wsb] long-read launch: %lld pairs on clusters of %d blocks, grid %d\n", (long long)g.n_units, g.cluster, geo[k].grid);
                 CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, geo[k].lfn, lp));
             } else {
                 geo[k].lfn<<<geo[k].grid, g.long_nw * 32, 0, ctx->aux[a]>>>(lp);
