@@ -903,13 +903,26 @@ struct Shape { int P, K; };
 static const Shape kShapesF16[] = {{4, 16}, {8, 19}, {8, 32}, {4, 38}, {16, 16}};
 // int32 shapes: narrow groups for short reads, full warps with wide stages for long reads
 static const Shape kShapesI32[] = {{8, 16}, {16, 16}, {32, 16}, {8, 19}};
-static const Shape kShapesS16[] = {{8, 16}, {8, 19}};   // packed int16 short-read kernel (local only)
+// packed int16 short-read kernels.  (16, 10) is the LATENCY shape: twice the lanes per unit, strips half as long; 22 % more
+// instructions per cell, but a batch too small to fill the machine with (8, 19) groups finishes in ~60 % of the time
+// (cfg1's 10 000 pairs are a single launch whose duration is one unit's sweep).  Chosen per launch group, latency_shape().
+static const Shape kShapesS16[] = {{8, 16}, {8, 19}, {16, 10}};
 static Shape shape_of(int variant, int shape);
 constexpr int kNumShapesF16 = 3, kNumShapesI32 = 4;  // shapes the planner may choose
 constexpr int kNumShapes = 5;  // bucket array bound
 
 static Shape shape_of(int variant, int shape) {
     return variant == WSB_VARIANT_F16X2 ? kShapesF16[shape] : variant == WSB_VARIANT_S16X2 ? kShapesS16[shape] : kShapesI32[shape];
+}
+
+// A packed int16 short-read launch group whose units leave a quarter or more of the resident (8, K) lane groups empty
+// runs on (16, 10) lane groups instead (WSB_S16_LAT = 0: never, 2: always; tuning aid).
+static int latency_shape(int shape, int64_t n_units, int max_m, int sm_count) {
+    static const char* lat = getenv("WSB_S16_LAT");
+    const int mode = (lat && lat[0]) ? atoi(lat) : 1;
+    if (mode == 0 || max_m < 2) return shape;
+    const int64_t resident = (int64_t)sm_count * 4 * (kThreads / 8);   // lane groups of the (8, K) shapes, four blocks per SM
+    return (mode >= 2 || n_units * 4 <= resident * 3) ? 2 : shape;
 }
 
 static double padded_cost(const Shape& s, int m, int n) {
@@ -1163,6 +1176,7 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
             g.variant = var; g.shape = shape; g.gap = var == WSB_VARIANT_I32 ? gap_i32 : gap_f16;
             g.n_units = var == WSB_VARIANT_I32 ? np : (np + 1) / 2;
             g.unit_off = -1; g.max_m = b->m[0]; g.max_n = b->n[0];
+            if (var == WSB_VARIANT_S16X2) g.shape = latency_shape(g.shape, g.n_units, g.max_m, ctx->sm_count);
             plan.groups.push_back(g);
             account_plan(plan, std::vector<int32_t>());
             return WSB_OK;
@@ -1308,6 +1322,7 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
             for (int64_t p : v) { g.max_m = std::max(g.max_m, b->m[p]); g.max_n = std::max(g.max_n, b->n[p]); }
             if (cls != 1) {
                 g.n_units = ((int64_t)v.size() + 1) / 2;
+                if (cls == 2) g.shape = latency_shape(g.shape, g.n_units, g.max_m, ctx->sm_count);
                 for (size_t k = 0; k < v.size(); k += 2) {
                     units.push_back((int32_t)v[k]);
                     units.push_back(k + 1 < v.size() ? (int32_t)v[k + 1] : -1);
@@ -1448,7 +1463,7 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
         const KernelSel sel = pick_kernel(g.variant, g.shape, atype, g.gap, sch->mismatch > 0 || sch->match < 0, short_ok,
                                           std::abs(sch->match - sch->mismatch) > 127, sch->gap_open,
                                           affine ? std::min(sch->gap_open, sch->gap_extend) : sch->gap_open,
-                                          /*ragged=*/g.unit_off >= 0 || g.max_m < 16);
+                                          /*ragged=*/g.unit_off >= 0 || g.max_m < 2 * sh.P);
         KernelFn fn = sel.fn;
         if (!fn) return WSB_E_SCHEME;
         CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel.smem));

@@ -35,10 +35,12 @@ template <int P, int K> static KernelSel pick_global(int gap, int alpha, int gam
 }
 
 KernelSel pick_short16_local(int shape, int gap, int alpha, int gamma) {
-    return shape == 0 ? pick_local<8, 16>(gap, alpha, gamma) : pick_local<8, 19>(gap, alpha, gamma);
+    return shape == 0 ? pick_local<8, 16>(gap, alpha, gamma) : shape == 1 ? pick_local<8, 19>(gap, alpha, gamma)
+                                                                           : pick_local<16, 10>(gap, alpha, gamma);
 }
 KernelSel pick_short16_global(int shape, int gap, int alpha, int gamma, bool ragged) {
-    return shape == 0 ? pick_global<8, 16>(gap, alpha, gamma, ragged) : pick_global<8, 19>(gap, alpha, gamma, ragged);
+    return shape == 0 ? pick_global<8, 16>(gap, alpha, gamma, ragged) : shape == 1 ? pick_global<8, 19>(gap, alpha, gamma, ragged)
+                                                                                   : pick_global<16, 10>(gap, alpha, gamma, ragged);
 }
 
 template <int GAP, int AIMM, int GIMM> static LongFn pick_long16_atype(int atype) {

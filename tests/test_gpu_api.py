@@ -315,9 +315,10 @@ def test_engine_stats_from_the_planner():
     scheme = W.ScoringScheme(2, -1, 2, 1, "affine")
     st = W.EngineStats()
     W.engine_score(q, s, W.AlignConfig("local", "affine"), scheme, stats=st, instrument=True)
-    # packed int16 short kernel: lane groups of 8 x 19 columns, two alignments per register (the second half rides empty)
-    assert (st.stages, st.iterations, st.cells) == (1, 150 + 8 - 1, 150 * 150)
-    assert st.updates == 1 * 150 * 152 * 2
+    # packed int16 short kernel, two alignments per register (the second half rides empty); a batch this small runs on the
+    # latency shape: lane groups of 16 x 10 columns
+    assert (st.stages, st.iterations, st.cells) == (1, 150 + 16 - 1, 150 * 150)
+    assert st.updates == 1 * 150 * 160 * 2
     assert st.ops_max * 4 == st.updates * 5 and st.ops_addsub * 4 == st.updates * 6 and st.ops_lookup * 2 == st.updates
     st2 = W.EngineStats()
     lin = W.ScoringScheme(2, -1, 1, 1, "linear")
