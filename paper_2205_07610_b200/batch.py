@@ -209,7 +209,10 @@ def _run_shard(device: int, queries: SequencePool, subjects: SequencePool, pair_
         both_packed = queries.packed is not None and subjects.packed is not None
         no_flags = both_packed and not (queries.flag_pos is not None and len(queries.flag_pos)) and \
             not (subjects.flag_pos is not None and len(subjects.flag_pos))
-        if regular and len(pair_q) >= 65536 and (no_flags or (queries.packed is None and subjects.packed is None)):
+        # (score-only jobs take it from 1 024 pairs on: the six metadata arrays of the general upload cost ~120 us per call,
+        # more than the kernel of a cfg1-sized batch; tools/e2e_small_probe.py)
+        small_ok = cfg.result_mode != "traceback" and len(pair_q) >= 1024 and min(queries.uniform_len or 0, subjects.uniform_len or 0) > 0
+        if regular and (len(pair_q) >= 65536 or small_ok) and (no_flags or (queries.packed is None and subjects.packed is None)):
             # uniform pools, identity pairs: no offset / length / pair arrays at all
             batch = N.Batch.uniform(ctx, queries.packed if both_packed else queries.codes, queries.uniform_len,
                                     subjects.packed if both_packed else subjects.codes, subjects.uniform_len,

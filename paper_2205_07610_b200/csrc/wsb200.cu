@@ -105,7 +105,8 @@ struct LaunchGroup {  // pairs that run in one kernel launch
 
 struct Plan {
     std::vector<LaunchGroup> groups;
-    int32_t* d_units = nullptr;
+    int32_t* d_units = nullptr;   // from the context's block cache (cudaMalloc + cudaFree per call cost more than a cfg1-sized launch)
+    std::vector<int32_t> h_units; // source of the upload: lives as long as the plan, so no synchronisation after queueing the copy
     std::vector<int32_t> status;  // per pair
     bool any_error = false;
     // geometry counters of the plan (wsb_batch_plan_stats): the GPU counterpart of EngineStats (engine.py:109-146)
@@ -417,7 +418,7 @@ extern "C" void wsb_batch_destroy(wsb_batch* b) {
                     (void*)b->d_slen, (void*)b->d_pq, (void*)b->d_ps, (void*)b->d_score, (void*)b->d_i, (void*)b->d_j,
                     b->d_bnd, (void*)b->d_redo, (void*)b->d_redo_long, b->stage_blocks[0], b->stage_blocks[1], b->stage_blocks[2], b->stage_blocks[3]})
         if (p) b->ctx->release(p);
-    for (auto& kv : b->plans) if (kv.second.d_units) cudaFree(kv.second.d_units);
+    for (auto& kv : b->plans) if (kv.second.d_units) b->ctx->release(kv.second.d_units);
     // traceback buffers come from the context's block cache
     for (void* p : {(void*)b->tb.d_qs, (void*)b->tb.d_ss, (void*)b->tb.d_run_off, (void*)b->tb.d_runs}) if (p) b->ctx->release(p);
     b->tb.d_qs = b->tb.d_ss = nullptr; b->tb.d_run_off = nullptr; b->tb.d_runs = nullptr;
@@ -904,8 +905,8 @@ static const Shape kShapesF16[] = {{4, 16}, {8, 19}, {8, 32}, {4, 38}, {16, 16}}
 // int32 shapes: narrow groups for short reads, full warps with wide stages for long reads
 static const Shape kShapesI32[] = {{8, 16}, {16, 16}, {32, 16}, {8, 19}};
 // packed int16 short-read kernels.  (16, 10) is the LATENCY shape: twice the lanes per unit, strips half as long; 22 % more
-// instructions per cell, but a batch too small to fill the machine with (8, 19) groups finishes in ~60 % of the time
-// (cfg1's 10 000 pairs are a single launch whose duration is one unit's sweep).  Chosen per launch group, latency_shape().
+// instructions per cell, but a batch that leaves most SMs with less than one block of (8, K) groups finishes ~20 % sooner.
+// Chosen per launch group, latency_shape().
 static const Shape kShapesS16[] = {{8, 16}, {8, 19}, {16, 10}};
 static Shape shape_of(int variant, int shape);
 constexpr int kNumShapesF16 = 3, kNumShapesI32 = 4;  // shapes the planner may choose
@@ -915,14 +916,15 @@ static Shape shape_of(int variant, int shape) {
     return variant == WSB_VARIANT_F16X2 ? kShapesF16[shape] : variant == WSB_VARIANT_S16X2 ? kShapesS16[shape] : kShapesI32[shape];
 }
 
-// A packed int16 short-read launch group whose units leave a quarter or more of the resident (8, K) lane groups empty
-// runs on (16, 10) lane groups instead (WSB_S16_LAT = 0: never, 2: always; tuning aid).
+// A packed int16 short-read launch group with at most one block of (8, K) lane groups per SM runs on (16, 10) lane groups
+// instead: twice the blocks, strips half as long (WSB_S16_LAT = 0: never, 2: always; tuning aid).  Measured (B200, 150 bp,
+// kernel time): 2 000 pairs 35 -> 28 us (global linear), 48 -> 37 us (local affine); at 10 000 pairs (two blocks per SM
+// either way) the wide shape's 22 % extra instructions already lose: 54 vs 59 us.
 static int latency_shape(int shape, int64_t n_units, int max_m, int sm_count) {
     static const char* lat = getenv("WSB_S16_LAT");
     const int mode = (lat && lat[0]) ? atoi(lat) : 1;
     if (mode == 0 || max_m < 2) return shape;
-    const int64_t resident = (int64_t)sm_count * 4 * (kThreads / 8);   // lane groups of the (8, K) shapes, four blocks per SM
-    return (mode >= 2 || n_units * 4 <= resident * 3) ? 2 : shape;
+    return (mode >= 2 || n_units <= (int64_t)sm_count * (kThreads / 8)) ? 2 : shape;
 }
 
 static double padded_cost(const Shape& s, int m, int n) {
@@ -1335,9 +1337,10 @@ static int build_plan(wsb_batch* b, const wsb_scheme* sch, int atype, int varian
         }
     account_plan(plan, units);
     if (!units.empty()) {
-        CUDA_TRY(ctx, cudaMalloc((void**)&plan.d_units, units.size() * sizeof(int32_t)));
-        CUDA_TRY(ctx, cudaMemcpyAsync(plan.d_units, units.data(), units.size() * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
-        CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+        plan.h_units = std::move(units);
+        CUDA_TRY(ctx, ctx->alloc((void**)&plan.d_units, plan.h_units.size() * sizeof(int32_t)));
+        CUDA_TRY(ctx, cudaMemcpyAsync(plan.d_units, plan.h_units.data(), plan.h_units.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
+                                      ctx->stream));
     }
     return WSB_OK;
 }
@@ -1411,7 +1414,7 @@ static int batch_score_impl(wsb_batch* b, const wsb_scheme* sch, int atype, int 
     if (it == b->plans.end()) {
         Plan plan;
         rc = build_plan(b, sch, atype, variant, plan, want_s16);
-        if (rc) { if (plan.d_units) cudaFree(plan.d_units); return rc; }
+        if (rc) { if (plan.d_units) ctx->release(plan.d_units); return rc; }
         it = b->plans.emplace(key, std::move(plan)).first;
     }
     const Plan& plan = it->second;

@@ -276,6 +276,31 @@ def test_sharded_reads_matrix_takes_the_metadata_free_path_per_shard(monkeypatch
         c.close()
 
 
+@pytest.mark.parametrize("align_type,gap_model", COMBOS)
+def test_small_reads_matrix_takes_the_metadata_free_path(align_type, gap_model):
+    """cfg1-sized regular jobs (uniform pools, identity pairs, score only) skip the offset / length / pair arrays like the
+    big ones: same results as the general upload of the same reads and as the oracle, and only pool bytes on the bus."""
+    rng = np.random.default_rng(77)
+    n, L = 3000, 150
+    q = rng.integers(0, 4, (n, L), dtype=np.uint8); s = rng.integers(0, 4, (n, L), dtype=np.uint8)
+    s[::2] = q[::2]; s[::2, 40:43] = 3 - s[::2, 40:43]
+    scheme = W.ScoringScheme(2, -1, 2, 1, "affine") if gap_model == "affine" else W.ScoringScheme(2, -1, 1, 1, "linear")
+    cfg = W.AlignConfig(align_type, gap_model)
+    ident = np.stack([np.arange(n), np.arange(n)], 1).astype(np.int32)
+    fast = W.run_batch(W.BatchJob(W.SequencePool.from_uniform(q), W.SequencePool.from_uniform(s), ident, cfg, scheme))
+    assert fast.h2d_bytes == 2 * n * L
+    # the same pairs in reverse order: not an identity list, so the general upload carries them
+    rev = ident[::-1].copy()
+    slow = W.run_batch(W.BatchJob(W.SequencePool.from_uniform(q), W.SequencePool.from_uniform(s), rev, cfg, scheme))
+    assert slow.h2d_bytes > 2 * n * L
+    off = np.arange(n, dtype=np.int64) * L; ln = np.full(n, L, np.int32); idx = np.arange(n, dtype=np.int32)
+    sc, ei, ej = oracle.score_batch(q.reshape(-1), off, ln, s.reshape(-1), off, ln, idx, idx, align_type, gap_model == "affine",
+                                    scheme.match_score, scheme.mismatch_score, scheme.gap_open, scheme.gap_extend)[:3]
+    for k in range(n):
+        a, b = fast.results[k], slow.results[n - 1 - k]
+        assert (a.score, a.q_end, a.s_end) == (b.score, b.q_end, b.s_end) == (int(sc[k]), int(ei[k]), int(ej[k]))
+
+
 def test_selftest_draws_the_reference_cases_and_agrees_with_the_oracle():
     """selftest() mirrors cli.cmd_selftest (cli.py:264-301): same random cases per seed, AUTO kernels vs the int32 kernel on
     the GPU, here with the CPU oracle as a third voice; a planted wrong answer must come back as a JSON-able repro blob."""
