@@ -318,7 +318,9 @@ class Batch:
             score, ei, ej = dest
             assert all(a.dtype == np.int32 and a.flags.c_contiguous and len(a) == n for a in dest)
         else:
-            score, ei, ej = (pinned_empty(n) for _ in range(3)) if n >= 65536 else (np.empty(n, np.int32) for _ in range(3))
+            # page-locked destinations from 1 024 pairs on: three downloads into pageable memory are staged one by one
+            # (~15 us each), which is a third of a cfg1-sized call
+            score, ei, ej = (pinned_empty(n) for _ in range(3)) if n >= 1024 else (np.empty(n, np.int32) for _ in range(3))
         s = scheme_struct(scheme)
         ms = ctypes.c_float(0.0)
         nl = ctypes.c_int32(0)
