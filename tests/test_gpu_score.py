@@ -288,3 +288,19 @@ def test_packed_int16_global_short_kernel(ctx, gap_model):
         pairs = [(i, i) for i in range(len(qs))]
         assert_scores_equal(gpu_scores(ctx, qs, ss, pairs, scheme, "global", "auto"),
                             oracle_scores(qs, ss, pairs, scheme, "global"), f"ragged {gap_model} {sch}")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("lat", ["0", "2"])
+def test_packed_int16_short_kernels_agree_with_the_oracle_in_both_lane_group_shapes(lat):
+    """The planner picks the lane-group shape of the packed int16 short-read kernels by launch size (8 x K groups, or the
+    16 x 10 latency shape for small launch groups); WSB_S16_LAT pins one of them for a whole process, so the randomized
+    cross-check (ragged and uniform batches of 3 .. 12 000 pairs up to 154 x 152, random schemes, flagged symbols, local and
+    global) runs once per shape in a subprocess."""
+    import os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WSB_S16_LAT=lat)
+    out = subprocess.run([sys.executable, os.path.join(root, "tools", "fuzz_short16.py"), "31", "10"], env=env, cwd=root,
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "TOTAL MISMATCHES 0" in out.stdout, out.stdout[-2000:]
