@@ -32,6 +32,15 @@ template <int P, int K> static TbFillFn tb_pick_fill(int atype, bool affine) {
     }
 }
 
+// schemes beyond the signed-byte profile (tb_fill_kernel's WIDE form): one shape, any length
+static TbFillFn tb_pick_fill_wide(int atype, bool affine) {
+    switch (atype) {
+        case AT_GLOBAL: return affine ? tb_fill_kernel<32, 16, AT_GLOBAL, true, true> : tb_fill_kernel<32, 16, AT_GLOBAL, false, true>;
+        case AT_LOCAL: return affine ? tb_fill_kernel<32, 16, AT_LOCAL, true, true> : tb_fill_kernel<32, 16, AT_LOCAL, false, true>;
+        default: return affine ? tb_fill_kernel<32, 16, AT_SEMI, true, true> : tb_fill_kernel<32, 16, AT_SEMI, false, true>;
+    }
+}
+
 // packed int16 fill (traceback_fill16.cuh): batches of one stage, two alignments per thread
 template <int P, int K, bool AFFINE> static TbFillFn tb_pick_fill16_gap(int atype, bool ragged) {
     if (atype == AT_GLOBAL) return ragged ? tb_fill16_kernel<P, K, AT_GLOBAL, true, AFFINE> : tb_fill16_kernel<P, K, AT_GLOBAL, false, AFFINE>;
@@ -68,11 +77,8 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
     CUDA_TRY(ctx, cudaSetDevice(ctx->device));
     const bool affine = sch->gap_model == WSB_GAP_AFFINE;
     const int beta_eff = affine ? sch->gap_extend : sch->gap_open;
-    // the fill kernel looks sigma + alpha up in a signed-byte profile
-    if (std::abs(sch->match + sch->gap_open) > 127 || std::abs(sch->mismatch + sch->gap_open) > 127) {
-        b->ctx->last_error = "traceback needs |match + gap_open| and |mismatch + gap_open| <= 127";
-        return WSB_E_SCHEME;
-    }
+    // the fill kernels look sigma + alpha up in a signed-byte profile; schemes beyond it take the compare / select form
+    const bool wide_tb = std::abs(sch->match + sch->gap_open) > 127 || std::abs(sch->mismatch + sch->gap_open) > 127;
     const int64_t np = b->n_pairs;
     TracebackState& tb = b->tb;
     tb.valid = false;
@@ -88,6 +94,10 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
     bool any_giant = false;
     if (b->uniform) any_giant = is_giant(0);
     else for (int64_t p = 0; p < np && !any_giant; ++p) any_giant = is_giant(p);
+    if (wide_tb && any_giant) {   // the checkpointed-tile path (traceback_band.cuh) has the byte profile only
+        b->ctx->last_error = "traceback beyond the code budget needs |match + gap_open| and |mismatch + gap_open| <= 127";
+        return WSB_E_SCHEME;
+    }
     b->tb_band_pairs = b->tb_band_cells = b->tb_band_tiles = b->tb_band_peak = 0;
 
     // 1. end cells with the score kernels (identical tie-break); per-pair length faults surface here
@@ -110,13 +120,14 @@ extern "C" int wsb_batch_traceback(wsb_batch* b, const wsb_scheme* sch, int atyp
     else for (int64_t p = 0; p < np; ++p) { max_m = std::max(max_m, b->m[p]); max_n = std::max(max_n, b->n[p]); }
     // two alignments per thread in int16 halves where the batch allows it
     static const bool no16 = getenv("WSB_TB_NO16") != nullptr;   // tuning aid
-    const bool can16 = !no16 && max_m > 0 && max_n > 0 &&
+    const bool can16 = !no16 && !wide_tb && max_m > 0 && max_n > 0 &&
                        tb_fill16_range_ok(max_m, max_n, sch->match, sch->mismatch, sch->gap_open, beta_eff);
     // equal-sized pairs without rejected ones share every bound; anything else takes the masked (ragged) form
     const bool ragged16 = !b->uniform || !(!score_plan || score_plan->status.empty() || score_plan->status[0] == 0);
-    const int shape = tb_pick_shape(max_n, can16);
+    const int shape = wide_tb ? 2 : tb_pick_shape(max_n, can16);
     const int P = kTbShapes[shape].P, K = kTbShapes[shape].K;
-    TbFillFn fill = shape == 0 ? tb_pick_fill<8, 16>(atype, affine)
+    TbFillFn fill = wide_tb    ? tb_pick_fill_wide(atype, affine)
+                  : shape == 0 ? tb_pick_fill<8, 16>(atype, affine)
                   : shape == 1 ? tb_pick_fill<8, 32>(atype, affine)
                   : shape == 2 ? tb_pick_fill<32, 16>(atype, affine)
                   : shape == 3 ? tb_pick_fill<16, 16>(atype, affine) : tb_pick_fill<8, 32>(atype, affine);   // 4: never launched

@@ -78,7 +78,10 @@ __device__ __forceinline__ int max_mark(int a, int b, uint32_t& w, uint32_t bit,
     return r;
 }
 
-template <int P, int K, int ATYPE, bool AFFINE>
+// WIDE: substitution scores whose sum with alpha does not fit the signed-byte profile (|match + alpha| or |mismatch + alpha|
+// > 127): the strip keeps the subject symbols instead of profile words and a cell takes compare + select + add instead of
+// the one IDP.4A (three instructions for one; such schemes are rare, so only the (32, 16) shape is instantiated).
+template <int P, int K, int ATYPE, bool AFFINE, bool WIDE = false>
 __global__ void __launch_bounds__(kThreads) tb_fill_kernel(const TbParams prm) {
     constexpr int GPB = kThreads / P;
     constexpr int W = P * K;
@@ -97,6 +100,7 @@ __global__ void __launch_bounds__(kThreads) tb_fill_kernel(const TbParams prm) {
     // profile bytes hold sigma + alpha, so that the diagonal candidate comes straight from the stored H - alpha
     const unsigned miss4 = (unsigned)((mism + alpha) & 0xff) * 0x01010101u;
     const unsigned hit = (unsigned)((prm.match + alpha) & 0xff);
+    const int hit_w = prm.match + alpha, miss_w = mism + alpha;   // WIDE: the same two values, unpacked
 
     const int64_t rounds = (prm.n_pairs + n_groups - 1) / n_groups;
     for (int64_t rd = 0; rd < rounds; ++rd) {
@@ -136,7 +140,8 @@ __global__ void __launch_bounds__(kThreads) tb_fill_kernel(const TbParams prm) {
                 if (col0 + c < n) {
                     const int x = sp[col0 + c];
                     if (x < 4) pw = (miss4 & ~(0xffu << (8 * x))) | (hit << (8 * x));
-                }
+                    if (WIDE) pw = x < 4 ? (unsigned)x : 4u;
+                } else if (WIDE) pw = 4u;
                 prof[c] = pw;
                 AL[c] = edge_h(GLOBAL_EDGES, col0 + c + 1, alpha, beta) - alpha;
                 if (AFFINE) EP[c] = kNeg32;
@@ -171,7 +176,9 @@ __global__ void __launch_bounds__(kThreads) tb_fill_kernel(const TbParams prm) {
 #pragma unroll
                             for (int c8 = 0; c8 < 8; ++c8) {
                                 const int c = w8 * 8 + c8;
-                                const int d = FLAGGED ? ad + (mism + alpha) : __dp4a((int)prof[c], (int)qsel, ad);
+                                const int d = FLAGGED ? ad + (mism + alpha)
+                                              : WIDE  ? ad + ((int)prof[c] == q_cur ? hit_w : miss_w)
+                                                      : __dp4a((int)prof[c], (int)qsel, ad);
                                 ad = AL[c];
                                 int h;
                                 if (LOCAL) {

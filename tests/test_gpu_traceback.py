@@ -229,3 +229,24 @@ def test_packed_int16_fill_ragged_batches(ctx, align_type):
         pairs = [(i, i) for i in range(count)]
         assert_tb_equal(gpu_traceback(ctx, qs, ss, pairs, scheme, align_type), oracle_traceback(qs, ss, pairs, scheme, align_type),
                         f"{align_type} ragged {sch}")
+
+
+@pytest.mark.parametrize("align_type,gap_model", COMBOS)
+def test_schemes_beyond_the_byte_profile(ctx, align_type, gap_model):
+    """|match + gap_open| or |mismatch + gap_open| > 127: the fill takes its compare / select form instead of the signed-byte
+    profile (the reference has no such limit); spans and CIGARs still equal ref_traceback."""
+    rng = np.random.default_rng(127)
+    for sch in ((200, -150, 100, 3), (90, -60, 70, 70), (3, -250, 5, 2)):
+        scheme = scheme_of(sch, gap_model)
+        qs, ss = [], []
+        for k in range(120):
+            q = random_codes(rng, int(rng.integers(1, 700 if k < 6 else 200)))
+            s = mutate_codes(rng, q, 0.06, 0.03, 0.03) if k % 2 else random_codes(rng, int(rng.integers(1, 700 if k < 6 else 200)))
+            if k % 9 == 0:
+                q = q.copy(); q[rng.integers(0, len(q))] = 4
+            if k % 11 == 0:
+                s = s.copy(); s[rng.integers(0, len(s))] = 4
+            qs.append(q); ss.append(s)
+        pairs = [(i, i) for i in range(len(qs))]
+        assert_tb_equal(gpu_traceback(ctx, qs, ss, pairs, scheme, align_type), oracle_traceback(qs, ss, pairs, scheme, align_type),
+                        f"{align_type}/{gap_model}/{sch}")
