@@ -21,7 +21,7 @@
 namespace wsb {
 
 template <int P, int K> constexpr size_t short16g_smem_bytes() {
-    return (size_t)2 * (K / 4 + 1) * kThreads * 16          // row m of both halves
+    return (size_t)2 * (K / 4 + 1) * (kThreads / P) * 16    // row m of both halves: the strip of the lane that owns column n
            + (size_t)(kThreads / P) * short16_qrows<P>() * 8
            + (size_t)(kThreads / P) * 4 * kShort16Raw
            + (size_t)(kThreads / P) * 16 * 4;
@@ -66,17 +66,20 @@ __device__ __forceinline__ void g16_row(const unsigned (&sel)[K], unsigned (&TA)
     h_last = hprev;
 }
 
-template <int P, int K, int GAP, bool RAGGED, int AIMM = 0, int GIMM = 0>
-__global__ void __launch_bounds__(kThreads, 4) s16_global_short_kernel(const ScoreParams prm) {
+#ifndef WSB_S16G_MINB
+#define WSB_S16G_MINB 4
+#endif
+template <int P, int K, int GAP, bool RAGGED, int AIMM = 0, int GIMM = 0, int MINB = WSB_S16G_MINB>
+__global__ void __launch_bounds__(kThreads, MINB) s16_global_short_kernel(const ScoreParams prm) {
     constexpr int GPB = kThreads / P;
     constexpr int NCH = K / 4 + 1;
     constexpr int NW = NCH * 4;
     constexpr bool MERGED = GAP == GAP_MERGED;
     static_assert(P >= 4, "lanes 0..3 of a group carry the metadata of the four sequences of a unit");
     extern __shared__ uint4 smem_dyn[];
-    uint4 (*snap)[NCH][kThreads] = reinterpret_cast<uint4 (*)[NCH][kThreads]>(smem_dyn);
+    uint4 (*snap)[NCH][GPB] = reinterpret_cast<uint4 (*)[NCH][GPB]>(smem_dyn);   // [half][quad][lane group]
     constexpr int QROWS = short16_qrows<P>();
-    uint2 (*qbuf)[QROWS] = reinterpret_cast<uint2 (*)[QROWS]>(smem_dyn + 2 * NCH * kThreads);
+    uint2 (*qbuf)[QROWS] = reinterpret_cast<uint2 (*)[QROWS]>(smem_dyn + 2 * NCH * GPB);
     uint8_t (*raw)[4][kShort16Raw] = reinterpret_cast<uint8_t (*)[4][kShort16Raw]>(&qbuf[GPB][0]);
     int (*meta)[16] = reinterpret_cast<int (*)[16]>(&raw[GPB][0][0]);
 
@@ -221,6 +224,7 @@ __global__ void __launch_bounds__(kThreads, 4) s16_global_short_kernel(const Sco
         asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(qc0), "=r"(qc1) : "r"(qaddr) : "memory");
         asm volatile("ld.shared.v2.b32 {%0, %1}, [%2+8];" : "=r"(qn0), "=r"(qn1) : "r"(qaddr) : "memory");
         int rowi = 0;   // row this lane finished last
+        const int own0 = (n[0] - 1) / K, own1 = (n[1] - 1) / K;   // lanes that own column n of either half
         // one trip: CAP = park the row in shared memory when it is row m of a half
         auto trip = [&](auto cap_tag) {
             constexpr bool CAP = decltype(cap_tag)::value;
@@ -243,10 +247,10 @@ __global__ void __launch_bounds__(kThreads, 4) s16_global_short_kernel(const Sco
                 for (int c = K; c < NW; ++c) hrow[c] = 0u;
 #pragma unroll
                 for (int v = 0; v < 2; ++v)
-                    if (rowi == m[v]) {
+                    if (rowi == m[v] && t == (v ? own1 : own0)) {   // only the lane that owns column n parks its strip
 #pragma unroll
                         for (int ch = 0; ch < NCH; ++ch)
-                            snap[v][ch][tid] = make_uint4(hrow[4 * ch], hrow[4 * ch + 1], hrow[4 * ch + 2], hrow[4 * ch + 3]);
+                            snap[v][ch][gib] = make_uint4(hrow[4 * ch], hrow[4 * ch + 1], hrow[4 * ch + 2], hrow[4 * ch + 3]);
                     }
             }
             s_t = t_last; s_h = h_last;   // sent by the caller, outside the mask
@@ -300,7 +304,7 @@ __global__ void __launch_bounds__(kThreads, 4) s16_global_short_kernel(const Sco
             if (pidx[v] < 0 || m[v] <= 0 || n[v] <= 0) continue;
             const int owner = (n[v] - 1) / K, idx = (n[v] - 1) - owner * K;
             if (t == owner) {
-                const unsigned* words = reinterpret_cast<const unsigned*>(&snap[v][idx >> 2][tid]);
+                const unsigned* words = reinterpret_cast<const unsigned*>(&snap[v][idx >> 2][gib]);
                 const int sc = half16(words[idx & 3], v);
                 prm.out_score[pidx[v]] = sc;
                 prm.out_i[pidx[v]] = m[v];
