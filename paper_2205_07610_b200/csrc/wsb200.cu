@@ -916,15 +916,16 @@ static Shape shape_of(int variant, int shape) {
     return variant == WSB_VARIANT_F16X2 ? kShapesF16[shape] : variant == WSB_VARIANT_S16X2 ? kShapesS16[shape] : kShapesI32[shape];
 }
 
-// A packed int16 short-read launch group with at most one block of (8, K) lane groups per SM runs on (16, 10) lane groups
+// A packed int16 short-read launch group of at most 1.5 blocks of (8, K) lane groups per SM runs on (16, 10) lane groups
 // instead: twice the blocks, strips half as long (WSB_S16_LAT = 0: never, 2: always; tuning aid).  Measured (B200, 150 bp,
-// kernel time): 2 000 pairs 35 -> 28 us (global linear), 48 -> 37 us (local affine); at 10 000 pairs (two blocks per SM
-// either way) the wide shape's 22 % extra instructions already lose: 54 vs 59 us.
+// kernel time, (8, 19) against (16, 10)): 2 000 pairs 35 / 28 us (global linear), 48 / 37 us (local affine); 4 700 pairs
+// 35 / 31 and 45 / 39; 6 000 pairs 40 / 36 and 52 / 48; at 10 000 pairs the wide shape's 22 % extra instructions lose:
+// 54 / 59 and 72 / 81 us.
 static int latency_shape(int shape, int64_t n_units, int max_m, int sm_count) {
     static const char* lat = getenv("WSB_S16_LAT");
     const int mode = (lat && lat[0]) ? atoi(lat) : 1;
     if (mode == 0 || max_m < 2) return shape;
-    return (mode >= 2 || n_units <= (int64_t)sm_count * (kThreads / 8)) ? 2 : shape;
+    return (mode >= 2 || n_units * 2 <= (int64_t)sm_count * 3 * (kThreads / 8)) ? 2 : shape;
 }
 
 static double padded_cost(const Shape& s, int m, int n) {
